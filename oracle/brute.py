@@ -1,0 +1,109 @@
+"""ORACLE PIN (test infrastructure only): brute-force full transport tensor on micro instances.
+
+Builds M in R_+^{L x N^(T+1)} literally as M = K ⊙ U (eq:MKU P:357-358, thm:solution P:777-781,
+node form SURVEY §8.0):
+
+    M[l, v_0, ..., v_T] = U0[l, v_0] * prod_t KW_t[v_t, v_{t+1}] * UT[l, v_T]
+
+with KW_t the dense N x N matrix exp(-C_t/eps) * W_t on arcs and 0 off the graph (C = inf).
+Projections are literal sums over all other modes (eq:proj_discrete P:319-321,
+eq:proj_discrete_bi P:469-471).  ``brute_sweep`` runs the Sinkhorn scheme of prp:sinkhorn
+(eq:sinkhorn_graph_E / _Vineq) with every projection taken from the full tensor,
+in the Gauss-Seidel order of Algorithm 2 (U0 block, W_0..W_{T-1} blocks, UT block).
+Linear domain float64: only for instances where no product under- or overflows (micro sizes).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def dense_kernel(problem, t: int, W_t: np.ndarray) -> np.ndarray:
+    """N x N matrix with exp(-C_t[a]/eps) * W_t[a] at (tail_a, head_a), 0 elsewhere."""
+    p = problem
+    K = np.zeros((p.N, p.N))
+    K[p.tail, p.head] = np.exp(-np.asarray(p.cost_t(t), float) / p.eps) * W_t
+    return K
+
+
+def full_tensor(problem, U0: np.ndarray, W: np.ndarray, UT: np.ndarray) -> np.ndarray:
+    """M with shape (L, N, ..., N) (T+1 node modes)."""
+    p = problem
+    M = U0.copy()                                   # (L, N)
+    for t in range(p.T):
+        KW = dense_kernel(p, t, W[t])
+        M = M[..., :, None] * KW.reshape((1,) * (M.ndim - 1) + KW.shape)
+    return M * UT.reshape((p.L,) + (1,) * (p.T) + (p.N,))
+
+
+def commodity_marginal(M: np.ndarray, mode: int) -> np.ndarray:
+    """P_{c,mode}(M): [L, N], summing every node mode except ``mode`` (0..T)."""
+    axes = tuple(k for k in range(1, M.ndim) if k != mode + 1)
+    return M.sum(axis=axes)
+
+
+def bimarginal(M: np.ndarray, t: int) -> np.ndarray:
+    """P_{t,t+1}(M) per commodity: [L, N, N]."""
+    axes = tuple(k for k in range(1, M.ndim) if k not in (t + 1, t + 2))
+    return M.sum(axis=axes)
+
+
+def arc_flows(problem, M: np.ndarray) -> np.ndarray:
+    """Aggregate arc flows F_t[a] = sum_l P_{t,t+1}(M^l)[tail_a, head_a]: [T, A]."""
+    p = problem
+    return np.stack([bimarginal(M, t).sum(axis=0)[p.tail, p.head] for t in range(p.T)])
+
+
+def commodity_arc_flows(problem, M: np.ndarray, t: int) -> np.ndarray:
+    p = problem
+    return bimarginal(M, t)[:, p.tail, p.head].T      # [A, L]
+
+
+def _ratio(num: np.ndarray, den: np.ndarray) -> np.ndarray:
+    """num/den with 0/0 := 0 and x/0 := +inf (x > 0)."""
+    out = np.zeros_like(num, dtype=float)
+    pos = den > 0
+    out[pos] = num[pos] / den[pos]
+    out[(~pos) & (num > 0)] = np.inf
+    return out
+
+
+class BruteState:
+    def __init__(self, problem):
+        p = problem
+        self.p = p
+        self.U0 = np.ones((p.L, p.N))
+        self.W = np.ones((p.T, p.A))
+        self.UT = (p.muT > 0).astype(float)     # Q7: all-ones on the support
+        self.sweeps = 0
+
+    def tensor(self):
+        return full_tensor(self.p, self.U0, self.W, self.UT)
+
+
+def brute_sweep(bs: BruteState) -> None:
+    """One GS sweep of eq:sinkhorn_graph with projections of the full tensor."""
+    p = bs.p
+    # U^(0,1) block: U <- U ⊙ R ./ P_{0,1}(K⊙U)   (eq:sinkhorn_graph_E)
+    P0 = commodity_marginal(bs.tensor(), 0)
+    r = _ratio(p.mu0, P0)
+    if np.isinf(r).any():
+        raise RuntimeError("infeasible source")
+    bs.U0 = bs.U0 * r
+    # u_t blocks: u <- min(u ⊙ d ./ P_t(K⊙U), 1)   (eq:sinkhorn_graph_Vineq)
+    for t in range(p.T):
+        F = arc_flows(p, bs.tensor())[t]
+        cap = np.asarray(p.cap_t(t), float)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            ratio = np.where(F > 0, cap / np.where(F > 0, F, 1.0), np.inf)
+        with np.errstate(invalid="ignore"):
+            neww = np.minimum(bs.W[t] * ratio, 1.0)
+        neww = np.where(cap == 0, 0.0, neww)
+        neww = np.where(np.isinf(cap), 1.0, neww)
+        bs.W[t] = neww
+    # U^(0,T) block
+    PT = commodity_marginal(bs.tensor(), p.T)
+    r = _ratio(p.muT, PT)
+    if np.isinf(r).any():
+        raise RuntimeError("infeasible sink")
+    bs.UT = bs.UT * r
+    bs.sweeps += 1

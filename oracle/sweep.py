@@ -1,0 +1,229 @@
+"""ORACLE (test infrastructure only): float64 log-domain Gauss-Seidel Sinkhorn sweep, node form.
+
+Transcribes SURVEY.md §8(c) steps 1-5, which follow Algorithm 2 (alg:multi_commodity, PAPER.md
+P:1085-1107) pushed through the node form of SURVEY.md §8.0:
+
+    a = log alpha  (forward messages  Psi-hat, eq:psi_hat P:1031-1036)
+    b = log beta   (backward messages Psi,     eq:psi     P:1038-1043)
+    lam0 = log U0 (U^(0,1)), lamT = log UT (U^(0,T)), omega = log W (u_t)
+
+State arrays:  lK [T, A] = -C_t/eps ; omega [T, A] ; lam0, lamT [L, N] ; a, b [T+1, N, L].
+LSE = log-sum-exp with max shift; -inf encodes an exact zero (thm:solution_extension's zero
+entries, eq:u_augment P:843-848).  No blocking, fusion or reordering beyond the algorithm: every
+step is a whole-array numpy expression over arcs and commodities.
+
+The capacity-dual update is written in Algorithm 2's own form
+    u_t <- min( d ./ ((Psi-hat_t ⊙ Psi_t ⊙ K)^T 1), 1 )
+i.e. omega_t[a] <- min(log d[a] - LSE_l(a_t[i_a,l] + lK_t[a] + b_{t+1}[j_a,l]), 0), which does not
+involve the previous W (prp:sinkhorn P:861 with u_t cancelled).  Zero conventions (SURVEY Q6/Q8,
+P:109 "0 * inf = 0"): d = +inf -> W = 1; d = 0 -> W = 0; flow-without-W = 0 and d > 0 -> W = 1;
+0/0 := 0 at the boundary scalings; x/0 with x > 0 raises OracleInfeasible.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import Callable, Optional
+
+import numpy as np
+
+NEG_INF = -np.inf
+
+
+class OracleInfeasible(RuntimeError):
+    """Boundary scaling x/0 with x > 0: a commodity's source (sink) node cannot reach any sink
+    (source) node through the current kernel."""
+
+    def __init__(self, where: str, commodity: int, node: int):
+        super().__init__(f"infeasible at {where}: commodity {commodity}, node {node}")
+        self.where, self.commodity, self.node = where, commodity, node
+
+
+def _csr(keys: np.ndarray, n: int):
+    order = np.argsort(keys, kind="stable")
+    counts = np.bincount(keys, minlength=n)
+    starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    return order, counts, starts
+
+
+def seg_lse(X: np.ndarray, seg: tuple, n: int) -> np.ndarray:
+    """out[v, :] = log sum_{a in segment v} exp(X[a, :]); empty segment -> -inf."""
+    order, counts, starts = seg
+    out = np.full((n, X.shape[1]), NEG_INF)
+    nz = counts > 0
+    if not nz.any():
+        return out
+    Xs = X[order]
+    st = starts[nz]
+    mx = np.maximum.reduceat(Xs, st, axis=0)
+    shift = np.where(np.isfinite(mx), mx, 0.0)
+    seg_of = np.repeat(np.arange(st.size), counts[nz])
+    s = np.add.reduceat(np.exp(Xs - shift[seg_of]), st, axis=0)
+    with np.errstate(divide="ignore"):
+        out[nz] = shift + np.log(s)
+    return out
+
+
+def _lse_rows(X: np.ndarray) -> np.ndarray:
+    """LSE over axis 1 of an [A, L] array; all -inf row -> -inf."""
+    mx = X.max(axis=1)
+    shift = np.where(np.isfinite(mx), mx, 0.0)
+    with np.errstate(divide="ignore"):
+        return shift + np.log(np.exp(X - shift[:, None]).sum(axis=1))
+
+
+def _log(x: np.ndarray) -> np.ndarray:
+    with np.errstate(divide="ignore"):
+        return np.log(x)
+
+
+@dataclasses.dataclass
+class OracleState:
+    problem: object
+    lK: np.ndarray      # [T, A]   log K_t = -C_t / eps           (eq K_multicommodity)
+    logd: np.ndarray    # [T, A]   log d_t (+inf free, -inf closed)
+    omega: np.ndarray   # [T, A]   log W_t <= 0
+    lam0: np.ndarray    # [L, N]   log U0
+    lamT: np.ndarray    # [L, N]   log UT
+    a: np.ndarray       # [T+1, N, L] log alpha_t (kept from the last forward pass)
+    b: np.ndarray       # [T+1, N, L] log beta_t  (from the last backward pass)
+    log_mu0: np.ndarray  # [L, N]
+    log_muT: np.ndarray  # [L, N]
+    in_seg: tuple
+    out_seg: tuple
+    sweeps: int = 0
+
+
+def oracle_init(problem) -> OracleState:
+    """Step 1-2 of SURVEY §8(c): lK = -C/eps (fp64), W = 1, UT = 1 on supp(muT) (Q7),
+    then one backward pass (Alg. 2 "Initialize ... Compute Psi_t")."""
+    p = problem
+    T, A, N, L = p.T, p.A, p.N, p.L
+    cost = np.broadcast_to(p.cost, (T, A)) if p.cost.ndim == 1 else p.cost
+    cap = np.broadcast_to(p.cap, (T, A)) if p.cap.ndim == 1 else p.cap
+    lK = -np.asarray(cost, np.float64) / float(p.eps)
+    logd = _log(np.asarray(cap, np.float64))
+    mu0 = p.mu0
+    muT = p.muT
+    st = OracleState(
+        problem=p, lK=lK, logd=logd, omega=np.zeros((T, A)),
+        lam0=np.full((L, N), NEG_INF), lamT=np.where(muT > 0, 0.0, NEG_INF),
+        a=np.full((T + 1, N, L), NEG_INF), b=np.full((T + 1, N, L), NEG_INF),
+        log_mu0=_log(mu0), log_muT=_log(muT),
+        in_seg=_csr(p.head.astype(np.int64), N), out_seg=_csr(p.tail.astype(np.int64), N))
+    backward(st)
+    return st
+
+
+def backward(st: OracleState) -> None:
+    """Backward recursion (eq:psi P:1038-1043; Alg. 2), node form:
+    b_T = lamT^T ; b_t[i,l] = LSE_{a: i_a = i}( lK_t[a] + omega_t[a] + b_{t+1}[j_a, l] )."""
+    p = st.problem
+    st.b[p.T] = st.lamT.T
+    for t in range(p.T - 1, -1, -1):
+        X = (st.lK[t] + st.omega[t])[:, None] + st.b[t + 1][p.head]
+        st.b[t] = seg_lse(X, st.out_seg, p.N)
+
+
+def _boundary(log_mu: np.ndarray, msg: np.ndarray, where: str) -> np.ndarray:
+    """U = mu ./ msg in logs: 0/0 := 0 (mu = 0 -> -inf); mu > 0 with msg = 0 -> infeasible."""
+    with np.errstate(invalid="ignore"):
+        lam = np.where(np.isfinite(log_mu), log_mu - msg.T, NEG_INF)
+    bad = np.isfinite(log_mu) & ~np.isfinite(msg.T)
+    if bad.any():
+        l, v = np.argwhere(bad)[0]
+        raise OracleInfeasible(where, int(l), int(v))
+    return lam
+
+
+def capacity_update(logd_t: np.ndarray, log_ks: np.ndarray) -> np.ndarray:
+    """Algorithm 2 line P:1093: omega = min(log d - log(K-weighted bimarginal without W), 0),
+    with d = +inf -> 0, d = 0 -> -inf, (d > 0 and flow 0) -> 0."""
+    with np.errstate(invalid="ignore"):
+        om = np.minimum(logd_t - log_ks, 0.0)
+    om = np.where(np.isposinf(logd_t), 0.0, om)
+    om = np.where(np.isneginf(logd_t), NEG_INF, om)
+    om = np.where(np.isfinite(logd_t) & np.isneginf(log_ks), 0.0, om)
+    return om
+
+
+def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None) -> None:
+    """One Gauss-Seidel sweep in Algorithm 2's order.
+
+    on_block(kind, t, mass) is called after every dual block update (kind in {"U0", "W", "UT"}),
+    with the tensor mass <K, U> at that moment, for the BCA-monotonicity pin (prp:sinkhorn)."""
+    p = st.problem
+    # a2: U^(0,1) <- R^(0,1) ./ Psi_1
+    st.lam0 = _boundary(st.log_mu0, st.b[0], "source")
+    st.a[0] = st.lam0.T
+    if on_block is not None:
+        on_block("U0", -1, float(np.exp(st.a[0] + st.b[0]).sum()))
+    # a3: forward loop
+    for t in range(p.T):
+        X = st.a[t][p.tail] + st.lK[t][:, None] + st.b[t + 1][p.head]      # [A, L], no W
+        st.omega[t] = capacity_update(st.logd[t], _lse_rows(X))
+        if on_block is not None:
+            on_block("W", t, float(np.exp(X + st.omega[t][:, None]).sum()))
+        Y = st.a[t][p.tail] + (st.lK[t] + st.omega[t])[:, None]
+        st.a[t + 1] = seg_lse(Y, st.in_seg, p.N)                           # Psi-hat_{t+1}
+    # a4: U^(0,T) <- R^(0,T) ./ Psi-hat_T
+    st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
+    if on_block is not None:
+        on_block("UT", p.T, float(np.exp(st.a[p.T] + st.lamT.T).sum()))
+    # a5: backward recompute
+    backward(st)
+    st.sweeps += 1
+
+
+def oracle_run(problem, sweeps: int) -> OracleState:
+    st = oracle_init(problem)
+    for _ in range(sweeps):
+        oracle_sweep(st)
+    return st
+
+
+def readout_commodity_flows(st: OracleState, t: int) -> np.ndarray:
+    """Per-commodity arc flow F^l_t[a] = alpha_t[i_a,l] K_t[a] W_t[a] beta_{t+1}[j_a,l]
+    (cor:proj P:1078 in node form), from the kept forward messages and the latest backward pass."""
+    p = st.problem
+    return np.exp(st.a[t][p.tail] + (st.lK[t] + st.omega[t])[:, None] + st.b[t + 1][p.head])
+
+
+def readout_flows(st: OracleState) -> tuple:
+    """(F [T, A], W [T, A]) : aggregate edge flows F_t[a] = sum_l F^l_t[a] and capacity duals."""
+    p = st.problem
+    F = np.stack([readout_commodity_flows(st, t).sum(axis=1) for t in range(p.T)])
+    return F, np.exp(st.omega)
+
+
+def dual_objective(st: OracleState, mass: float) -> float:
+    """Dual objective of thm:solution (eq:omt_multi_graph_dual P:786-788) in node form with
+    U = exp(-Lambda/eps):  Phi = -eps*mass + eps*[sum mu0*lam0 + sum muT*lamT + sum d*omega],
+    with 0 * (+-inf) = 0."""
+    p = st.problem
+    mu0, muT = p.mu0, p.muT
+    cap = np.broadcast_to(p.cap, st.omega.shape)
+    s0 = np.where(mu0 > 0, mu0 * np.where(np.isfinite(st.lam0), st.lam0, 0.0), 0.0).sum()
+    sT = np.where(muT > 0, muT * np.where(np.isfinite(st.lamT), st.lamT, 0.0), 0.0).sum()
+    fin = np.isfinite(cap) & (cap > 0)
+    sd = (np.where(fin, cap, 0.0) * np.where(fin, st.omega, 0.0)).sum()
+    return float(p.eps * (-mass + s0 + sT + sd))
+
+
+def stats(st: OracleState) -> dict:
+    """End-of-sweep statistics."""
+    p = st.problem
+    F, W = readout_flows(st)
+    cost = np.broadcast_to(p.cost, F.shape)
+    cap = np.broadcast_to(p.cap, F.shape)
+    mass = float(np.exp(st.a[p.T] + st.lamT.T).sum())
+    P0 = np.exp(st.lam0 + st.b[0].T)            # source marginal of the end-of-sweep tensor
+    PT = np.exp(st.a[p.T].T + st.lamT)          # sink marginal
+    return {
+        "mass": mass,
+        "primal": float((cost * F).sum()),
+        "dual": dual_objective(st, mass),
+        "src_mismatch": float(np.abs(P0 - p.mu0).sum()),
+        "sink_mismatch": float(np.abs(PT - p.muT).sum()),
+        "cap_violation": float(np.maximum(F - cap, 0.0)[np.isfinite(cap)].max(initial=0.0)),
+        "sweeps": st.sweeps,
+    }

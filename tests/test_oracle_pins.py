@@ -1,0 +1,358 @@
+"""Pins of the float64 log-domain oracle against things other than itself.
+
+Every test here is CPU-only (-m "not gpu").  A plausible mistake anywhere in oracle/sweep.py (a
+dropped K, a transposed message, a wrong sign in the capacity update, a wrong GS order, a wrong
+zero convention) fails at least one of: brute-force tensor projections (P1), the closed-form
+Schroedinger bridge (P2), textbook bimarginal Sinkhorn (P3), exact identities (P4), dual-ascent
+monotonicity (P5), the LP bracket (P6) and the extended-precision twins (P9).
+"""
+import numpy as np
+import pytest
+
+from oracle import (oracle_init, oracle_sweep, oracle_run, readout_flows, readout_commodity_flows,
+                    dual_objective, stats, OracleInfeasible)
+from oracle.brute import BruteState, brute_sweep, full_tensor, arc_flows, commodity_marginal
+from oracle.lp import solve_lp, count_walks, time_expanded_counts
+from oracle.twins import LinearTwin, MpTwin
+from workloads import gen, grid_problem, fig1_problem
+from tests._metrics import max_rel_err
+
+MICROS = [
+    dict(rows=2, cols=2, T=3, L=2, eps=0.5, seed=1),
+    dict(rows=2, cols=3, T=4, L=3, eps=0.7, seed=2),
+    dict(rows=2, cols=2, T=1, L=2, eps=0.4, seed=3),                                  # T = 1 (P7)
+    dict(rows=2, cols=3, T=3, L=1, eps=0.5, seed=4),                                  # L = 1 (P7)
+    dict(rows=2, cols=2, T=4, L=3, eps=0.6, seed=5, marginals="dense"),
+    dict(rows=2, cols=3, T=3, L=2, eps=0.5, seed=6, time_varying=True),
+    dict(rows=2, cols=3, T=4, L=2, eps=0.5, seed=8, closed_arcs=3, marginals="dense"),  # d = 0 arcs
+]
+
+
+def _micro(kw):
+    kw = dict(kw)
+    return grid_problem(kw.pop("rows"), kw.pop("cols"), kw.pop("T"), kw.pop("L"), kw.pop("eps"), **kw)
+
+
+# ---------------------------------------------------------------------------------------------
+# P1 brute force
+
+@pytest.mark.parametrize("kw", MICROS)
+def test_p1_structured_projections_equal_full_tensor(kw):
+    """cor:proj / thm:biproj in node form == literal sums of M = K ⊙ U (eq:proj_discrete)."""
+    p = _micro(kw)
+    st = oracle_run(p, 3)
+    M = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT))
+    F_brute = arc_flows(p, M)
+    F, W = readout_flows(st)
+    assert max_rel_err(F, F_brute, 1e-300) < 1e-12
+    for t in range(p.T):
+        from oracle.brute import commodity_arc_flows
+        assert max_rel_err(readout_commodity_flows(st, t), commodity_arc_flows(p, M, t), 1e-300) < 1e-12
+    # end-of-sweep marginals: P_{c,T} = muT exactly after a4, P_{c,0} from the new backward pass
+    assert max_rel_err(commodity_marginal(M, p.T), p.muT, 1e-300) < 1e-12
+    P0 = np.exp(st.lam0 + st.b[0].T)
+    assert max_rel_err(commodity_marginal(M, 0), P0, 1e-300) < 1e-12
+
+
+@pytest.mark.parametrize("kw", MICROS)
+def test_p1_iterates_identical_to_full_tensor_sinkhorn(kw):
+    """10 GS sweeps of prp:sinkhorn with projections of the full tensor (W*d/F form)
+    == the oracle's message-passing sweeps (P:1093 form): U0, W, UT after every sweep."""
+    p = _micro(kw)
+    st = oracle_init(p)
+    bs = BruteState(p)
+    for k in range(10):
+        oracle_sweep(st)
+        brute_sweep(bs)
+        assert max_rel_err(np.exp(st.lam0), bs.U0, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.omega), bs.W, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.lamT), bs.UT, 1e-300) < 1e-12, k
+
+
+# ---------------------------------------------------------------------------------------------
+# P2 closed-form bridge
+
+def _dense_K(p, t):
+    K = np.zeros((p.N, p.N))
+    for a in range(p.A):
+        K[p.tail[a], p.head[a]] = np.exp(-p.cost_t(t)[a] / p.eps)
+    return K
+
+
+@pytest.mark.parametrize("tv", [False, True])
+def test_p2_schroedinger_bridge_closed_form(tv):
+    """d = inf, point masses: after one sweep F^l_t[a] = m_l (PK)_{0:t}[s,i] K_t[a] (PK)_{t+1:T}[j,g]
+    / (PK)_{0:T}[s,g] (remark P:922-928: a discrete Schroedinger bridge) and it is a fixed point."""
+    p = grid_problem(3, 3, 6, 3, 0.3, seed=11, cap=None, time_varying=tv, mass=[1.0, 2.0, 0.5])
+    Ks = [_dense_K(p, t) for t in range(p.T)]
+
+    def prod(r, q):
+        P = np.eye(p.N)
+        for t in range(r, q):
+            P = P @ Ks[t]
+        return P
+
+    st = oracle_init(p)
+    for sweep in range(3):
+        oracle_sweep(st)
+        for t in range(p.T):
+            Fl = readout_commodity_flows(st, t)
+            pre, post, tot = prod(0, t), prod(t + 1, p.T), prod(0, p.T)
+            for l in range(p.L):
+                s, g = p.src[l], p.dst[l]
+                ref = p.mass[l] * pre[s, p.tail] * Ks[t][p.tail, p.head] * post[p.head, g] / tot[s, g]
+                assert max_rel_err(Fl[:, l], ref, 1e-300) < 1e-12
+
+
+# ---------------------------------------------------------------------------------------------
+# P3 textbook Sinkhorn
+
+def test_p3_textbook_bimarginal_sinkhorn():
+    """d = inf, dense mu: the GS sweep's (U0, UT) equal classical Sinkhorn scalings (u, v) for
+    the kernel Kbar = prod_t K_t (eq:omt P:305-311 regularised), iterate by iterate."""
+    p = grid_problem(3, 3, 5, 2, 0.5, seed=12, cap=None, marginals="dense")
+    Kbar = np.eye(p.N)
+    for t in range(p.T):
+        Kbar = Kbar @ _dense_K(p, t)
+    v = (p.muT > 0).astype(float)
+    st = oracle_init(p)
+    for k in range(8):
+        with np.errstate(divide="ignore", invalid="ignore"):
+            u = np.where(p.mu0 > 0, p.mu0 / (v @ Kbar.T), 0.0)
+            v = np.where(p.muT > 0, p.muT / (u @ Kbar), 0.0)
+        oracle_sweep(st)
+        assert max_rel_err(np.exp(st.lam0), u, 1e-300) < 1e-12
+        assert max_rel_err(np.exp(st.lamT), v, 1e-300) < 1e-12
+
+
+# ---------------------------------------------------------------------------------------------
+# P4 exact identities
+
+@pytest.mark.parametrize("which", ["tiny", "dense-micro", "closed-micro"])
+def test_p4_conservation_marginals_capacity(which):
+    if which == "tiny":
+        p = gen(1)
+    elif which == "dense-micro":
+        p = grid_problem(3, 4, 6, 3, 0.3, seed=13, marginals="dense")
+    else:
+        p = grid_problem(3, 3, 5, 2, 0.3, seed=15, closed_arcs=4)
+    st = oracle_init(p)
+    in_step = []
+
+    def hook(kind, t, mass):
+        if kind == "W":
+            # F_t <= d_t right after W_t's own update (prp:sinkhorn, the min(.,1) block)
+            Fl = readout_commodity_flows(st, t)  # uses a_t and W_t new, b_{t+1} old: the current tensor
+            in_step.append((t, Fl.sum(axis=1)))
+
+    for k in range(5):
+        in_step.clear()
+        oracle_sweep(st, on_block=hook)
+        for t, F in in_step:
+            cap = p.cap_t(t)
+            fin = np.isfinite(cap)
+            assert np.all(F[fin] <= cap[fin] * (1 + 1e-12) + 1e-300)
+        m = stats(st)["mass"]
+        Fagg, W = readout_flows(st)
+        assert np.all(W >= 0) and np.all(W <= 1)
+        assert np.all(Fagg >= 0)
+        # (ii) every time slice carries the whole mass
+        assert np.allclose(Fagg.sum(axis=1), m, rtol=1e-12, atol=0)
+        for t in range(1, p.T):
+            fin_prev = readout_commodity_flows(st, t - 1)
+            fout = readout_commodity_flows(st, t)
+            inflow = np.zeros((p.N, p.L))
+            outflow = np.zeros((p.N, p.L))
+            np.add.at(inflow, p.head, fin_prev)
+            np.add.at(outflow, p.tail, fout)
+            # (i) per-commodity conservation at every node and step
+            assert max_rel_err(inflow, outflow, 1e-14 * m) < 1e-11
+        # (iii) sink marginal exact after a4
+        lastin = np.zeros((p.N, p.L))
+        np.add.at(lastin, p.head, readout_commodity_flows(st, p.T - 1))
+        assert max_rel_err(lastin.T, p.muT, 1e-14) < 1e-11
+        # (iv) point masses: source marginal exact too
+        if p.is_point:
+            firstout = np.zeros((p.N, p.L))
+            np.add.at(firstout, p.tail, readout_commodity_flows(st, 0))
+            assert max_rel_err(firstout.T, p.mu0, 1e-14) < 1e-11
+        closed = np.isfinite(p.cap) & (p.cap == 0) if p.cap.ndim == 1 else None
+        if closed is not None and closed.any():
+            assert np.all(W[:, closed] == 0) and np.all(Fagg[:, closed] == 0)
+
+
+# ---------------------------------------------------------------------------------------------
+# P5 block-coordinate ascent
+
+@pytest.mark.parametrize("which", ["tiny", "micro-dense", "grid-tight"])
+def test_p5_dual_nondecreasing_after_every_block(which):
+    """prp:sinkhorn: each update is an exact block maximisation of the dual, so
+    the dual objective never decreases -- after U0, after every W_t and after UT."""
+    if which == "tiny":
+        p = gen(1)
+    elif which == "micro-dense":
+        p = grid_problem(3, 3, 5, 3, 0.3, seed=15, marginals="dense")
+    else:
+        p = grid_problem(4, 4, 8, 4, 0.2, seed=16, cap=(0.05, 0.4))
+    st = oracle_init(p)
+    vals = []
+    st_ref = st
+
+    def hook(kind, t, mass):
+        vals.append(dual_objective(st_ref, mass))
+
+    for k in range(15):
+        oracle_sweep(st, on_block=hook)
+    v = np.array(vals)
+    scale = np.abs(v).max()
+    assert np.all(np.diff(v) >= -1e-12 * scale), np.diff(v).min()
+    if which != "tiny":            # Tiny's capacities do not bind (W stays 1): dual constant
+        assert v[-1] > v[0]
+
+
+# ---------------------------------------------------------------------------------------------
+# P6 LP bracket
+
+def _converge(p, max_sweeps=20000, tol=1e-10):
+    st = oracle_init(p)
+    prev = None
+    for k in range(max_sweeps):
+        oracle_sweep(st)
+        w = st.omega.copy()
+        if prev is not None and np.nanmax(np.abs(np.exp(w) - np.exp(prev))) < tol:
+            break
+        prev = w
+    return st
+
+
+@pytest.mark.parametrize("which", ["tiny", "tight-micro"])
+def test_p6_lp_bracket_and_eps_monotone(which):
+    """thm:equiv_mc + entropic bound: 0 <= <C,F_eps> - OPT_LP <= eps m_tot log(P m_max / m_tot),
+    and <C,F_eps> is non-increasing as eps decreases.  "tight-micro" has binding caps
+    (its LP optimum exceeds the uncapacitated one)."""
+    import dataclasses
+    if which == "tiny":
+        base = gen(1)
+    else:
+        base = grid_problem(3, 3, 6, 3, 1.0, seed=35, cap=(0.3, 0.6))
+    lp = solve_lp(base)
+    assert lp["status"] == 0, "instance must be LP-feasible"
+    if which == "tiny":
+        # Tiny LP size: 3150 variables, 825 equalities, 800 capacity rows
+        assert (lp["n_var"], lp["n_eq"], lp["n_ub"]) == (3150, 825, 800)
+    else:
+        free = solve_lp(dataclasses.replace(base, cap=np.full_like(base.cap, np.inf)))
+        assert lp["opt"] > free["opt"] + 0.05
+    P = count_walks(base)
+    mtot = float(base.mass.sum())
+    mmax = float(base.mass.max())
+    prims = []
+    for eps in [1.0, 0.3, 0.1, 0.03]:
+        p = dataclasses.replace(base, eps=eps)
+        st = _converge(p)
+        s = stats(st)
+        assert s["cap_violation"] < 1e-7
+        gap = s["primal"] - lp["opt"]
+        assert -1e-7 <= gap <= eps * mtot * np.log(P * mmax / mtot) + 1e-7, (eps, gap)
+        prims.append(s["primal"])
+    assert all(prims[i + 1] <= prims[i] + 1e-9 for i in range(len(prims) - 1)), prims
+
+
+def test_p8_conditioning_probe():
+    """P8: the oracle disagrees with itself, on inputs perturbed at 1e-15 relative, by far less than
+    the fp64 parity tolerance 1e-10 after the parity sweep count -- so 1e-10 is attainable."""
+    import dataclasses
+    from tests._metrics import flow_floor
+    for base, sweeps in [(grid_problem(3, 3, 6, 3, 0.1, seed=35, cap=(0.3, 0.6)), 200), (gen(2, L=4, T=12), 30)]:
+        rng = np.random.default_rng(0)
+        pert = dataclasses.replace(base, cost=base.cost * (1 + 1e-15 * rng.uniform(-1, 1, base.cost.shape)))
+        F1, W1 = readout_flows(oracle_run(base, sweeps))
+        F2, W2 = readout_flows(oracle_run(pert, sweeps))
+        assert max_rel_err(F2, F1, flow_floor(base)) < 1e-11
+        assert max_rel_err(W2, W1, 1e-30) < 1e-11
+
+
+def test_lp_builder_on_fig1_counts():
+    """Golden: Fig. time_exp: 3 nodes, 4 edges, T=3 -> 12 vertices, 12 edges."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "fig1_time_expansion.txt")
+    gold = dict(line.split() for line in open(path) if line.strip() and not line.startswith("#"))
+    p = fig1_problem(int(gold["T"]))
+    assert p.N == int(gold["nodes"]) and p.A == int(gold["edges"])
+    assert time_expanded_counts(p) == (int(gold["expanded_vertices"]), int(gold["expanded_edges"]))
+    lp = solve_lp(p)
+    assert lp["n_var"] == int(gold["expanded_edges"]) * p.L
+
+
+def test_lp_tiny_optimum_matches_walk_enumeration():
+    """The LP itself pinned on an uncapacitated micro instance: OPT = sum_l m_l * (min-cost T-step
+    walk s_l -> g_l), by brute-force dynamic programming over walks."""
+    p = grid_problem(3, 3, 4, 3, 1.0, seed=17, cap=None)
+    lp = solve_lp(p)
+    best = 0.0
+    for l in range(p.L):
+        d = np.full(p.N, np.inf)
+        d[p.src[l]] = 0.0
+        for t in range(p.T):
+            nd = np.full(p.N, np.inf)
+            for a in range(p.A):
+                nd[p.head[a]] = min(nd[p.head[a]], d[p.tail[a]] + p.cost_t(t)[a])
+            d = nd
+        best += p.mass[l] * d[p.dst[l]]
+    assert abs(lp["opt"] - best) < 1e-9
+
+
+# ---------------------------------------------------------------------------------------------
+# P9 representation twins
+
+@pytest.mark.parametrize("which,sweeps", [("tiny", 200), ("micro-dense", 30), ("grid2-lite", 5)])
+def test_p9_longdouble_linear_twin(which, sweeps):
+    if which == "tiny":
+        p = gen(1)
+    elif which == "micro-dense":
+        p = grid_problem(3, 4, 6, 3, 0.3, seed=18, marginals="dense", closed_arcs=2)
+    else:
+        p = gen(2, L=4, T=12)
+    st = oracle_init(p)
+    tw = LinearTwin(p, np.longdouble)
+    for k in range(sweeps):
+        oracle_sweep(st)
+        tw.sweep()
+    F, W = readout_flows(st)
+    from tests._metrics import flow_floor
+    assert max_rel_err(F, tw.flows().astype(np.float64), flow_floor(p)) < 1e-12
+    assert max_rel_err(W, tw.W.astype(np.float64), 1e-30) < 1e-12
+
+
+def test_p9_mpmath_twin_micro():
+    p = grid_problem(2, 2, 3, 2, 0.5, seed=19)
+    st = oracle_init(p)
+    tw = MpTwin(p, dps=40)
+    for k in range(4):
+        oracle_sweep(st)
+        tw.sweep()
+    F, W = readout_flows(st)
+    assert max_rel_err(F, tw.flows(), 1e-300) < 1e-13
+    assert max_rel_err(W, np.array([[float(x) for x in row] for row in tw.W]), 1e-300) < 1e-13
+
+
+# ---------------------------------------------------------------------------------------------
+# conventions
+
+def test_infeasible_source_raises():
+    """x/0 with x > 0 at the boundary scaling: a sink unreachable within T steps."""
+    p = grid_problem(3, 3, 2, 1, 0.5, seed=20)
+    p.src = np.array([0], np.int32)
+    p.dst = np.array([8], np.int32)   # Manhattan distance 4 > T = 2
+    st = oracle_init(p)
+    with pytest.raises(OracleInfeasible):
+        oracle_sweep(st)
+
+
+def test_tiny_runs_200_sweeps_and_satisfies_capacities_approximately():
+    p = gen(1)
+    st = oracle_run(p, p.sweeps)
+    s = stats(st)
+    assert abs(s["mass"] - 3.0) < 1e-9
+    assert s["src_mismatch"] < 1e-6
+    assert s["cap_violation"] < 1e-3
