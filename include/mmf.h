@@ -1,0 +1,150 @@
+/*
+ * mmf.h — C ABI of the B200 (sm_100a) Sinkhorn-sweep library for entropy-regularised dynamic
+ * multi-commodity min-cost flow (Haasler, Ringh, Chen, Karlsson, arXiv:2106.14485).
+ *
+ * The library runs the hot path of the paper's Algorithm 2 (alg:multi_commodity, PAPER.md
+ * P:1085-1107) in the node form of SURVEY.md §8.0: per sweep
+ *   a2  U0 = mu0 ./ beta_0                                   (eq:sinkhorn_graph_E P:859)
+ *   a3  for t = 0..T-1:  F_t[a] = K_t[a] W_t[a] sum_l alpha_t[i_a,l] beta_{t+1}[j_a,l]   (cor:proj P:1078)
+ *                        W_t[a] <- min(W_t[a] d_t[a] / F_t[a], 1)                  (eq:sinkhorn_graph_Vineq P:861)
+ *                        alpha_{t+1}[j,:] = sum_{a->j} alpha_t[i_a,:] K_t[a] W_t[a] (eq:psi_hat P:1031-1036)
+ *   a4  UT = muT ./ alpha_T
+ *   a5  for t = T-1..0:  beta_t[i,:] = sum_{a: i_a=i} K_t[a] W_t[a] beta_{t+1}[j_a,:] (eq:psi P:1038-1043)
+ * with K_t = exp(-C_t/eps) (eq:K_multicommodity P:1010-1013).  Arcs are the directed edges plus any
+ * self-loops ("stay" arcs) the caller includes.
+ *
+ * Conventions: d = +INFINITY leaves an arc
+ * uncapacitated (W = 1 always); d = 0 closes it (W = 0); F = 0 with d > 0 gives W = 1; at the
+ * boundary scalings 0/0 := 0 and x/0 with x > 0 raises the sticky MMF_EINFEASIBLE.
+ *
+ * Numerics: messages are stored as (significand, integer binary exponent) pairs — "extended range"
+ * (SURVEY D3): fp32 significand + int16 exponent in MMF_FP32, fp64 significand + int32 exponent in
+ * MMF_FP64 — so that horizons whose log-message span exceeds the native exponent range
+ * (thousands of nats) neither underflow nor lose relative precision.  Flows are linear M-typed.
+ *
+ * Threading and ownership: one host thread per context.  All host input arrays are borrowed for the
+ * duration of the call only (copied / converted).  The CUDA stream and the workspace are borrowed
+ * for the context's lifetime.  Every call returns a status; nothing throws across the ABI.
+ * mmf_last_error() returns a context-owned string valid until the next call on that context.
+ */
+#ifndef MMF_H_
+#define MMF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mmf_ctx mmf_ctx; /* opaque */
+
+typedef enum {
+  MMF_OK = 0,
+  MMF_EVERIFY = 1,     /* reserved (mirrors SPEC S:625 exit code 1) */
+  MMF_EINVAL = 2,      /* invalid argument / validation failure at setup */
+  MMF_ENOTCONV = 3,    /* reserved for solve-to-tolerance */
+  MMF_EINFEASIBLE = 4, /* sticky: x/0 with x > 0 at a boundary scaling (a2/a4) */
+  MMF_ENOMEM = 5,      /* workspace too small / allocation failure */
+  MMF_ECUDA = 6,       /* CUDA runtime error */
+  MMF_ENCCL = 7,       /* NCCL error */
+  MMF_ESTATE = 8,      /* call out of order */
+  MMF_ERANGE = 9       /* sticky: extended exponent overflow, or NaN in a flow */
+} mmf_status;
+
+typedef enum { MMF_FP64 = 0, MMF_FP32 = 1 } mmf_prec;
+
+typedef struct {
+  int64_t sweeps;        /* sweeps run since mmf_init */
+  double mass;           /* <K, U> of the end-of-sweep tensor = sum_{l,j} alpha_T beta_T (all ranks) */
+  double src_mismatch;   /* sum_{l,i} |U0 beta_0 - mu0|   (end-of-sweep source marginal error, L1) */
+  double sink_mismatch;  /* sum_{l,j} |alpha_T UT - muT| (≈ 0 right after a4) */
+  double cap_violation;  /* max_{t,a} (F_t[a] - d_t[a])_+ over capacitated arcs */
+  double dual;           /* thm:solution dual objective: eps*(-mass + <mu0,log U0> + <muT,log UT> + <d,log W>) */
+  double primal;         /* sum_{t,a} C_t[a] F_t[a] */
+} mmf_stats;
+
+/* Create a context on CUDA device `device` with message precision `prec`.  `cuda_stream` is a
+ * borrowed cudaStream_t (NULL = legacy default stream); all device work is ordered on it. */
+mmf_status mmf_create(mmf_ctx** out, int device, mmf_prec prec, void* cuda_stream);
+
+/* Graph: N nodes, n_arcs arcs (tail[a] -> head[a]), node ids in [0, N).  Self-loops allowed (one
+ * per node at most); duplicate (tail, head) pairs are rejected.  Arc a's position in
+ * these arrays is the "user arc order" of every [T][A] input and output below. */
+mmf_status mmf_set_graph(mmf_ctx* ctx, int32_t N, int64_t n_arcs, const int32_t* tail, const int32_t* head);
+
+/* Costs C_t[a] (finite, any sign) and eps > 0.  time_varying = 0: cost is [n_arcs] for every step;
+ * 1: cost is [T][n_arcs] (per-step topology/cost).  K = exp(-C/eps) is formed in fp64. */
+mmf_status mmf_set_costs(mmf_ctx* ctx, int32_t T, double eps, const double* cost, int time_varying);
+
+/* Capacities d_t[a] >= 0, +INFINITY = uncapacitated, 0 = closed; layout as for costs. */
+mmf_status mmf_set_capacity(mmf_ctx* ctx, const double* cap, int time_varying);
+
+/* Dense source / sink distributions of commodities [l_begin, l_begin + l_count) of L_global:
+ * mu0, muT are [l_count][N] row-major, >= 0, with equal per-commodity masses (rel. 1e-12). */
+mmf_status mmf_set_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count,
+                             const double* mu0, const double* muT);
+
+/* Point-mass commodities: commodity l moves mass[l] > 0 from node src[l] to node dst[l]. */
+mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count,
+                                   const int32_t* src, const int32_t* dst, const double* mass);
+
+/* Device bytes needed once graph, costs, capacities and marginals are set. */
+mmf_status mmf_workspace_bytes(const mmf_ctx* ctx, size_t* bytes);
+
+/* Borrowed device workspace (>= mmf_workspace_bytes, 256-byte aligned).  If never called,
+ * mmf_init allocates an owned workspace with cudaMalloc. */
+mmf_status mmf_set_workspace(mmf_ctx* ctx, void* dptr, size_t bytes);
+
+/* Multi-GPU commodity sharding: join an NCCL communicator of `nranks` ranks from a 128-byte
+ * ncclUniqueId (bootstrapped by the caller, e.g. torch.distributed).  Every rank must then make the
+ * same calls with identical graph / cost / capacity arrays and its own commodity slice; the
+ * per-step edge flows F_t are all-reduced (sum) over NVLink before the capacity-dual update.
+ * The communicator is owned by the context.  Returns MMF_ENCCL if NCCL is unavailable. */
+mmf_status mmf_attach_nccl(mmf_ctx* ctx, const void* unique_id128, int nranks, int rank);
+
+/* Options (call before mmf_init): key "graph" (1 = capture one sweep as a CUDA graph, default 1),
+ * "reorder" (1 = locality node reordering, default 1), "profile" (1 = per-kernel CUDA-event timing). */
+mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);
+
+/* W = 1, UT = 1 on supp(muT), one backward pass (Alg. 2 "Initialize").  Async. */
+mmf_status mmf_init(mmf_ctx* ctx);
+
+/* Enqueue n full sweeps (a2..a5) on the stream.  Async; errors surface at mmf_sync / read_*. */
+mmf_status mmf_sweep(mmf_ctx* ctx, int32_t n);
+
+/* Wait for the stream; report sticky device errors (MMF_EINFEASIBLE / MMF_ERANGE, with the first
+ * (commodity, node) in mmf_last_error) and NCCL async errors. */
+mmf_status mmf_sync(mmf_ctx* ctx);
+
+/* End-of-sweep edge flows F_t[a] = sum over ALL commodities (all ranks), fp64, [T][n_arcs] in user
+ * arc order: one extra forward pass without updates (cor:proj P:1078-1079).  Synchronises. */
+mmf_status mmf_read_edge_flows(mmf_ctx* ctx, double* out_TxA);
+
+/* Capacity duals W_t[a] in [0, 1], fp64, [T][n_arcs] user arc order (values below 2^-1074 read 0). */
+mmf_status mmf_read_cap_duals(mmf_ctx* ctx, double* out_TxA);
+
+/* Statistics of the end-of-sweep state (see mmf_stats).  Synchronises. */
+mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out);
+
+/* Kernel accounting: launches (cumulative) and, with option "profile", device milliseconds per
+ * kernel kind.  kinds: 0 bwd_step, 1 fwd_flow, 2 fwd_reduce, 3 fwd_update, 4 boundary, 5 other,
+ * 6 fwd_fused.  n = array length (<= 8). */
+mmf_status mmf_read_kernel_stats(mmf_ctx* ctx, int64_t* launches, double* ms, int n);
+
+/* Algorithmic bytes moved by one sweep (SURVEY §8(d) byte model, with this build's element size). */
+mmf_status mmf_sweep_bytes(const mmf_ctx* ctx, double* bytes_total, double* bytes_per_kind, int n);
+
+/* Free owned resources (not the borrowed stream / workspace).  Safe on NULL. */
+mmf_status mmf_destroy(mmf_ctx* ctx);
+
+/* Last error message of this context (or of the last failed mmf_create if ctx is NULL). */
+const char* mmf_last_error(const mmf_ctx* ctx);
+
+/* Library version string. */
+const char* mmf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MMF_H_ */

@@ -1,0 +1,96 @@
+"""Convenience wrapper: one ``Solver`` = one mmf context (include/mmf.h), marshalling only.
+
+PyTorch supplies the device workspace (a uint8 tensor) and the CUDA stream; every computation of the
+sweep happens in libmmf.so.  Commodity sharding: pass ``l_begin``/``l_count`` and an NCCL unique id.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+
+class Solver:
+    def __init__(self, problem, prec: Optional[str] = None, device: int = 0, stream=None, graph: bool = True,
+                 reorder: bool = True, profile: bool = False, l_begin: int = 0, l_count: Optional[int] = None,
+                 nccl_uid: Optional[bytes] = None, nranks: int = 1, rank: int = 0):
+        import torch  # device memory + streams only
+
+        self.p = problem
+        prec = prec or getattr(problem, "prec", "fp64")
+        self.prec = prec
+        self.device = device
+        self.torch_device = torch.device("cuda", device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.torch_device)
+        self.stream = stream
+        handle = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self.ctx = L.mmf_create(device, L.MMF_FP32 if prec == "fp32" else L.MMF_FP64, handle)
+        self._ws = None
+        try:
+            L.mmf_set_option(self.ctx, "graph", int(graph))
+            L.mmf_set_option(self.ctx, "reorder", int(reorder))
+            L.mmf_set_option(self.ctx, "profile", int(profile))
+            self.upload(problem, l_begin, l_count)
+            if nccl_uid is not None:
+                L.mmf_attach_nccl(self.ctx, nccl_uid, nranks, rank)
+            nbytes = L.mmf_workspace_bytes(self.ctx)
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.torch_device)
+            L.mmf_set_workspace(self.ctx, self._ws.data_ptr(), nbytes)
+            L.mmf_init(self.ctx)
+        except Exception:
+            self.close()
+            raise
+
+    def upload(self, p, l_begin: int = 0, l_count: Optional[int] = None):
+        l_count = p.L - l_begin if l_count is None else l_count
+        self.l_begin, self.l_count = l_begin, l_count
+        L.mmf_set_graph(self.ctx, p.N, p.tail, p.head)
+        L.mmf_set_costs(self.ctx, p.T, p.eps, p.cost, p.cost.ndim == 2)
+        L.mmf_set_capacity(self.ctx, p.cap, p.cap.ndim == 2)
+        sl = slice(l_begin, l_begin + l_count)
+        if p.is_point:
+            L.mmf_set_point_marginals(self.ctx, p.L, l_begin, p.src[sl], p.dst[sl], p.mass[sl])
+        else:
+            L.mmf_set_marginals(self.ctx, p.L, l_begin, p.mu0[sl], p.muT[sl])
+
+    def sweep(self, n: int = 1):
+        L.mmf_sweep(self.ctx, n)
+
+    def sync(self):
+        L.mmf_sync(self.ctx)
+
+    def edge_flows(self) -> np.ndarray:
+        return L.mmf_read_edge_flows(self.ctx, self.p.T, self.p.A)
+
+    def cap_duals(self) -> np.ndarray:
+        return L.mmf_read_cap_duals(self.ctx, self.p.T, self.p.A)
+
+    def stats(self) -> dict:
+        return L.mmf_read_stats(self.ctx)
+
+    def kernel_stats(self) -> dict:
+        return L.mmf_read_kernel_stats(self.ctx)
+
+    def sweep_bytes(self):
+        return L.mmf_sweep_bytes(self.ctx)
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            L.mmf_destroy(self.ctx)
+            self.ctx = None
+        self._ws = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

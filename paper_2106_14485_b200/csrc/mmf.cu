@@ -1,0 +1,1100 @@
+// mmf.cu — host engine and C ABI (include/mmf.h) of the B200 Sinkhorn-sweep library.
+//
+// Host side: validation (SURVEY §8(b) error conventions), locality node reordering, CSR build,
+// fp64 -> extended-range conversion of K = exp(-C/eps) and the marginals, workspace layout, the
+// sweep launch sequence (a2, T x forward step, a4, T x backward step) optionally
+// captured once as a CUDA graph, readouts and statistics, and the NCCL per-step all-reduce of the
+// edge flows for commodity sharding.
+#include "../../include/mmf.h"
+#include "kernels.cuh"
+
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace mmf;
+
+// ------------------------------------------------------------------------------------------------
+// NCCL, resolved at run time from the process (torch loads libnccl.so.2) so the library itself has
+// no link-time NCCL dependency.
+namespace {
+typedef int ncclResult_t_;
+typedef void* ncclComm_t_;
+struct NcclUid {
+  char internal[128];
+};
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t_ (*CommInitRank)(ncclComm_t_*, int, NcclUid, int) = nullptr;
+  ncclResult_t_ (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t_, cudaStream_t) = nullptr;
+  ncclResult_t_ (*CommDestroy)(ncclComm_t_) = nullptr;
+  ncclResult_t_ (*CommGetAsyncError)(ncclComm_t_, ncclResult_t_*) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t_) = nullptr;
+};
+// ncclDataType_t / ncclRedOp_t values (stable NCCL ABI)
+constexpr int NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
+
+NcclApi& nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.ok = api.CommInitRank && api.AllReduce && api.CommDestroy && api.CommGetAsyncError;
+  return api;
+}
+
+std::string g_create_error;
+
+enum Kind { K_BWD = 0, K_FLOW = 1, K_REDUCE = 2, K_UPDATE = 3, K_BOUNDARY = 4, K_OTHER = 5, K_FUSED = 6, K_NKINDS = 8 };
+
+}  // namespace
+
+struct mmf_ctx {
+  int device = 0;
+  mmf_prec prec = MMF_FP64;
+  cudaStream_t stream = nullptr;  // borrowed
+  cudaStream_t priv = nullptr;    // owned (graph capture / launch)
+  std::string err;
+
+  // ---- host problem, user order
+  int N = 0;
+  int64_t A = 0;
+  std::vector<int> tail, head;
+  int T = 0;
+  double eps = 0;
+  std::vector<double> cost;
+  bool cost_tv = false, have_cost = false;
+  std::vector<double> cap;
+  bool cap_tv = false, have_cap = false;
+  int Lg = 0, l_begin = 0, L = 0;
+  bool point = false, have_marg = false;
+  std::vector<double> mu0, muT, mass;
+  std::vector<int> src, dst;
+
+  // ---- options
+  bool opt_graph = true, opt_reorder = true, opt_profile = false;
+
+  // ---- derived
+  int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
+  std::vector<int> newid;       // user node -> internal
+  std::vector<int> int_of_arc;  // user arc -> internal arc
+
+  // ---- device
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  bool ws_owned = false;
+  DevPtrs dp{};
+  bool inited = false;
+  int64_t sweeps = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t graph_launch_tally[K_NKINDS] = {};
+  cudaEvent_t ev_user = nullptr, ev_priv = nullptr;
+
+  // ---- NCCL
+  ncclComm_t_ comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // ---- accounting
+  int64_t launches[K_NKINDS] = {};
+  double ms[K_NKINDS] = {};
+  bool capturing = false;
+  struct Prof {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Prof> prof;
+  std::vector<cudaEvent_t> ev_pool;
+
+  size_t sm() const { return prec == MMF_FP32 ? sizeof(float) : sizeof(double); }
+  size_t se() const { return prec == MMF_FP32 ? sizeof(int16_t) : sizeof(int32_t); }
+};
+
+namespace {
+
+mmf_status fail(mmf_ctx* c, mmf_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return fail(ctx, MMF_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------------
+// reverse Cuthill-McKee over the undirected support of the arcs: nodes adjacent in the graph get
+// nearby internal ids, so a step's gathers of alpha/beta rows hit L2 (and the same DRAM pages).
+std::vector<int> rcm_newid(int N, const std::vector<int>& tail, const std::vector<int>& head) {
+  std::vector<int> deg(N, 0);
+  for (size_t a = 0; a < tail.size(); ++a)
+    if (tail[a] != head[a]) {
+      deg[tail[a]]++;
+      deg[head[a]]++;
+    }
+  std::vector<int64_t> ptr(N + 1, 0);
+  for (int v = 0; v < N; ++v) ptr[v + 1] = ptr[v] + deg[v];
+  std::vector<int> adj(ptr[N]);
+  std::vector<int64_t> fill(ptr.begin(), ptr.end() - 1);
+  for (size_t a = 0; a < tail.size(); ++a)
+    if (tail[a] != head[a]) {
+      adj[fill[tail[a]]++] = head[a];
+      adj[fill[head[a]]++] = tail[a];
+    }
+  std::vector<int> byDeg(N);
+  std::iota(byDeg.begin(), byDeg.end(), 0);
+  std::stable_sort(byDeg.begin(), byDeg.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+  std::vector<char> seen(N, 0);
+  std::vector<int> order;
+  order.reserve(N);
+  std::vector<int> nb;
+  for (int s : byDeg) {
+    if (seen[s]) continue;
+    seen[s] = 1;
+    size_t head_q = order.size();
+    order.push_back(s);
+    while (head_q < order.size()) {
+      int v = order[head_q++];
+      nb.clear();
+      for (int64_t k = ptr[v]; k < ptr[v + 1]; ++k)
+        if (!seen[adj[k]]) {
+          seen[adj[k]] = 1;
+          nb.push_back(adj[k]);
+        }
+      std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+      order.insert(order.end(), nb.begin(), nb.end());
+    }
+  }
+  std::vector<int> newid(N);
+  for (int k = 0; k < N; ++k) newid[order[N - 1 - k]] = k;
+  return newid;
+}
+
+// fp64 -> (significand, binary exponent) with significand in [1, 2); 0 -> (0, EZERO)
+inline void to_xf(double x, double& m, int& e) {
+  if (!(x > 0)) {
+    m = 0;
+    e = EZERO;
+    return;
+  }
+  int ex;
+  double fr = std::frexp(x, &ex);  // x = fr 2^ex, fr in [0.5, 1)
+  m = fr * 2.0;
+  e = ex - 1;
+}
+
+// K = exp(lk) with lk = -C/eps formed in fp64 (Q20): x = lk log2(e) split into floor + fraction
+inline void k_to_xf(double lk, double& m, int& e) {
+  long double x = (long double)lk * 1.4426950408889634073599246810018921L;
+  long double fl = std::floor(x);
+  m = (double)std::exp2(x - fl);
+  e = (int)fl;
+  if (m >= 2.0) {
+    m *= 0.5;
+    e += 1;
+  }
+}
+
+struct Layout {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  }
+};
+
+void derive_shapes(mmf_ctx* c) {
+  c->Lp = ((c->L + 31) / 32) * 32;
+  int chunks = c->Lp / 32;
+  int w = 8;
+  while (chunks % w) w >>= 1;
+  c->block = 32 * w;
+  c->G = c->Lp / c->block;
+}
+
+// walk the workspace layout; assign pointers when base != nullptr
+size_t layout(mmf_ctx* c, char* base) {
+  Layout L;
+  const size_t A = (size_t)c->A, N = (size_t)c->N, T = (size_t)c->T, Lp = (size_t)c->Lp;
+  const size_t TK = c->cost_tv ? T : 1, TC = c->cap_tv ? T : 1;
+  const size_t sm = c->sm(), se = c->se();
+  DevPtrs& p = c->dp;
+  auto at = [&](size_t o) -> char* { return base ? base + o : nullptr; };
+  p.tail = (const int*)at(L.take(A * 4));
+  p.in_ptr = (const int*)at(L.take((N + 1) * 4));
+  p.out_ptr = (const int*)at(L.take((N + 1) * 4));
+  p.out_arc = (const int*)at(L.take(A * 4));
+  p.out_head = (const int*)at(L.take(A * 4));
+  p.Km = at(L.take(TK * A * sm));
+  p.Ke = (const int*)at(L.take(TK * A * 4));
+  p.dcap = at(L.take(TC * A * sm));
+  p.Wm = at(L.take(T * A * sm));
+  p.We = (int*)at(L.take(T * A * 4));
+  p.am = at(L.take(2 * N * Lp * sm));
+  p.ae = at(L.take(2 * N * Lp * se));
+  p.bm = at(L.take((T + 1) * N * Lp * sm));
+  p.be = at(L.take((T + 1) * N * Lp * se));
+  p.u0m = at(L.take(N * Lp * sm));
+  p.u0e = at(L.take(N * Lp * se));
+  if (!c->point) {
+    p.mu0m = at(L.take(N * Lp * sm));
+    p.mu0e = at(L.take(N * Lp * se));
+    p.muTm = at(L.take(N * Lp * sm));
+    p.muTe = at(L.take(N * Lp * se));
+    p.psrc = p.pdst = nullptr;
+    p.pmass = nullptr;
+  } else {
+    p.mu0m = p.mu0e = p.muTm = p.muTe = nullptr;
+    p.psrc = (const int*)at(L.take((size_t)c->L * 4));
+    p.pdst = (const int*)at(L.take((size_t)c->L * 4));
+    p.pmass = (const double*)at(L.take((size_t)c->L * 8));
+  }
+  p.part = at(L.take((size_t)c->G * A * sm));
+  p.Fsum = at(L.take(A * sm));
+  p.Fout = at(L.take(T * A * sm));
+  p.err = (unsigned*)at(L.take(8));
+  p.errloc = (unsigned long long*)at(L.take(8));
+  p.stats = (double*)at(L.take(8 * 8));
+  p.N = c->N;
+  p.Lp = c->Lp;
+  p.L = c->L;
+  p.A = (int)c->A;
+  p.T = c->T;
+  p.TK = (int)TK;
+  p.TC = (int)TC;
+  p.G = c->G;
+  p.maxdeg_in = c->maxdeg_in;
+  return L.off;
+}
+
+bool ready_for_layout(const mmf_ctx* c) { return c->N > 0 && c->have_cost && c->have_cap && c->have_marg; }
+
+// ------------------------------------------------------------------------------------------------
+// launch helpers (accounting + optional per-kernel event timing)
+
+cudaEvent_t get_event(mmf_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct LaunchScope {
+  mmf_ctx* c;
+  int kind;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  LaunchScope(mmf_ctx* cc, int k, cudaStream_t ss) : c(cc), kind(k), s(ss) {
+    if (c->opt_profile && !c->capturing) {
+      a = get_event(c);
+      b = get_event(c);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~LaunchScope() {
+    if (c->capturing)
+      c->graph_launch_tally[kind]++;
+    else
+      c->launches[kind]++;
+    if (a) {
+      cudaEventRecord(b, s);
+      c->prof.push_back({kind, a, b});
+    }
+  }
+};
+
+inline unsigned grid1d(size_t n, int bs) {
+  size_t g = (n + bs - 1) / bs;
+  if (g > 148u * 16u) g = 148u * 16u;
+  return (unsigned)std::max<size_t>(g, 1);
+}
+
+template <class T_> struct Eng {
+  typedef typename T_::M M;
+  typedef typename T_::E E;
+
+  static void zero_slot(mmf_ctx* c, cudaStream_t s, void* pm, void* pe) {
+    LaunchScope ls(c, K_BOUNDARY, s);
+    size_t n = (size_t)c->N * c->Lp;
+    k_zero<T_><<<grid1d(n, 256), 256, 0, s>>>((M*)pm, (E*)pe, n);
+  }
+
+  static void boundary(mmf_ctx* c, cudaStream_t s, int which) {
+    const DevPtrs& p = c->dp;
+    if (!c->point) {
+      LaunchScope ls(c, K_BOUNDARY, s);
+      size_t n = (size_t)c->N * c->Lp;
+      k_boundary_dense<T_><<<grid1d(n, 256), 256, 0, s>>>(p, which);
+    } else {
+      if (which == 0) {
+        zero_slot(c, s, p.am, p.ae);
+        zero_slot(c, s, p.u0m, p.u0e);
+      } else {
+        zero_slot(c, s, (M*)p.bm + (size_t)c->T * c->N * c->Lp, (E*)p.be + (size_t)c->T * c->N * c->Lp);
+      }
+      LaunchScope ls(c, K_BOUNDARY, s);
+      k_boundary_point<T_><<<(c->L + 127) / 128, 128, 0, s>>>(p, which);
+    }
+  }
+
+  static void bwd_pass(mmf_ctx* c, cudaStream_t s) {
+    dim3 grid(c->N, c->G);
+    for (int t = c->T - 1; t >= 0; --t) {
+      LaunchScope ls(c, K_BWD, s);
+      k_bwd<T_><<<grid, c->block, 0, s>>>(c->dp, t);
+    }
+  }
+
+  // forward step t; readout = 1: flows of all arcs into Fout[t], no dual update
+  static mmf_status fwd_step(mmf_ctx* ctx, cudaStream_t s, int t, int readout) {
+    mmf_ctx* c = ctx;
+    const DevPtrs& p = c->dp;
+    dim3 grid(c->N, c->G);
+    {
+      LaunchScope ls(c, K_FLOW, s);
+      k_flow<T_><<<grid, c->block, 0, s>>>(p, t, readout ? 0 : 1);
+    }
+    const unsigned ga = (unsigned)((c->A + 255) / 256);
+    if (readout) {
+      M* out = (M*)p.Fout + (size_t)t * c->A;
+      {
+        LaunchScope ls(c, K_REDUCE, s);
+        k_reduce<T_><<<ga, 256, 0, s>>>(p, t, out, 0);
+      }
+      if (c->comm) {
+        int r = nccl_api().AllReduce(out, out, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
+                                     NCCL_SUM, c->comm, s);
+        if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
+      }
+    } else if (c->comm) {
+      {
+        LaunchScope ls(c, K_REDUCE, s);
+        k_reduce<T_><<<ga, 256, 0, s>>>(p, t, (M*)p.Fsum, 1);
+      }
+      int r = nccl_api().AllReduce(p.Fsum, p.Fsum, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
+                                   NCCL_SUM, c->comm, s);
+      if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
+      LaunchScope ls(c, K_REDUCE, s);
+      k_dual<T_><<<ga, 256, 0, s>>>(p, t);
+    } else {
+      LaunchScope ls(c, K_REDUCE, s);
+      k_reduce<T_><<<ga, 256, 0, s>>>(p, t, nullptr, 2);
+    }
+    {
+      LaunchScope ls(c, K_UPDATE, s);
+      k_spmm_fwd<T_><<<grid, c->block, 0, s>>>(p, t);
+    }
+    return MMF_OK;
+  }
+
+  static mmf_status enqueue_sweep(mmf_ctx* c, cudaStream_t s) {
+    boundary(c, s, 0);  // a2
+    for (int t = 0; t < c->T; ++t) {
+      mmf_status st = fwd_step(c, s, t, 0);  // a3
+      if (st != MMF_OK) return st;
+    }
+    boundary(c, s, 1);  // a4
+    bwd_pass(c, s);     // a5
+    return MMF_OK;
+  }
+
+  static mmf_status init_device(mmf_ctx* ctx, cudaStream_t s) {
+    mmf_ctx* c = ctx;
+    const DevPtrs& p = c->dp;
+    {
+      LaunchScope ls(c, K_OTHER, s);
+      size_t n = (size_t)c->T * c->A;
+      k_init_w<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
+    }
+    if (!c->point) {
+      LaunchScope ls(c, K_OTHER, s);
+      size_t n = (size_t)c->N * c->Lp;
+      k_init_ut_dense<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
+    } else {
+      zero_slot(c, s, (M*)p.bm + (size_t)c->T * c->N * c->Lp, (E*)p.be + (size_t)c->T * c->N * c->Lp);
+      LaunchScope ls(c, K_OTHER, s);
+      k_init_ut_point<T_><<<(c->L + 127) / 128, 128, 0, s>>>(p);
+    }
+    bwd_pass(c, s);
+    return MMF_OK;
+  }
+
+  static mmf_status readout(mmf_ctx* ctx, cudaStream_t s) {
+    mmf_ctx* c = ctx;
+    const DevPtrs& p = c->dp;
+    const size_t n = (size_t)c->N * c->Lp;
+    CU(cudaMemcpyAsync(p.am, p.u0m, n * sizeof(M), cudaMemcpyDeviceToDevice, s));
+    CU(cudaMemcpyAsync(p.ae, p.u0e, n * sizeof(E), cudaMemcpyDeviceToDevice, s));
+    for (int t = 0; t < c->T; ++t) {
+      mmf_status st = fwd_step(c, s, t, 1);
+      if (st != MMF_OK) return st;
+    }
+    return MMF_OK;
+  }
+
+  static mmf_status stats(mmf_ctx* ctx, cudaStream_t s) {
+    mmf_ctx* c = ctx;
+    const DevPtrs& p = c->dp;
+    CU(cudaMemsetAsync(p.stats, 0, 8 * sizeof(double), s));
+    {
+      LaunchScope ls(c, K_OTHER, s);
+      size_t n = (size_t)c->N * c->Lp;
+      k_stats_nodes<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
+    }
+    {
+      LaunchScope ls(c, K_OTHER, s);
+      size_t n = (size_t)c->T * c->A;
+      k_stats_arcs<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
+    }
+    return MMF_OK;
+  }
+};
+
+template <class F> mmf_status dispatch(mmf_ctx* c, F f) {
+  if (c->prec == MMF_FP32) return f(Eng<TrF32>());
+  return f(Eng<TrF64>());
+}
+
+mmf_status check_sticky(mmf_ctx* ctx) {
+  mmf_ctx* c = ctx;
+  unsigned err = 0;
+  unsigned long long loc = 0;
+  CU(cudaMemcpy(&err, c->dp.err, sizeof(err), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(&loc, c->dp.errloc, sizeof(loc), cudaMemcpyDeviceToHost));
+  if (err) {
+    int commodity = (int)((loc >> 32) & 0x7fffffffull);
+    int node_int = (int)(loc & 0xffffffffull);
+    int node_user = node_int;
+    if (node_int >= 0 && node_int < c->N && (err & (ERR_INFEASIBLE | ERR_RANGE)))
+      for (int v = 0; v < c->N; ++v)
+        if (c->newid[v] == node_int) {
+          node_user = v;
+          break;
+        }
+    char buf[256];
+    if (err & ERR_INFEASIBLE) {
+      snprintf(buf, sizeof buf, "infeasible boundary scaling (x/0, x>0): commodity %d, node %d",
+               commodity + c->l_begin, node_user);
+      return fail(c, MMF_EINFEASIBLE, buf);
+    }
+    if (err & ERR_RANGE) {
+      snprintf(buf, sizeof buf, "extended exponent overflow: commodity %d, node %d", commodity + c->l_begin, node_user);
+      return fail(c, MMF_ERANGE, buf);
+    }
+    snprintf(buf, sizeof buf, "NaN/inf edge flow (internal arc %d)", node_int);
+    return fail(c, MMF_ERANGE, buf);
+  }
+  if (c->comm) {
+    ncclResult_t_ r = 0;
+    nccl_api().CommGetAsyncError(c->comm, &r);
+    if (r != 0) return fail(c, MMF_ENCCL, "NCCL async error");
+  }
+  return MMF_OK;
+}
+
+mmf_status collect_profile(mmf_ctx* ctx) {
+  mmf_ctx* c = ctx;
+  for (auto& pr : c->prof) {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, pr.a, pr.b));
+    c->ms[pr.kind] += ms;
+    c->ev_pool.push_back(pr.a);
+    c->ev_pool.push_back(pr.b);
+  }
+  c->prof.clear();
+  return MMF_OK;
+}
+
+// build internal structures and upload (called by mmf_init)
+mmf_status finalize(mmf_ctx* ctx) {
+  mmf_ctx* c = ctx;
+  const int N = c->N;
+  const int64_t A = c->A;
+  c->newid = c->opt_reorder ? rcm_newid(N, c->tail, c->head) : std::vector<int>();
+  if (!c->opt_reorder) {
+    c->newid.resize(N);
+    std::iota(c->newid.begin(), c->newid.end(), 0);
+  }
+  std::vector<int> it(A), ih(A);
+  for (int64_t a = 0; a < A; ++a) {
+    it[a] = c->newid[c->tail[a]];
+    ih[a] = c->newid[c->head[a]];
+  }
+  std::vector<int64_t> ord(A);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return ih[x] != ih[y] ? ih[x] < ih[y] : it[x] < it[y]; });
+  c->int_of_arc.assign(A, 0);
+  std::vector<int> h_tail(A), h_inptr(N + 1, 0), h_outptr(N + 1, 0), h_outarc(A), h_outhead(A);
+  for (int64_t k = 0; k < A; ++k) {
+    c->int_of_arc[ord[k]] = (int)k;
+    h_tail[k] = it[ord[k]];
+    h_inptr[ih[ord[k]] + 1]++;
+  }
+  for (int v = 0; v < N; ++v) h_inptr[v + 1] += h_inptr[v];
+  c->maxdeg_in = 0;
+  for (int v = 0; v < N; ++v) c->maxdeg_in = std::max(c->maxdeg_in, h_inptr[v + 1] - h_inptr[v]);
+  std::vector<int64_t> ordo(A);
+  std::iota(ordo.begin(), ordo.end(), 0);  // internal arc ids
+  std::vector<int> ihead_int(A);
+  for (int64_t k = 0; k < A; ++k) ihead_int[k] = ih[ord[k]];
+  std::sort(ordo.begin(), ordo.end(), [&](int64_t x, int64_t y) {
+    return h_tail[x] != h_tail[y] ? h_tail[x] < h_tail[y] : ihead_int[x] < ihead_int[y];
+  });
+  for (int64_t k = 0; k < A; ++k) {
+    h_outarc[k] = (int)ordo[k];
+    h_outhead[k] = ihead_int[ordo[k]];
+    h_outptr[h_tail[ordo[k]] + 1]++;
+  }
+  for (int v = 0; v < N; ++v) h_outptr[v + 1] += h_outptr[v];
+
+  derive_shapes(c);
+  size_t need = layout(c, nullptr);
+  if (!c->ws) {
+    void* d = nullptr;
+    if (cudaMalloc(&d, need) != cudaSuccess) return fail(c, MMF_ENOMEM, "cudaMalloc of the workspace failed");
+    c->ws = d;
+    c->ws_bytes = need;
+    c->ws_owned = true;
+  } else if (c->ws_bytes < need) {
+    return fail(c, MMF_ENOMEM, "workspace smaller than mmf_workspace_bytes");
+  }
+  layout(c, (char*)c->ws);
+  DevPtrs& p = c->dp;
+  cudaStream_t s = c->stream;
+
+  CU(cudaMemcpyAsync((void*)p.tail, h_tail.data(), A * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.in_ptr, h_inptr.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.out_ptr, h_outptr.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.out_arc, h_outarc.data(), A * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.out_head, h_outhead.data(), A * 4, cudaMemcpyHostToDevice, s));
+
+  const bool f32 = c->prec == MMF_FP32;
+  const size_t sm = c->sm(), se = c->se();
+  // K = exp(-C/eps) (fp64 on host), capacities
+  const int TK = c->cost_tv ? c->T : 1, TC = c->cap_tv ? c->T : 1;
+  std::vector<char> hKm((size_t)TK * A * sm), hdc((size_t)TC * A * sm);
+  std::vector<int> hKe((size_t)TK * A);
+  for (int t = 0; t < TK; ++t)
+    for (int64_t a = 0; a < A; ++a) {
+      double m;
+      int e;
+      k_to_xf(-c->cost[(size_t)t * A + a] / c->eps, m, e);
+      size_t k = (size_t)t * A + c->int_of_arc[a];
+      if (f32)
+        ((float*)hKm.data())[k] = (float)m;
+      else
+        ((double*)hKm.data())[k] = m;
+      hKe[k] = e;
+    }
+  for (int t = 0; t < TC; ++t)
+    for (int64_t a = 0; a < A; ++a) {
+      double d = c->cap[(size_t)t * A + a];
+      size_t k = (size_t)t * A + c->int_of_arc[a];
+      if (f32)
+        ((float*)hdc.data())[k] = (float)d;
+      else
+        ((double*)hdc.data())[k] = d;
+    }
+  CU(cudaMemcpyAsync((void*)p.Km, hKm.data(), hKm.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.Ke, hKe.data(), hKe.size() * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.dcap, hdc.data(), hdc.size(), cudaMemcpyHostToDevice, s));
+
+  // marginals
+  std::vector<char> h0, h0e, hT, hTe;
+  std::vector<int> hs, hd;
+  if (!c->point) {
+    const size_t n = (size_t)N * c->Lp;
+    h0.assign(n * sm, 0);
+    hT.assign(n * sm, 0);
+    h0e.assign(n * se, 0);
+    hTe.assign(n * se, 0);
+    for (int l = 0; l < c->Lp; ++l)
+      for (int v = 0; v < N; ++v) {
+        size_t k = (size_t)c->newid[v] * c->Lp + l;
+        double m0 = 0, mT = 0;
+        int e0 = EZERO, eT = EZERO;
+        if (l < c->L) {
+          to_xf(c->mu0[(size_t)l * N + v], m0, e0);
+          to_xf(c->muT[(size_t)l * N + v], mT, eT);
+        }
+        if (f32) {
+          ((float*)h0.data())[k] = (float)m0;
+          ((float*)hT.data())[k] = (float)mT;
+          ((int16_t*)h0e.data())[k] = (int16_t)e0;
+          ((int16_t*)hTe.data())[k] = (int16_t)eT;
+        } else {
+          ((double*)h0.data())[k] = m0;
+          ((double*)hT.data())[k] = mT;
+          ((int32_t*)h0e.data())[k] = e0;
+          ((int32_t*)hTe.data())[k] = eT;
+        }
+      }
+    CU(cudaMemcpyAsync((void*)p.mu0m, h0.data(), h0.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)p.mu0e, h0e.data(), h0e.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)p.muTm, hT.data(), hT.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)p.muTe, hTe.data(), hTe.size(), cudaMemcpyHostToDevice, s));
+  } else {
+    hs.resize(c->L);
+    hd.resize(c->L);
+    for (int l = 0; l < c->L; ++l) {
+      hs[l] = c->newid[c->src[l]];
+      hd[l] = c->newid[c->dst[l]];
+    }
+    CU(cudaMemcpyAsync((void*)p.psrc, hs.data(), c->L * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)p.pdst, hd.data(), c->L * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)p.pmass, c->mass.data(), c->L * 8, cudaMemcpyHostToDevice, s));
+  }
+  CU(cudaMemsetAsync(p.err, 0, 8, s));
+  CU(cudaMemsetAsync(p.errloc, 0, 8, s));
+  // host staging buffers die at return: wait for the copies
+  CU(cudaStreamSynchronize(s));
+  return MMF_OK;
+}
+
+}  // namespace
+
+// ================================================================================================
+// C ABI
+
+extern "C" {
+
+const char* mmf_version(void) { return "mmf 0.1 (sm_100a, XF f32/i16 + f64/i32)"; }
+
+const char* mmf_last_error(const mmf_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_error.c_str(); }
+
+mmf_status mmf_create(mmf_ctx** out, int device, mmf_prec prec, void* cuda_stream) {
+  if (!out) {
+    g_create_error = "out is NULL";
+    return MMF_EINVAL;
+  }
+  *out = nullptr;
+  if (prec != MMF_FP32 && prec != MMF_FP64) {
+    g_create_error = "unknown precision";
+    return MMF_EINVAL;
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    g_create_error = "no such CUDA device";
+    return MMF_ECUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) {
+    g_create_error = "cudaSetDevice failed";
+    return MMF_ECUDA;
+  }
+  mmf_ctx* c = new mmf_ctx();
+  c->device = device;
+  c->prec = prec;
+  c->stream = (cudaStream_t)cuda_stream;
+  if (cudaStreamCreateWithFlags(&c->priv, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_priv, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    g_create_error = "stream/event creation failed";
+    return MMF_ECUDA;
+  }
+  *out = c;
+  return MMF_OK;
+}
+
+mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
+  if (!ctx || !key) return MMF_EINVAL;
+  std::string k(key);
+  if (k == "graph")
+    ctx->opt_graph = value != 0;
+  else if (k == "profile")
+    ctx->opt_profile = value != 0;
+  else if (k == "reorder") {
+    if (ctx->inited) return fail(ctx, MMF_ESTATE, "reorder must be set before mmf_init");
+    ctx->opt_reorder = value != 0;
+  } else
+    return fail(ctx, MMF_EINVAL, "unknown option " + k);
+  return MMF_OK;
+}
+
+mmf_status mmf_set_graph(mmf_ctx* ctx, int32_t N, int64_t n_arcs, const int32_t* tail, const int32_t* head) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "graph already initialised");
+  if (N < 1) return fail(ctx, MMF_EINVAL, "N must be >= 1");
+  if (n_arcs < 1 || n_arcs > (int64_t)0x7fffffff) return fail(ctx, MMF_EINVAL, "n_arcs out of range");
+  if (!tail || !head) return fail(ctx, MMF_EINVAL, "tail/head NULL");
+  std::vector<int64_t> key(n_arcs);
+  for (int64_t a = 0; a < n_arcs; ++a) {
+    if (tail[a] < 0 || tail[a] >= N || head[a] < 0 || head[a] >= N)
+      return fail(ctx, MMF_EINVAL, "arc " + std::to_string(a) + ": node id out of range");
+    key[a] = (int64_t)tail[a] * N + head[a];
+  }
+  std::sort(key.begin(), key.end());
+  for (int64_t a = 1; a < n_arcs; ++a)
+    if (key[a] == key[a - 1]) return fail(ctx, MMF_EINVAL, "duplicate (tail, head) arc");
+  ctx->N = N;
+  ctx->A = n_arcs;
+  ctx->tail.assign(tail, tail + n_arcs);
+  ctx->head.assign(head, head + n_arcs);
+  ctx->have_cost = ctx->have_cap = false;
+  return MMF_OK;
+}
+
+mmf_status mmf_set_costs(mmf_ctx* ctx, int32_t T, double eps, const double* cost, int time_varying) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
+  if (ctx->N == 0) return fail(ctx, MMF_ESTATE, "mmf_set_graph first");
+  if (T < 1) return fail(ctx, MMF_EINVAL, "T must be >= 1");
+  if (!(eps > 0) || !std::isfinite(eps)) return fail(ctx, MMF_EINVAL, "eps must be finite and > 0");
+  if (!cost) return fail(ctx, MMF_EINVAL, "cost NULL");
+  const size_t n = (size_t)(time_varying ? T : 1) * ctx->A;
+  for (size_t k = 0; k < n; ++k)
+    if (!std::isfinite(cost[k])) return fail(ctx, MMF_EINVAL, "non-finite cost");
+  ctx->T = T;
+  ctx->eps = eps;
+  ctx->cost.assign(cost, cost + n);
+  ctx->cost_tv = time_varying != 0;
+  ctx->have_cost = true;
+  if (ctx->have_cap && ctx->cap_tv && ctx->cap.size() != (size_t)T * ctx->A) ctx->have_cap = false;
+  return MMF_OK;
+}
+
+mmf_status mmf_set_capacity(mmf_ctx* ctx, const double* cap, int time_varying) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
+  if (!ctx->have_cost) return fail(ctx, MMF_ESTATE, "mmf_set_costs first");
+  if (!cap) return fail(ctx, MMF_EINVAL, "cap NULL");
+  const size_t n = (size_t)(time_varying ? ctx->T : 1) * ctx->A;
+  for (size_t k = 0; k < n; ++k)
+    if (!(cap[k] >= 0)) return fail(ctx, MMF_EINVAL, "capacity < 0 or NaN");
+  ctx->cap.assign(cap, cap + n);
+  ctx->cap_tv = time_varying != 0;
+  ctx->have_cap = true;
+  return MMF_OK;
+}
+
+static mmf_status check_slice(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count) {
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
+  if (ctx->N == 0) return fail(ctx, MMF_ESTATE, "mmf_set_graph first");
+  if (L_global < 1 || l_count < 1 || l_begin < 0 || l_begin + l_count > L_global)
+    return fail(ctx, MMF_EINVAL, "bad commodity slice");
+  return MMF_OK;
+}
+
+mmf_status mmf_set_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count, const double* mu0,
+                             const double* muT) {
+  if (!ctx) return MMF_EINVAL;
+  mmf_status st = check_slice(ctx, L_global, l_begin, l_count);
+  if (st != MMF_OK) return st;
+  if (!mu0 || !muT) return fail(ctx, MMF_EINVAL, "mu0/muT NULL");
+  const int N = ctx->N;
+  for (int l = 0; l < l_count; ++l) {
+    double s0 = 0, sT = 0;
+    for (int v = 0; v < N; ++v) {
+      double a = mu0[(size_t)l * N + v], b = muT[(size_t)l * N + v];
+      if (!(a >= 0) || !(b >= 0) || !std::isfinite(a) || !std::isfinite(b))
+        return fail(ctx, MMF_EINVAL, "marginal entries must be finite and >= 0");
+      s0 += a;
+      sT += b;
+    }
+    if (std::fabs(s0 - sT) > 1e-12 * std::max(s0, sT))
+      return fail(ctx, MMF_EINVAL, "commodity " + std::to_string(l + l_begin) + ": mass imbalance (S:112)");
+  }
+  ctx->Lg = L_global;
+  ctx->l_begin = l_begin;
+  ctx->L = l_count;
+  ctx->point = false;
+  ctx->mu0.assign(mu0, mu0 + (size_t)l_count * N);
+  ctx->muT.assign(muT, muT + (size_t)l_count * N);
+  ctx->have_marg = true;
+  return MMF_OK;
+}
+
+mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count,
+                                   const int32_t* src, const int32_t* dst, const double* mass) {
+  if (!ctx) return MMF_EINVAL;
+  mmf_status st = check_slice(ctx, L_global, l_begin, l_count);
+  if (st != MMF_OK) return st;
+  if (!src || !dst || !mass) return fail(ctx, MMF_EINVAL, "src/dst/mass NULL");
+  for (int l = 0; l < l_count; ++l) {
+    if (src[l] < 0 || src[l] >= ctx->N || dst[l] < 0 || dst[l] >= ctx->N)
+      return fail(ctx, MMF_EINVAL, "point marginal node out of range");
+    if (!(mass[l] > 0) || !std::isfinite(mass[l])) return fail(ctx, MMF_EINVAL, "mass must be finite and > 0");
+  }
+  ctx->Lg = L_global;
+  ctx->l_begin = l_begin;
+  ctx->L = l_count;
+  ctx->point = true;
+  ctx->src.assign(src, src + l_count);
+  ctx->dst.assign(dst, dst + l_count);
+  ctx->mass.assign(mass, mass + l_count);
+  ctx->have_marg = true;
+  return MMF_OK;
+}
+
+mmf_status mmf_workspace_bytes(const mmf_ctx* cctx, size_t* bytes) {
+  if (!cctx || !bytes) return MMF_EINVAL;
+  mmf_ctx* ctx = const_cast<mmf_ctx*>(cctx);
+  if (!ready_for_layout(ctx)) return fail(ctx, MMF_ESTATE, "graph, costs, capacity and marginals must be set");
+  DevPtrs saved = ctx->dp;
+  int mdi = ctx->maxdeg_in;
+  derive_shapes(ctx);
+  *bytes = layout(ctx, nullptr);
+  ctx->dp = saved;
+  ctx->maxdeg_in = mdi;
+  return MMF_OK;
+}
+
+mmf_status mmf_set_workspace(mmf_ctx* ctx, void* dptr, size_t bytes) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
+  if (!dptr || ((uintptr_t)dptr & 255)) return fail(ctx, MMF_EINVAL, "workspace must be non-NULL and 256-byte aligned");
+  if (ctx->ws_owned) {
+    cudaFree(ctx->ws);
+    ctx->ws_owned = false;
+  }
+  ctx->ws = dptr;
+  ctx->ws_bytes = bytes;
+  return MMF_OK;
+}
+
+mmf_status mmf_attach_nccl(mmf_ctx* ctx, const void* unique_id128, int nranks, int rank) {
+  if (!ctx || !unique_id128) return MMF_EINVAL;
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "attach NCCL before mmf_init");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, MMF_EINVAL, "bad nranks/rank");
+  NcclApi& api = nccl_api();
+  if (!api.ok) return fail(ctx, MMF_ENCCL, "libnccl.so.2 not found in the process");
+  NcclUid uid;
+  memcpy(uid.internal, unique_id128, 128);
+  ncclComm_t_ comm = nullptr;
+  int r = api.CommInitRank(&comm, nranks, uid, rank);
+  if (r != 0)
+    return fail(ctx, MMF_ENCCL,
+                std::string("ncclCommInitRank: ") + (api.GetErrorString ? api.GetErrorString(r) : "error"));
+  ctx->comm = comm;
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return MMF_OK;
+}
+
+mmf_status mmf_init(mmf_ctx* ctx) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
+  if (!ready_for_layout(ctx)) return fail(ctx, MMF_ESTATE, "graph, costs, capacity and marginals must be set");
+  CU(cudaSetDevice(ctx->device));
+  mmf_status st = finalize(ctx);
+  if (st != MMF_OK) return st;
+  st = dispatch(ctx, [&](auto eng) { return decltype(eng)::init_device(ctx, ctx->stream); });
+  if (st != MMF_OK) return st;
+  CU(cudaGetLastError());
+  ctx->inited = true;
+  ctx->sweeps = 0;
+  return MMF_OK;
+}
+
+mmf_status mmf_sweep(mmf_ctx* ctx, int32_t n) {
+  if (!ctx) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  if (n < 0) return fail(ctx, MMF_EINVAL, "n < 0");
+  if (n == 0) return MMF_OK;
+  CU(cudaSetDevice(ctx->device));
+  const bool use_graph = ctx->opt_graph && !ctx->opt_profile;
+  if (!use_graph) {
+    for (int k = 0; k < n; ++k) {
+      mmf_status st = dispatch(ctx, [&](auto eng) { return decltype(eng)::enqueue_sweep(ctx, ctx->stream); });
+      if (st != MMF_OK) return st;
+    }
+    CU(cudaGetLastError());
+    ctx->sweeps += n;
+    return MMF_OK;
+  }
+  if (!ctx->gexec) {
+    ctx->capturing = true;
+    std::fill(ctx->graph_launch_tally, ctx->graph_launch_tally + K_NKINDS, 0);
+    cudaError_t e = cudaStreamBeginCapture(ctx->priv, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+      ctx->capturing = false;
+      return fail(ctx, MMF_ECUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+    }
+    mmf_status st = dispatch(ctx, [&](auto eng) { return decltype(eng)::enqueue_sweep(ctx, ctx->priv); });
+    cudaGraph_t g = nullptr;
+    e = cudaStreamEndCapture(ctx->priv, &g);
+    ctx->capturing = false;
+    if (st != MMF_OK) return st;
+    if (e != cudaSuccess) return fail(ctx, MMF_ECUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+    ctx->graph = g;
+    CU(cudaGraphInstantiate(&ctx->gexec, g, 0));
+  }
+  CU(cudaEventRecord(ctx->ev_user, ctx->stream));
+  CU(cudaStreamWaitEvent(ctx->priv, ctx->ev_user, 0));
+  for (int k = 0; k < n; ++k) {
+    CU(cudaGraphLaunch(ctx->gexec, ctx->priv));
+    for (int q = 0; q < K_NKINDS; ++q) ctx->launches[q] += ctx->graph_launch_tally[q];
+  }
+  CU(cudaEventRecord(ctx->ev_priv, ctx->priv));
+  CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_priv, 0));
+  ctx->sweeps += n;
+  return MMF_OK;
+}
+
+mmf_status mmf_sync(mmf_ctx* ctx) {
+  if (!ctx) return MMF_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->stream));
+  CU(cudaGetLastError());
+  if (!ctx->inited) return MMF_OK;
+  mmf_status st = collect_profile(ctx);
+  if (st != MMF_OK) return st;
+  return check_sticky(ctx);
+}
+
+mmf_status mmf_read_edge_flows(mmf_ctx* ctx, double* out) {
+  if (!ctx || !out) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  CU(cudaSetDevice(ctx->device));
+  mmf_status st = dispatch(ctx, [&](auto eng) { return decltype(eng)::readout(ctx, ctx->stream); });
+  if (st != MMF_OK) return st;
+  st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  const size_t TA = (size_t)ctx->T * ctx->A;
+  std::vector<char> h(TA * ctx->sm());
+  CU(cudaMemcpy(h.data(), ctx->dp.Fout, h.size(), cudaMemcpyDeviceToHost));
+  const int64_t A = ctx->A;
+  for (int t = 0; t < ctx->T; ++t)
+    for (int64_t a = 0; a < A; ++a) {
+      size_t k = (size_t)t * A + ctx->int_of_arc[a];
+      out[(size_t)t * A + a] = ctx->prec == MMF_FP32 ? (double)((float*)h.data())[k] : ((double*)h.data())[k];
+    }
+  return MMF_OK;
+}
+
+mmf_status mmf_read_cap_duals(mmf_ctx* ctx, double* out) {
+  if (!ctx || !out) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  mmf_status st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  const size_t TA = (size_t)ctx->T * ctx->A;
+  std::vector<char> hm(TA * ctx->sm());
+  std::vector<int> he(TA);
+  CU(cudaMemcpy(hm.data(), ctx->dp.Wm, hm.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(he.data(), ctx->dp.We, TA * 4, cudaMemcpyDeviceToHost));
+  const int64_t A = ctx->A;
+  for (int t = 0; t < ctx->T; ++t)
+    for (int64_t a = 0; a < A; ++a) {
+      size_t k = (size_t)t * A + ctx->int_of_arc[a];
+      double m = ctx->prec == MMF_FP32 ? (double)((float*)hm.data())[k] : ((double*)hm.data())[k];
+      out[(size_t)t * A + a] = m == 0 ? 0.0 : std::ldexp(m, he[k]);
+    }
+  return MMF_OK;
+}
+
+mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {
+  if (!ctx || !out) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  const size_t TA = (size_t)ctx->T * ctx->A;
+  std::vector<double> F(TA);
+  mmf_status st = mmf_read_edge_flows(ctx, F.data());  // also leaves alpha_T of the end-of-sweep state
+  if (st != MMF_OK) return st;
+  st = dispatch(ctx, [&](auto eng) { return decltype(eng)::stats(ctx, ctx->stream); });
+  if (st != MMF_OK) return st;
+  if (ctx->comm) {
+    int r = nccl_api().AllReduce(ctx->dp.stats, ctx->dp.stats, 5, NCCL_FLOAT64, NCCL_SUM, ctx->comm, ctx->stream);
+    if (r != 0) return fail(ctx, MMF_ENCCL, "ncclAllReduce(stats) failed");
+  }
+  st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  double s[8];
+  CU(cudaMemcpy(s, ctx->dp.stats, sizeof s, cudaMemcpyDeviceToHost));
+  double primal = 0, viol = 0;
+  const int64_t A = ctx->A;
+  for (int t = 0; t < ctx->T; ++t)
+    for (int64_t a = 0; a < A; ++a) {
+      const double f = F[(size_t)t * A + a];
+      primal += ctx->cost[(ctx->cost_tv ? (size_t)t * A : 0) + a] * f;
+      const double d = ctx->cap[(ctx->cap_tv ? (size_t)t * A : 0) + a];
+      if (std::isfinite(d)) viol = std::max(viol, f - d);
+    }
+  out->sweeps = ctx->sweeps;
+  out->mass = s[0];
+  out->src_mismatch = s[1];
+  out->sink_mismatch = s[2];
+  out->cap_violation = viol;
+  out->dual = ctx->eps * (-s[0] + s[3] + s[4] + s[5]);
+  out->primal = primal;
+  return MMF_OK;
+}
+
+mmf_status mmf_read_kernel_stats(mmf_ctx* ctx, int64_t* launches, double* ms, int n) {
+  if (!ctx) return MMF_EINVAL;
+  mmf_status st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  for (int k = 0; k < n && k < K_NKINDS; ++k) {
+    if (launches) launches[k] = ctx->launches[k];
+    if (ms) ms[k] = ctx->ms[k];
+  }
+  return MMF_OK;
+}
+
+mmf_status mmf_sweep_bytes(const mmf_ctx* ctx, double* total, double* per_kind, int n) {
+  if (!ctx) return MMF_EINVAL;
+  // SURVEY §8(d) byte model with B_e = significand + exponent bytes, true L (not padded):
+  //   bwd step : read beta_{t+1}, write beta_t            = 2 N L B_e + arc data
+  //   fwd flow : read alpha_t, beta_{t+1}                 = 2 N L B_e
+  //   fwd spmm : read alpha_t, write alpha_{t+1}          = 2 N L B_e
+  // (a fused forward kernel needs 3 N L B_e: alpha_t once, beta_{t+1}, alpha_{t+1})
+  const double Be = (double)(ctx->sm() + ctx->se());
+  const double NL = (double)ctx->N * ctx->L;
+  const double arcs = (double)ctx->A * (ctx->sm() + 4) * 2;  // K and W significand + exponent
+  double k[K_NKINDS] = {};
+  k[K_BWD] = ctx->T * (2 * NL * Be + arcs);
+  k[K_FLOW] = ctx->T * (2 * NL * Be + arcs);
+  k[K_UPDATE] = ctx->T * (2 * NL * Be + arcs);
+  k[K_REDUCE] = ctx->T * ((double)ctx->G * ctx->A * ctx->sm() + arcs);
+  k[K_BOUNDARY] = ctx->point ? 2 * NL * Be : 6 * NL * Be;
+  k[K_FUSED] = ctx->T * (3 * NL * Be + arcs);
+  double tot = k[K_BWD] + k[K_FLOW] + k[K_UPDATE] + k[K_REDUCE] + k[K_BOUNDARY];
+  if (total) *total = tot;
+  for (int q = 0; q < n && q < K_NKINDS; ++q)
+    if (per_kind) per_kind[q] = k[q];
+  return MMF_OK;
+}
+
+mmf_status mmf_destroy(mmf_ctx* ctx) {
+  if (!ctx) return MMF_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream || ctx->priv) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->priv);
+  }
+  if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+  if (ctx->graph) cudaGraphDestroy(ctx->graph);
+  for (auto& pr : ctx->prof) {
+    cudaEventDestroy(pr.a);
+    cudaEventDestroy(pr.b);
+  }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->ev_user) cudaEventDestroy(ctx->ev_user);
+  if (ctx->ev_priv) cudaEventDestroy(ctx->ev_priv);
+  if (ctx->comm) nccl_api().CommDestroy(ctx->comm);
+  if (ctx->ws_owned) cudaFree(ctx->ws);
+  if (ctx->priv) cudaStreamDestroy(ctx->priv);
+  delete ctx;
+  return MMF_OK;
+}
+
+}  // extern "C"

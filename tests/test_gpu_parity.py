@@ -1,0 +1,134 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the float64 oracle, element by element.
+
+Tolerances are BASELINE.json north_star's: max relative error 1e-10 on edge flows and capacity
+duals in fp64 mode, 1e-4 in fp32 mode (metric: SURVEY §8(c) Q11, tests/_metrics.py).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle_run, readout_flows, stats as oracle_stats
+from workloads import gen, grid_problem
+from tests._metrics import max_rel_err, flow_floor, W_FLOOR
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp64": 1e-10, "fp32": 1e-4}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2106_14485_b200.build import build
+    build()
+
+
+def run_gpu(p, sweeps, prec, **kw):
+    from paper_2106_14485_b200 import Solver
+    with Solver(p, prec=prec, **kw) as s:
+        s.sweep(sweeps)
+        s.sync()
+        F, W = s.edge_flows(), s.cap_duals()
+        st = s.stats()
+    return F, W, st
+
+
+def run_oracle(p, sweeps):
+    st = oracle_run(p, sweeps)
+    F, W = readout_flows(st)
+    return F, W, oracle_stats(st)
+
+
+def assert_parity(p, sweeps, prec, **kw):
+    Fo, Wo, so = run_oracle(p, sweeps)
+    Fg, Wg, sg = run_gpu(p, sweeps, prec, **kw)
+    ef = max_rel_err(Fg, Fo, flow_floor(p))
+    ew = max_rel_err(Wg, Wo, W_FLOOR)
+    assert ef < TOL[prec] and ew < TOL[prec], (p.name, prec, ef, ew)
+    assert abs(sg["mass"] - so["mass"]) <= 10 * TOL[prec] * abs(so["mass"])
+    return ef, ew
+
+
+MICROS = [
+    dict(rows=2, cols=2, T=3, L=2, eps=0.5, seed=1),
+    dict(rows=2, cols=3, T=4, L=3, eps=0.7, seed=2),
+    dict(rows=2, cols=2, T=1, L=2, eps=0.4, seed=3),
+    dict(rows=2, cols=3, T=3, L=1, eps=0.5, seed=4),
+    dict(rows=2, cols=2, T=4, L=3, eps=0.6, seed=5, marginals="dense"),
+    dict(rows=2, cols=3, T=3, L=2, eps=0.5, seed=6, time_varying=True),
+    dict(rows=2, cols=3, T=4, L=2, eps=0.5, seed=8, closed_arcs=3, marginals="dense"),
+]
+
+
+def _micro(kw):
+    kw = dict(kw)
+    return grid_problem(kw.pop("rows"), kw.pop("cols"), kw.pop("T"), kw.pop("L"), kw.pop("eps"), **kw)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("kw", MICROS)
+def test_micro_parity(kw, prec):
+    assert_parity(_micro(kw), 10, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_tiny_config1(prec):
+    p = gen(1)
+    assert_parity(p, p.sweeps, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+@pytest.mark.parametrize("L,marg", [(37, "point"), (300, "point"), (45, "dense"), (1, "dense")])
+def test_ragged_and_multi_group(L, marg, prec):
+    """L not a multiple of the warp width (ragged tail) and L spanning several commodity groups."""
+    p = grid_problem(6, 7, 9, L, 0.2, seed=21, cap=(0.3, 1.5), marginals=marg)
+    assert_parity(p, 8, prec)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_tight_capacities_long_run(prec):
+    p = grid_problem(5, 5, 12, 6, 0.1, seed=22, cap=(0.1, 0.5))
+    assert_parity(p, 40, prec)
+
+
+def test_graph_capture_bitwise_equal_to_stream_launches():
+    p = grid_problem(5, 6, 8, 20, 0.2, seed=23)
+    F1, W1, _ = run_gpu(p, 5, "fp32", graph=True)
+    F2, W2, _ = run_gpu(p, 5, "fp32", graph=False)
+    assert np.array_equal(F1, F2) and np.array_equal(W1, W2)
+
+
+def test_reorder_invisible():
+    p = grid_problem(6, 6, 8, 12, 0.2, seed=24)
+    F1, W1, _ = run_gpu(p, 6, "fp64", reorder=True)
+    F2, W2, _ = run_gpu(p, 6, "fp64", reorder=False)
+    assert max_rel_err(F1, F2, flow_floor(p)) < 1e-12 and max_rel_err(W1, W2, W_FLOOR) < 1e-12
+
+
+def test_infeasible_is_sticky_error():
+    from paper_2106_14485_b200 import MMFError
+    p = grid_problem(3, 3, 2, 1, 0.5, seed=20)
+    p.src = np.array([0], np.int32)
+    p.dst = np.array([8], np.int32)
+    with pytest.raises(MMFError) as e:
+        run_gpu(p, 1, "fp64")
+    assert e.value.name == "MMF_EINFEASIBLE"
+
+
+def test_validation_errors():
+    import dataclasses
+    from paper_2106_14485_b200 import MMFError, Solver
+    p = grid_problem(3, 3, 4, 2, 0.5, seed=25)
+    bad = [
+        dataclasses.replace(p, eps=0.0),
+        dataclasses.replace(p, cap=np.where(np.isfinite(p.cap), -1.0, p.cap)),
+        dataclasses.replace(p, tail=np.r_[p.tail, p.tail[:1]], head=np.r_[p.head, p.head[:1]],
+                            cost=np.r_[p.cost, p.cost[:1]], cap=np.r_[p.cap, p.cap[:1]]),
+        dataclasses.replace(p, mass=None, src=None, dst=None, mu0_dense=p.mu0, muT_dense=p.muT * 1.5),
+        dataclasses.replace(p, cost=np.where(p.tail == p.head, np.nan, p.cost)),
+    ]
+    for q in bad:
+        with pytest.raises(MMFError) as e:
+            Solver(q, prec="fp64")
+        assert e.value.name == "MMF_EINVAL"
