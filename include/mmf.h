@@ -103,6 +103,9 @@ mmf_status mmf_set_workspace(mmf_ctx* ctx, void* dptr, size_t bytes);
  * The communicator is owned by the context.  Returns MMF_ENCCL if NCCL is unavailable. */
 mmf_status mmf_attach_nccl(mmf_ctx* ctx, const void* unique_id128, int nranks, int rank);
 
+/* Fill out128 with a fresh ncclUniqueId (call on one rank, then broadcast the 128 bytes). */
+mmf_status mmf_nccl_unique_id(void* out128);
+
 /* Options (call before mmf_init): key "graph" (1 = capture one sweep as a CUDA graph, default 1),
  * "reorder" (1 = locality node reordering, default 1), "profile" (1 = per-kernel CUDA-event timing). */
 mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);

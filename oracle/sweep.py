@@ -7,10 +7,11 @@ P:1085-1107) pushed through the node form of SURVEY.md §8.0:
     b = log beta   (backward messages Psi,     eq:psi     P:1038-1043)
     lam0 = log U0 (U^(0,1)), lamT = log UT (U^(0,T)), omega = log W (u_t)
 
-State arrays:  lK [T, A] = -C_t/eps ; omega [T, A] ; lam0, lamT [L, N] ; a, b [T+1, N, L].
+State arrays:  lK [T, A] = -C_t/eps ; omega [T, A] ; lam0, lamT [L, N] ; a, b [T+1, L, N].
 LSE = log-sum-exp with max shift; -inf encodes an exact zero (thm:solution_extension's zero
 entries, eq:u_augment P:843-848).  No blocking, fusion or reordering beyond the algorithm: every
-step is a whole-array numpy expression over arcs and commodities.
+step is a whole-array numpy expression over arcs and commodities (segment sums over the arcs
+of a node are a sparse 0/1 incidence-matrix product, a library primitive).
 
 The capacity-dual update is written in Algorithm 2's own form
     u_t <- min( d ./ ((Psi-hat_t ⊙ Psi_t ⊙ K)^T 1), 1 )
@@ -25,6 +26,7 @@ import dataclasses
 from typing import Callable, Optional
 
 import numpy as np
+import scipy.sparse as sp
 
 NEG_INF = -np.inf
 
@@ -38,37 +40,46 @@ class OracleInfeasible(RuntimeError):
         self.where, self.commodity, self.node = where, commodity, node
 
 
-def _csr(keys: np.ndarray, n: int):
+def _segments(keys: np.ndarray, n: int):
+    """Segment structure of arcs grouped by ``keys`` (head for in-arcs, tail for out-arcs):
+    arc order sorted by key, per-node counts, start offsets, and the 0/1 incidence matrix S [n, A]
+    with S[v, a] = 1 iff keys[a] = v (used as the segment sum, a plain sparse matmul)."""
     order = np.argsort(keys, kind="stable")
     counts = np.bincount(keys, minlength=n)
     starts = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
-    return order, counts, starts
+    S = sp.csr_matrix((np.ones(keys.size), (keys[order], np.arange(keys.size))), shape=(n, keys.size))
+    # ELL table of each segment's (sorted) arc positions, padded with A (an appended -inf column),
+    # for the segment max
+    D = int(counts.max()) if n else 0
+    ell = np.full((D, n), keys.size, np.int64)
+    pos = np.arange(keys.size) - starts[keys[order]]
+    ell[pos, keys[order]] = np.arange(keys.size)
+    return order, counts, starts, S, ell
 
 
-def seg_lse(X: np.ndarray, seg: tuple, n: int) -> np.ndarray:
-    """out[v, :] = log sum_{a in segment v} exp(X[a, :]); empty segment -> -inf."""
-    order, counts, starts = seg
-    out = np.full((n, X.shape[1]), NEG_INF)
-    nz = counts > 0
-    if not nz.any():
-        return out
-    Xs = X[order]
-    st = starts[nz]
-    mx = np.maximum.reduceat(Xs, st, axis=0)
+def seg_lse(X: np.ndarray, seg: tuple) -> np.ndarray:
+    """out[l, v] = log sum_{a in segment v} exp(X[l, a]) for X [L, A] whose arcs are already in
+    segment order; empty segment -> -inf.  Max-shifted per (l, v)."""
+    order, counts, starts, S, ell = seg
+    n = counts.size
+    Xp = np.concatenate([X, np.full((X.shape[0], 1), NEG_INF)], axis=1)
+    mx = np.full((X.shape[0], n), NEG_INF)
+    for k in range(ell.shape[0]):
+        np.maximum(mx, Xp[:, ell[k]], out=mx)
     shift = np.where(np.isfinite(mx), mx, 0.0)
-    seg_of = np.repeat(np.arange(st.size), counts[nz])
-    s = np.add.reduceat(np.exp(Xs - shift[seg_of]), st, axis=0)
+    E = np.exp(X - np.repeat(shift, counts, axis=1))
+    s = (S @ E.T).T
     with np.errstate(divide="ignore"):
-        out[nz] = shift + np.log(s)
+        out = shift + np.log(s)
     return out
 
 
 def _lse_rows(X: np.ndarray) -> np.ndarray:
-    """LSE over axis 1 of an [A, L] array; all -inf row -> -inf."""
-    mx = X.max(axis=1)
+    """LSE over axis 0 (commodities) of an [L, A] array; all -inf column -> -inf."""
+    mx = X.max(axis=0)
     shift = np.where(np.isfinite(mx), mx, 0.0)
     with np.errstate(divide="ignore"):
-        return shift + np.log(np.exp(X - shift[:, None]).sum(axis=1))
+        return shift + np.log(np.exp(X - shift[None, :]).sum(axis=0))
 
 
 def _log(x: np.ndarray) -> np.ndarray:
@@ -84,12 +95,12 @@ class OracleState:
     omega: np.ndarray   # [T, A]   log W_t <= 0
     lam0: np.ndarray    # [L, N]   log U0
     lamT: np.ndarray    # [L, N]   log UT
-    a: np.ndarray       # [T+1, N, L] log alpha_t (kept from the last forward pass)
-    b: np.ndarray       # [T+1, N, L] log beta_t  (from the last backward pass)
+    a: np.ndarray       # [T+1, L, N] log alpha_t (kept from the last forward pass)
+    b: np.ndarray       # [T+1, L, N] log beta_t  (from the last backward pass)
     log_mu0: np.ndarray  # [L, N]
     log_muT: np.ndarray  # [L, N]
-    in_seg: tuple
-    out_seg: tuple
+    in_seg: tuple        # arcs grouped by head (forward recursion)
+    out_seg: tuple       # arcs grouped by tail (backward recursion)
     sweeps: int = 0
 
 
@@ -107,28 +118,30 @@ def oracle_init(problem) -> OracleState:
     st = OracleState(
         problem=p, lK=lK, logd=logd, omega=np.zeros((T, A)),
         lam0=np.full((L, N), NEG_INF), lamT=np.where(muT > 0, 0.0, NEG_INF),
-        a=np.full((T + 1, N, L), NEG_INF), b=np.full((T + 1, N, L), NEG_INF),
+        a=np.full((T + 1, L, N), NEG_INF), b=np.full((T + 1, L, N), NEG_INF),
         log_mu0=_log(mu0), log_muT=_log(muT),
-        in_seg=_csr(p.head.astype(np.int64), N), out_seg=_csr(p.tail.astype(np.int64), N))
+        in_seg=_segments(p.head.astype(np.int64), N), out_seg=_segments(p.tail.astype(np.int64), N))
     backward(st)
     return st
 
 
 def backward(st: OracleState) -> None:
     """Backward recursion (eq:psi P:1038-1043; Alg. 2), node form:
-    b_T = lamT^T ; b_t[i,l] = LSE_{a: i_a = i}( lK_t[a] + omega_t[a] + b_{t+1}[j_a, l] )."""
+    b_T = lamT ; b_t[l,i] = LSE_{a: i_a = i}( lK_t[a] + omega_t[a] + b_{t+1}[l, j_a] )."""
     p = st.problem
-    st.b[p.T] = st.lamT.T
+    o = st.out_seg[0]
+    head_o = p.head[o]
+    st.b[p.T] = st.lamT
     for t in range(p.T - 1, -1, -1):
-        X = (st.lK[t] + st.omega[t])[:, None] + st.b[t + 1][p.head]
-        st.b[t] = seg_lse(X, st.out_seg, p.N)
+        X = (st.lK[t][o] + st.omega[t][o])[None, :] + st.b[t + 1][:, head_o]
+        st.b[t] = seg_lse(X, st.out_seg)
 
 
 def _boundary(log_mu: np.ndarray, msg: np.ndarray, where: str) -> np.ndarray:
-    """U = mu ./ msg in logs: 0/0 := 0 (mu = 0 -> -inf); mu > 0 with msg = 0 -> infeasible."""
+    """U = mu ./ msg in logs ([L, N]): 0/0 := 0 (mu = 0 -> -inf); mu > 0 with msg = 0 -> infeasible."""
     with np.errstate(invalid="ignore"):
-        lam = np.where(np.isfinite(log_mu), log_mu - msg.T, NEG_INF)
-    bad = np.isfinite(log_mu) & ~np.isfinite(msg.T)
+        lam = np.where(np.isfinite(log_mu), log_mu - msg, NEG_INF)
+    bad = np.isfinite(log_mu) & ~np.isfinite(msg)
     if bad.any():
         l, v = np.argwhere(bad)[0]
         raise OracleInfeasible(where, int(l), int(v))
@@ -152,23 +165,25 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None) -> None:
     on_block(kind, t, mass) is called after every dual block update (kind in {"U0", "W", "UT"}),
     with the tensor mass <K, U> at that moment, for the BCA-monotonicity pin (prp:sinkhorn)."""
     p = st.problem
+    oi = st.in_seg[0]
+    tail_i = p.tail[oi]
     # a2: U^(0,1) <- R^(0,1) ./ Psi_1  (P:1090)
     st.lam0 = _boundary(st.log_mu0, st.b[0], "source")
-    st.a[0] = st.lam0.T
+    st.a[0] = st.lam0
     if on_block is not None:
         on_block("U0", -1, float(np.exp(st.a[0] + st.b[0]).sum()))
     # a3: forward loop (P:1092-1095)
     for t in range(p.T):
-        X = st.a[t][p.tail] + st.lK[t][:, None] + st.b[t + 1][p.head]      # [A, L], no W
+        X = st.a[t][:, p.tail] + st.lK[t][None, :] + st.b[t + 1][:, p.head]      # [L, A], no W
         st.omega[t] = capacity_update(st.logd[t], _lse_rows(X))
         if on_block is not None:
-            on_block("W", t, float(np.exp(X + st.omega[t][:, None]).sum()))
-        Y = st.a[t][p.tail] + (st.lK[t] + st.omega[t])[:, None]
-        st.a[t + 1] = seg_lse(Y, st.in_seg, p.N)                           # Psi-hat_{t+1} (P:1094)
+            on_block("W", t, float(np.exp(X + st.omega[t][None, :]).sum()))
+        Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
+        st.a[t + 1] = seg_lse(Y, st.in_seg)                                    # Psi-hat_{t+1} (P:1094)
     # a4: U^(0,T) <- R^(0,T) ./ Psi-hat_T  (P:1096)
     st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
     if on_block is not None:
-        on_block("UT", p.T, float(np.exp(st.a[p.T] + st.lamT.T).sum()))
+        on_block("UT", p.T, float(np.exp(st.a[p.T] + st.lamT).sum()))
     # a5: backward recompute (P:1097-1100)
     backward(st)
     st.sweeps += 1
@@ -185,7 +200,7 @@ def readout_commodity_flows(st: OracleState, t: int) -> np.ndarray:
     """Per-commodity arc flow F^l_t[a] = alpha_t[i_a,l] K_t[a] W_t[a] beta_{t+1}[j_a,l]
     (cor:proj P:1078 in node form), from the kept forward messages and the latest backward pass."""
     p = st.problem
-    return np.exp(st.a[t][p.tail] + (st.lK[t] + st.omega[t])[:, None] + st.b[t + 1][p.head])
+    return np.exp(st.a[t][:, p.tail] + (st.lK[t] + st.omega[t])[None, :] + st.b[t + 1][:, p.head]).T
 
 
 def readout_flows(st: OracleState) -> tuple:
@@ -215,9 +230,9 @@ def stats(st: OracleState) -> dict:
     F, W = readout_flows(st)
     cost = np.broadcast_to(p.cost, F.shape)
     cap = np.broadcast_to(p.cap, F.shape)
-    mass = float(np.exp(st.a[p.T] + st.lamT.T).sum())
-    P0 = np.exp(st.lam0 + st.b[0].T)            # source marginal of the end-of-sweep tensor
-    PT = np.exp(st.a[p.T].T + st.lamT)          # sink marginal
+    mass = float(np.exp(st.a[p.T] + st.lamT).sum())
+    P0 = np.exp(st.lam0 + st.b[0])              # source marginal of the end-of-sweep tensor
+    PT = np.exp(st.a[p.T] + st.lamT)            # sink marginal
     return {
         "mass": mass,
         "primal": float((cost * F).sum()),

@@ -19,7 +19,7 @@ MMF_FP64, MMF_FP32 = 0, 1
 
 # functions declared in include/mmf.h (checked by tests/test_abi.py against the header)
 EXPORTS = ["mmf_create", "mmf_set_graph", "mmf_set_costs", "mmf_set_capacity", "mmf_set_marginals",
-           "mmf_set_point_marginals", "mmf_workspace_bytes", "mmf_set_workspace", "mmf_attach_nccl",
+           "mmf_set_point_marginals", "mmf_workspace_bytes", "mmf_set_workspace", "mmf_attach_nccl", "mmf_nccl_unique_id",
            "mmf_set_option", "mmf_init", "mmf_sweep", "mmf_sync", "mmf_read_edge_flows", "mmf_read_cap_duals",
            "mmf_read_stats", "mmf_read_kernel_stats", "mmf_sweep_bytes", "mmf_destroy", "mmf_last_error",
            "mmf_version"]
@@ -60,6 +60,7 @@ def load(path: str = LIB_PATH):
         "mmf_workspace_bytes": ([vp, C.POINTER(C.c_size_t)], C.c_int),
         "mmf_set_workspace": ([vp, vp, C.c_size_t], C.c_int),
         "mmf_attach_nccl": ([vp, C.c_char_p, C.c_int, C.c_int], C.c_int),
+        "mmf_nccl_unique_id": ([C.c_char_p], C.c_int),
         "mmf_set_option": ([vp, C.c_char_p, i64], C.c_int),
         "mmf_init": ([vp], C.c_int),
         "mmf_sweep": ([vp, i32], C.c_int),
@@ -153,6 +154,14 @@ def mmf_set_workspace(ctx, dptr: int, nbytes: int):
 def mmf_attach_nccl(ctx, unique_id: bytes, nranks: int, rank: int):
     assert len(unique_id) == 128
     _check(ctx, load().mmf_attach_nccl(ctx, C.c_char_p(bytes(unique_id)), int(nranks), int(rank)))
+
+
+def mmf_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = load().mmf_nccl_unique_id(buf)
+    if st != 0:
+        raise MMFError(st, load().mmf_last_error(None).decode())
+    return buf.raw
 
 
 def mmf_set_option(ctx, key: str, value: int):

@@ -36,6 +36,7 @@ struct NcclApi {
   ncclResult_t_ (*CommDestroy)(ncclComm_t_) = nullptr;
   ncclResult_t_ (*CommGetAsyncError)(ncclComm_t_, ncclResult_t_*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t_) = nullptr;
+  ncclResult_t_ (*GetUniqueId)(NcclUid*) = nullptr;
 };
 // ncclDataType_t / ncclRedOp_t values (stable NCCL ABI)
 constexpr int NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8, NCCL_SUM = 0;
@@ -53,6 +54,7 @@ NcclApi& nccl_api() {
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
   api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
   api.ok = api.CommInitRank && api.AllReduce && api.CommDestroy && api.CommGetAsyncError;
   return api;
 }
@@ -870,6 +872,22 @@ mmf_status mmf_set_workspace(mmf_ctx* ctx, void* dptr, size_t bytes) {
   }
   ctx->ws = dptr;
   ctx->ws_bytes = bytes;
+  return MMF_OK;
+}
+
+mmf_status mmf_nccl_unique_id(void* out128) {
+  if (!out128) return MMF_EINVAL;
+  NcclApi& api = nccl_api();
+  if (!api.ok || !api.GetUniqueId) {
+    g_create_error = "libnccl.so.2 not found in the process";
+    return MMF_ENCCL;
+  }
+  NcclUid uid;
+  if (api.GetUniqueId(&uid) != 0) {
+    g_create_error = "ncclGetUniqueId failed";
+    return MMF_ENCCL;
+  }
+  memcpy(out128, uid.internal, 128);
   return MMF_OK;
 }
 

@@ -50,7 +50,7 @@ def test_p1_structured_projections_equal_full_tensor(kw):
         assert max_rel_err(readout_commodity_flows(st, t), commodity_arc_flows(p, M, t), 1e-300) < 1e-12
     # end-of-sweep marginals: P_{c,T} = muT exactly after a4, P_{c,0} from the new backward pass
     assert max_rel_err(commodity_marginal(M, p.T), p.muT, 1e-300) < 1e-12
-    P0 = np.exp(st.lam0 + st.b[0].T)
+    P0 = np.exp(st.lam0 + st.b[0])
     assert max_rel_err(commodity_marginal(M, 0), P0, 1e-300) < 1e-12
 
 
