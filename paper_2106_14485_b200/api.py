@@ -15,7 +15,7 @@ from . import _lib as L
 class Solver:
     def __init__(self, problem, prec: Optional[str] = None, device: int = 0, stream=None, graph: bool = True,
                  reorder: bool = True, profile: bool = False, l_begin: int = 0, l_count: Optional[int] = None,
-                 nccl_uid: Optional[bytes] = None, nranks: int = 1, rank: int = 0):
+                 nccl_uid: Optional[bytes] = None, nranks: int = 1, rank: int = 0, options: Optional[dict] = None):
         import torch  # device memory + streams only
 
         self.p = problem
@@ -33,6 +33,8 @@ class Solver:
             L.mmf_set_option(self.ctx, "graph", int(graph))
             L.mmf_set_option(self.ctx, "reorder", int(reorder))
             L.mmf_set_option(self.ctx, "profile", int(profile))
+            for k, v in (options or {}).items():
+                L.mmf_set_option(self.ctx, k, int(v))
             self.upload(problem, l_begin, l_count)
             if nccl_uid is not None:
                 L.mmf_attach_nccl(self.ctx, nccl_uid, nranks, rank)

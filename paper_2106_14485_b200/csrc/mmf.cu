@@ -7,6 +7,8 @@
 // edge flows for commodity sharding.
 #include "../../include/mmf.h"
 #include "kernels.cuh"
+#include "tiled.cuh"
+#include "wide.cuh"
 
 #include <dlfcn.h>
 
@@ -89,11 +91,25 @@ struct mmf_ctx {
 
   // ---- options
   bool opt_graph = true, opt_reorder = true, opt_profile = false;
+  int opt_kernels = 3;  // 3 = wide-lane kernels (production), 2 = smem-staged tile kernels, 1 = per-node reference kernels
+  int opt_tile = 32;    // max nodes per tile
+  int opt_cpt = 0;      // commodities per lane (0 = auto: 2 for fp32, 1 for fp64)
+  int opt_halo = 0;     // max in-/out-halo nodes per tile (0 = auto: 2 * tile)
+  int opt_cpc = 0;      // commodity chunks per CTA (0 = auto)
+  int opt_order = 2;    // node order (kernels >= 2): 0 input order, 1 reverse Cuthill-McKee, 2 BFS tiles
 
   // ---- derived
   int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
+  int CPT = 1, LC = 32, nch = 1;
   std::vector<int> newid;       // user node -> internal
   std::vector<int> int_of_arc;  // user arc -> internal arc
+  bool prepared = false;        // host graph structures below are valid
+  std::vector<int> h_tail, h_head, h_inptr, h_outptr, h_outarc, h_outhead;
+  int ntiles = 0, tileB = 0, max_hin = 0, max_hout = 0, max_ia = 0, max_oa = 0;
+  std::vector<int> h_tile_ptr, h_hin_ptr, h_hin_node, h_hout_ptr, h_hout_node, h_in_hidx, h_out_hidx;
+  TileMeta tm{};
+  PipeCfg pc{1, 1};
+  WideCfg wc{};
 
   // ---- device
   void* ws = nullptr;
@@ -222,13 +238,239 @@ struct Layout {
   }
 };
 
+// Node tiles: BFS-grown blobs (seeds in reverse Cuthill-McKee order) of at most B nodes whose in-halo
+// and out-halo (tails of the tile's in-arcs, heads of its out-arcs) stay within `cap` nodes, so the
+// shared-memory footprint of a tile is bounded and uniform.  On grids and geometric graphs the blobs
+// are compact (halo / tile ~ 2 instead of the mean degree).
+void make_tiles(int N, const std::vector<int>& tail, const std::vector<int>& head, int B, int cap, bool reorder,
+                std::vector<int>& order, std::vector<int>& tile_ptr) {
+  order.clear();
+  tile_ptr.assign(1, 0);
+  if (!reorder) {
+    for (int v = 0; v < N; ++v) order.push_back(v);
+    for (int v = B; v < N; v += B) tile_ptr.push_back(v);
+    tile_ptr.push_back(N);
+    return;
+  }
+  const size_t A = tail.size();
+  auto csr = [&](const std::vector<int>& key, const std::vector<int>& val, std::vector<int64_t>& ptr,
+                 std::vector<int>& out, bool skip_loops) {
+    ptr.assign(N + 1, 0);
+    for (size_t a = 0; a < A; ++a)
+      if (!(skip_loops && tail[a] == head[a])) ptr[key[a] + 1]++;
+    for (int v = 0; v < N; ++v) ptr[v + 1] += ptr[v];
+    out.resize(ptr[N]);
+    std::vector<int64_t> f(ptr.begin(), ptr.end() - 1);
+    for (size_t a = 0; a < A; ++a)
+      if (!(skip_loops && tail[a] == head[a])) out[f[key[a]]++] = val[a];
+  };
+  std::vector<int64_t> pin, pout, pu1, pu2;
+  std::vector<int> nin, nout, u1, u2;
+  csr(head, tail, pin, nin, false);   // in-neighbours (tails of in-arcs), loops included
+  csr(tail, head, pout, nout, false); // out-neighbours
+  csr(tail, head, pu1, u1, true);     // undirected support for the BFS: out ...
+  csr(head, tail, pu2, u2, true);     // ... and in
+  std::vector<int> rid = rcm_newid(N, tail, head);
+  std::vector<int> seeds(N);
+  for (int v = 0; v < N; ++v) seeds[rid[v]] = v;
+  std::vector<int> mark_in(N, -1), mark_out(N, -1);
+  std::vector<char> done(N, 0);
+  int tid = 0, n_in = 0, n_out = 0;
+  auto cost = [&](int u, int& di, int& dout) {
+    di = dout = 0;
+    for (int64_t k = pin[u]; k < pin[u + 1]; ++k) di += mark_in[nin[k]] != tid;
+    for (int64_t k = pout[u]; k < pout[u + 1]; ++k) dout += mark_out[nout[k]] != tid;
+  };
+  auto add = [&](int u) {
+    done[u] = 1;
+    order.push_back(u);
+    for (int64_t k = pin[u]; k < pin[u + 1]; ++k)
+      if (mark_in[nin[k]] != tid) {
+        mark_in[nin[k]] = tid;
+        n_in++;
+      }
+    for (int64_t k = pout[u]; k < pout[u + 1]; ++k)
+      if (mark_out[nout[k]] != tid) {
+        mark_out[nout[k]] = tid;
+        n_out++;
+      }
+  };
+  for (int s : seeds) {
+    if (done[s]) continue;
+    n_in = n_out = 0;
+    const size_t q0 = order.size();
+    add(s);
+    for (size_t qi = q0; qi < order.size() && (int)(order.size() - q0) < B; ++qi) {
+      const int v = order[qi];
+      for (int pass = 0; pass < 2; ++pass) {
+        const std::vector<int64_t>& pp = pass ? pu2 : pu1;
+        const std::vector<int>& nn = pass ? u2 : u1;
+        for (int64_t k = pp[v]; k < pp[v + 1] && (int)(order.size() - q0) < B; ++k) {
+          const int u = nn[k];
+          if (done[u]) continue;
+          int di, dout;
+          cost(u, di, dout);
+          if (n_in + di <= cap && n_out + dout <= cap) add(u);
+        }
+      }
+    }
+    tile_ptr.push_back((int)order.size());
+    ++tid;
+  }
+}
+
 void derive_shapes(mmf_ctx* c) {
-  c->Lp = ((c->L + 31) / 32) * 32;
+  int cpt_auto = c->prec == MMF_FP32 ? 2 : 1;
+  if (c->opt_kernels == 3) {
+    if (c->prec == MMF_FP32)
+      cpt_auto = c->L >= 512 ? 8 : (c->L >= 128 ? 4 : 2);
+    else
+      cpt_auto = c->L >= 64 ? 2 : 1;
+  }
+  c->CPT = c->opt_cpt ? c->opt_cpt : cpt_auto;
+  if (c->prec == MMF_FP64) c->CPT = std::min(c->CPT, 2);   // fp64 lanes: at most 2 (16-byte loads)
+  if (c->opt_kernels == 2) c->CPT = std::min(c->CPT, 4);   // tile kernels: instantiated for 1, 2, 4
+  c->LC = 32 * c->CPT;
+  c->Lp = ((c->L + c->LC - 1) / c->LC) * c->LC;
+  c->nch = c->Lp / c->LC;
+  // wide path: warps = (nodes per CTA) x (chunks per CTA) = 8
+  {
+    int cp = 8;
+    while (cp > 1 && cp > c->nch) cp >>= 1;
+    c->wc.cpcta = cp;
+    c->wc.npc = (WIDE_THREADS / 32) / cp;
+    c->wc.ngroup = (c->nch + cp - 1) / cp;
+    c->wc.nch = c->nch;
+    int mo = 0;
+    if (!c->h_outptr.empty())
+      for (int j0 = 0; j0 < c->N; j0 += c->wc.npc)
+        mo = std::max(mo, c->h_outptr[std::min(j0 + c->wc.npc, c->N)] - c->h_outptr[j0]);
+    c->wc.max_oa = mo;
+  }
+  // chunk groups per tile: enough CTAs for ~4 per SM, each CTA pipelining cpc chunks
+  {
+    const int target = 4 * 148;
+    int ng = c->opt_cpc > 0 ? (c->nch + c->opt_cpc - 1) / c->opt_cpc
+                            : std::max(1, std::min(c->nch, (target + std::max(c->ntiles, 1) - 1) / std::max(c->ntiles, 1)));
+    c->pc.cpc = (c->nch + ng - 1) / ng;
+    c->pc.ngroup = (c->nch + c->pc.cpc - 1) / c->pc.cpc;
+  }
   int chunks = c->Lp / 32;
   int w = 8;
   while (chunks % w) w >>= 1;
   c->block = 32 * w;
   c->G = c->Lp / c->block;
+}
+
+// host-side graph structures: node order (tiles), internal arc order (in-CSR by head), out-CSR,
+// tile halos and halo-local indices.  Depends on the graph and options only.
+void prepare(mmf_ctx* c) {
+  if (c->prepared) return;
+  const int N = c->N;
+  const int64_t A = c->A;
+  std::vector<int> order;
+  const int B = c->opt_kernels >= 2 ? c->opt_tile : std::max(N, 1);
+  if (c->opt_kernels >= 2 && c->opt_order == 2) {
+    make_tiles(N, c->tail, c->head, B, c->opt_halo > 0 ? c->opt_halo : 2 * B, c->opt_reorder, order, c->h_tile_ptr);
+    c->newid.assign(N, 0);
+    for (int k = 0; k < N; ++k) c->newid[order[k]] = k;
+  } else if (c->opt_kernels >= 2) {
+    if (c->opt_reorder && c->opt_order == 1) {
+      c->newid = rcm_newid(N, c->tail, c->head);
+    } else {
+      c->newid.resize(N);
+      std::iota(c->newid.begin(), c->newid.end(), 0);
+    }
+    c->h_tile_ptr.assign(1, 0);
+    for (int v = B; v < N; v += B) c->h_tile_ptr.push_back(v);
+    c->h_tile_ptr.push_back(N);
+  } else {
+    if (c->opt_reorder) {
+      c->newid = rcm_newid(N, c->tail, c->head);
+    } else {
+      c->newid.resize(N);
+      std::iota(c->newid.begin(), c->newid.end(), 0);
+    }
+    c->h_tile_ptr = {0, N};
+  }
+  c->ntiles = (int)c->h_tile_ptr.size() - 1;
+  c->tileB = 0;
+  for (int k = 0; k < c->ntiles; ++k) c->tileB = std::max(c->tileB, c->h_tile_ptr[k + 1] - c->h_tile_ptr[k]);
+
+  std::vector<int> it(A), ih(A);
+  for (int64_t a = 0; a < A; ++a) {
+    it[a] = c->newid[c->tail[a]];
+    ih[a] = c->newid[c->head[a]];
+  }
+  std::vector<int64_t> ord(A);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return ih[x] != ih[y] ? ih[x] < ih[y] : it[x] < it[y]; });
+  c->int_of_arc.assign(A, 0);
+  c->h_tail.assign(A, 0);
+  c->h_head.assign(A, 0);
+  c->h_inptr.assign(N + 1, 0);
+  c->h_outptr.assign(N + 1, 0);
+  c->h_outarc.assign(A, 0);
+  c->h_outhead.assign(A, 0);
+  for (int64_t k = 0; k < A; ++k) {
+    c->int_of_arc[ord[k]] = (int)k;
+    c->h_tail[k] = it[ord[k]];
+    c->h_head[k] = ih[ord[k]];
+    c->h_inptr[ih[ord[k]] + 1]++;
+  }
+  for (int v = 0; v < N; ++v) c->h_inptr[v + 1] += c->h_inptr[v];
+  c->maxdeg_in = 0;
+  for (int v = 0; v < N; ++v) c->maxdeg_in = std::max(c->maxdeg_in, c->h_inptr[v + 1] - c->h_inptr[v]);
+  std::vector<int64_t> ordo(A);
+  std::iota(ordo.begin(), ordo.end(), 0);
+  std::sort(ordo.begin(), ordo.end(), [&](int64_t x, int64_t y) {
+    return c->h_tail[x] != c->h_tail[y] ? c->h_tail[x] < c->h_tail[y] : c->h_head[x] < c->h_head[y];
+  });
+  for (int64_t k = 0; k < A; ++k) {
+    c->h_outarc[k] = (int)ordo[k];
+    c->h_outhead[k] = c->h_head[ordo[k]];
+    c->h_outptr[c->h_tail[ordo[k]] + 1]++;
+  }
+  for (int v = 0; v < N; ++v) c->h_outptr[v + 1] += c->h_outptr[v];
+
+  // halos
+  std::vector<int> tile_of(N);
+  for (int k = 0; k < c->ntiles; ++k)
+    for (int v = c->h_tile_ptr[k]; v < c->h_tile_ptr[k + 1]; ++v) tile_of[v] = k;
+  c->h_hin_ptr.assign(1, 0);
+  c->h_hout_ptr.assign(1, 0);
+  c->h_hin_node.clear();
+  c->h_hout_node.clear();
+  c->h_in_hidx.assign(A, 0);
+  c->h_out_hidx.assign(A, 0);
+  c->max_hin = c->max_hout = c->max_ia = c->max_oa = 0;
+  std::vector<int> tmp;
+  for (int k = 0; k < c->ntiles; ++k) {
+    const int v0 = c->h_tile_ptr[k], v1 = c->h_tile_ptr[k + 1];
+    c->max_ia = std::max(c->max_ia, c->h_inptr[v1] - c->h_inptr[v0]);
+    c->max_oa = std::max(c->max_oa, c->h_outptr[v1] - c->h_outptr[v0]);
+    tmp.assign(c->h_tail.begin() + c->h_inptr[v0], c->h_tail.begin() + c->h_inptr[v1]);
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    const size_t base_in = c->h_hin_node.size();
+    c->h_hin_node.insert(c->h_hin_node.end(), tmp.begin(), tmp.end());
+    c->h_hin_ptr.push_back((int)c->h_hin_node.size());
+    c->max_hin = std::max(c->max_hin, (int)tmp.size());
+    for (int a = c->h_inptr[v0]; a < c->h_inptr[v1]; ++a)
+      c->h_in_hidx[a] = (int)(std::lower_bound(c->h_hin_node.begin() + base_in, c->h_hin_node.end(), c->h_tail[a]) -
+                              (c->h_hin_node.begin() + base_in));
+    tmp.assign(c->h_outhead.begin() + c->h_outptr[v0], c->h_outhead.begin() + c->h_outptr[v1]);
+    std::sort(tmp.begin(), tmp.end());
+    tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+    const size_t base_out = c->h_hout_node.size();
+    c->h_hout_node.insert(c->h_hout_node.end(), tmp.begin(), tmp.end());
+    c->h_hout_ptr.push_back((int)c->h_hout_node.size());
+    c->max_hout = std::max(c->max_hout, (int)tmp.size());
+    for (int q = c->h_outptr[v0]; q < c->h_outptr[v1]; ++q)
+      c->h_out_hidx[q] = (int)(std::lower_bound(c->h_hout_node.begin() + base_out, c->h_hout_node.end(), c->h_outhead[q]) -
+                               (c->h_hout_node.begin() + base_out));
+  }
+  c->prepared = true;
 }
 
 // walk the workspace layout; assign pointers when base != nullptr
@@ -238,6 +480,7 @@ size_t layout(mmf_ctx* c, char* base) {
   const size_t TK = c->cost_tv ? T : 1, TC = c->cap_tv ? T : 1;
   const size_t sm = c->sm(), se = c->se();
   DevPtrs& p = c->dp;
+  TileMeta& tm = c->tm;
   auto at = [&](size_t o) -> char* { return base ? base + o : nullptr; };
   p.tail = (const int*)at(L.take(A * 4));
   p.in_ptr = (const int*)at(L.take((N + 1) * 4));
@@ -274,6 +517,26 @@ size_t layout(mmf_ctx* c, char* base) {
   p.err = (unsigned*)at(L.take(8));
   p.errloc = (unsigned long long*)at(L.take(8));
   p.stats = (double*)at(L.take(8 * 8));
+  const size_t nt = (size_t)c->ntiles;
+  tm.tile_ptr = (const int*)at(L.take((nt + 1) * 4));
+  tm.hin_ptr = (const int*)at(L.take((nt + 1) * 4));
+  tm.hin_node = (const int*)at(L.take(c->h_hin_node.size() * 4 + 4));
+  tm.hout_ptr = (const int*)at(L.take((nt + 1) * 4));
+  tm.hout_node = (const int*)at(L.take(c->h_hout_node.size() * 4 + 4));
+  tm.in_hidx = (const int*)at(L.take(A * 4));
+  tm.out_hidx = (const int*)at(L.take(A * 4));
+  tm.cnt = (int*)at(L.take(nt * 4));
+  c->wc.cnt = (int*)at(L.take(((size_t)c->N + 1) * 4));
+  tm.part = at(L.take(A * (size_t)c->nch * sm));
+  c->wc.part = tm.part;
+  tm.ntiles = c->ntiles;
+  tm.max_hin = c->max_hin;
+  tm.max_hout = c->max_hout;
+  tm.max_ia = c->max_ia;
+  tm.max_oa = c->max_oa;
+  tm.B = c->tileB;
+  tm.nch = c->nch;
+  tm.LC = c->LC;
   p.N = c->N;
   p.Lp = c->Lp;
   p.L = c->L;
@@ -410,7 +673,131 @@ template <class T_> struct Eng {
     return MMF_OK;
   }
 
+  // ---------------- node-tile path (opt_kernels == 2)
+  template <int CPT, int MODE, int FMODE> static void launch_fwd(mmf_ctx* c, cudaStream_t s, int t, size_t smem) {
+    dim3 grid(c->ntiles, c->pc.ngroup);
+    k_fwd_tile<T_, CPT, MODE, FMODE><<<grid, TILE_THREADS, smem, s>>>(c->dp, c->tm, c->pc, t);
+  }
+  template <int CPT> static void tiled_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
+    const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
+    const size_t smem = FwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_hin, c->max_ia, c->max_oa);
+    switch (mode * 3 + fmode) {
+      case 0: launch_fwd<CPT, 0, 0>(c, s, t, smem); break;
+      case 1: launch_fwd<CPT, 0, 1>(c, s, t, smem); break;
+      case 2: launch_fwd<CPT, 0, 2>(c, s, t, smem); break;
+      case 3: launch_fwd<CPT, 1, 0>(c, s, t, smem); break;
+      case 4: launch_fwd<CPT, 1, 1>(c, s, t, smem); break;
+      case 5: launch_fwd<CPT, 1, 2>(c, s, t, smem); break;
+      case 6: launch_fwd<CPT, 2, 0>(c, s, t, smem); break;
+      case 7: launch_fwd<CPT, 2, 1>(c, s, t, smem); break;
+      default: launch_fwd<CPT, 2, 2>(c, s, t, smem); break;
+    }
+  }
+  template <int CPT> static void tiled_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
+    dim3 grid(c->ntiles, c->pc.ngroup);
+    k_bwd_tile<T_, CPT><<<grid, TILE_THREADS, BwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_oa), s>>>(
+        c->dp, c->tm, c->pc, t);
+  }
+  template <int CPT> static cudaError_t tiled_attrs_cpt(mmf_ctx* c) {
+    const int fwd = (int)FwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_hin, c->max_ia, c->max_oa);
+    const int bwd = (int)BwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_oa);
+    cudaError_t e = cudaSuccess;
+#define MMF_ATTR(K, B) \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, B);
+    MMF_ATTR((k_fwd_tile<T_, CPT, 0, 0>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 0, 1>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 0, 2>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 1, 0>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 1, 1>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 1, 2>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 2, 0>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 2, 1>), fwd)
+    MMF_ATTR((k_fwd_tile<T_, CPT, 2, 2>), fwd)
+    MMF_ATTR((k_bwd_tile<T_, CPT>), bwd)
+#undef MMF_ATTR
+    return e;
+  }
+  static constexpr bool is_f32() { return sizeof(M) == 4; }
+  // ---------------- wide-lane path (opt_kernels == 3)
+  template <int CPT, int MODE, int FMODE> static void launch_fwd_wide(mmf_ctx* c, cudaStream_t s, int t) {
+    dim3 grid((c->N + c->wc.npc - 1) / c->wc.npc, c->wc.ngroup);
+    k_fwd_wide<T_, CPT, MODE, FMODE><<<grid, WIDE_THREADS, wide_smem<M>(c->wc.max_oa, c->wc.cpcta), s>>>(c->dp, c->wc, t);
+  }
+  template <int CPT> static void wide_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
+    const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
+    switch (mode * 3 + fmode) {
+      case 0: launch_fwd_wide<CPT, 0, 0>(c, s, t); break;
+      case 1: launch_fwd_wide<CPT, 0, 1>(c, s, t); break;
+      case 2: launch_fwd_wide<CPT, 0, 2>(c, s, t); break;
+      case 3: launch_fwd_wide<CPT, 1, 0>(c, s, t); break;
+      case 4: launch_fwd_wide<CPT, 1, 1>(c, s, t); break;
+      case 5: launch_fwd_wide<CPT, 1, 2>(c, s, t); break;
+      case 6: launch_fwd_wide<CPT, 2, 0>(c, s, t); break;
+      case 7: launch_fwd_wide<CPT, 2, 1>(c, s, t); break;
+      default: launch_fwd_wide<CPT, 2, 2>(c, s, t); break;
+    }
+  }
+  template <int CPT> static void wide_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
+    dim3 grid((c->N + c->wc.npc - 1) / c->wc.npc, c->wc.ngroup);
+    k_bwd_wide<T_, CPT><<<grid, WIDE_THREADS, wide_smem<M>(0, 1), s>>>(c->dp, c->wc, t);
+  }
+  static void tiled_fwd(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
+    LaunchScope ls(c, K_FUSED, s);
+    if (c->opt_kernels == 3) {
+      if (c->CPT == 1) wide_fwd_cpt<1>(c, s, t, fmode);
+      else if (c->CPT == 2 || !is_f32()) wide_fwd_cpt<2>(c, s, t, fmode);
+      else if (c->CPT == 4) wide_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
+      else wide_fwd_cpt<is_f32() ? 8 : 2>(c, s, t, fmode);
+      return;
+    }
+    if (c->CPT == 1) tiled_fwd_cpt<1>(c, s, t, fmode);
+    else if (c->CPT == 2) tiled_fwd_cpt<2>(c, s, t, fmode);
+    else tiled_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
+  }
+  static void tiled_bwd(mmf_ctx* c, cudaStream_t s, int t) {
+    LaunchScope ls(c, K_BWD, s);
+    if (c->opt_kernels == 3) {
+      if (c->CPT == 1) wide_bwd_cpt<1>(c, s, t);
+      else if (c->CPT == 2 || !is_f32()) wide_bwd_cpt<2>(c, s, t);
+      else if (c->CPT == 4) wide_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
+      else wide_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
+      return;
+    }
+    if (c->CPT == 1) tiled_bwd_cpt<1>(c, s, t);
+    else if (c->CPT == 2) tiled_bwd_cpt<2>(c, s, t);
+    else tiled_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
+  }
+  static mmf_status tiled_attrs(mmf_ctx* ctx) {
+    mmf_ctx* c = ctx;
+    if (c->CPT == 1) CU(tiled_attrs_cpt<1>(c));
+    else if (c->CPT == 2) CU(tiled_attrs_cpt<2>(c));
+    else CU(tiled_attrs_cpt<is_f32() ? 4 : 2>(c));
+    return MMF_OK;
+  }
+  // the multi-GPU exchange of one forward step: all-reduce the rank-partial F_t, then W_t update
+  static mmf_status exchange(mmf_ctx* c, cudaStream_t s, int t) {
+    const DevPtrs& p = c->dp;
+    int r = nccl_api().AllReduce(p.Fsum, p.Fsum, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
+                                 NCCL_SUM, c->comm, s);
+    if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
+    LaunchScope ls(c, K_REDUCE, s);
+    k_dual<T_><<<(unsigned)((c->A + 255) / 256), 256, 0, s>>>(p, t);
+    return MMF_OK;
+  }
+
   static mmf_status enqueue_sweep(mmf_ctx* c, cudaStream_t s) {
+    if (c->opt_kernels >= 2) {
+      const int fmode = c->comm ? 1 : 0;
+      for (int t = 0; t <= c->T; ++t) {  // a2 fused in t = 0, a4 fused in t = T
+        tiled_fwd(c, s, t, fmode);
+        if (c->comm && t < c->T) {
+          mmf_status st = exchange(c, s, t);
+          if (st != MMF_OK) return st;
+        }
+      }
+      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      return MMF_OK;
+    }
     boundary(c, s, 0);  // a2
     for (int t = 0; t < c->T; ++t) {
       mmf_status st = fwd_step(c, s, t, 0);  // a3
@@ -424,6 +811,10 @@ template <class T_> struct Eng {
   static mmf_status init_device(mmf_ctx* ctx, cudaStream_t s) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
+    if (c->opt_kernels == 2) {
+      mmf_status st = tiled_attrs(c);
+      if (st != MMF_OK) return st;
+    }
     {
       LaunchScope ls(c, K_OTHER, s);
       size_t n = (size_t)c->T * c->A;
@@ -438,13 +829,28 @@ template <class T_> struct Eng {
       LaunchScope ls(c, K_OTHER, s);
       k_init_ut_point<T_><<<(c->L + 127) / 128, 128, 0, s>>>(p);
     }
-    bwd_pass(c, s);
+    if (c->opt_kernels >= 2)
+      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);
+    else
+      bwd_pass(c, s);
     return MMF_OK;
   }
 
   static mmf_status readout(mmf_ctx* ctx, cudaStream_t s) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
+    if (c->opt_kernels >= 2) {
+      for (int t = 0; t <= c->T; ++t) {
+        tiled_fwd(c, s, t, 2);
+        if (c->comm && t < c->T) {
+          M* out = (M*)p.Fout + (size_t)t * c->A;
+          int r = nccl_api().AllReduce(out, out, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
+                                       NCCL_SUM, c->comm, s);
+          if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
+        }
+      }
+      return MMF_OK;
+    }
     const size_t n = (size_t)c->N * c->Lp;
     CU(cudaMemcpyAsync(p.am, p.u0m, n * sizeof(M), cudaMemcpyDeviceToDevice, s));
     CU(cudaMemcpyAsync(p.ae, p.u0e, n * sizeof(E), cudaMemcpyDeviceToDevice, s));
@@ -533,42 +939,7 @@ mmf_status finalize(mmf_ctx* ctx) {
   mmf_ctx* c = ctx;
   const int N = c->N;
   const int64_t A = c->A;
-  c->newid = c->opt_reorder ? rcm_newid(N, c->tail, c->head) : std::vector<int>();
-  if (!c->opt_reorder) {
-    c->newid.resize(N);
-    std::iota(c->newid.begin(), c->newid.end(), 0);
-  }
-  std::vector<int> it(A), ih(A);
-  for (int64_t a = 0; a < A; ++a) {
-    it[a] = c->newid[c->tail[a]];
-    ih[a] = c->newid[c->head[a]];
-  }
-  std::vector<int64_t> ord(A);
-  std::iota(ord.begin(), ord.end(), 0);
-  std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return ih[x] != ih[y] ? ih[x] < ih[y] : it[x] < it[y]; });
-  c->int_of_arc.assign(A, 0);
-  std::vector<int> h_tail(A), h_inptr(N + 1, 0), h_outptr(N + 1, 0), h_outarc(A), h_outhead(A);
-  for (int64_t k = 0; k < A; ++k) {
-    c->int_of_arc[ord[k]] = (int)k;
-    h_tail[k] = it[ord[k]];
-    h_inptr[ih[ord[k]] + 1]++;
-  }
-  for (int v = 0; v < N; ++v) h_inptr[v + 1] += h_inptr[v];
-  c->maxdeg_in = 0;
-  for (int v = 0; v < N; ++v) c->maxdeg_in = std::max(c->maxdeg_in, h_inptr[v + 1] - h_inptr[v]);
-  std::vector<int64_t> ordo(A);
-  std::iota(ordo.begin(), ordo.end(), 0);  // internal arc ids
-  std::vector<int> ihead_int(A);
-  for (int64_t k = 0; k < A; ++k) ihead_int[k] = ih[ord[k]];
-  std::sort(ordo.begin(), ordo.end(), [&](int64_t x, int64_t y) {
-    return h_tail[x] != h_tail[y] ? h_tail[x] < h_tail[y] : ihead_int[x] < ihead_int[y];
-  });
-  for (int64_t k = 0; k < A; ++k) {
-    h_outarc[k] = (int)ordo[k];
-    h_outhead[k] = ihead_int[ordo[k]];
-    h_outptr[h_tail[ordo[k]] + 1]++;
-  }
-  for (int v = 0; v < N; ++v) h_outptr[v + 1] += h_outptr[v];
+  prepare(c);
 
   derive_shapes(c);
   size_t need = layout(c, nullptr);
@@ -585,11 +956,26 @@ mmf_status finalize(mmf_ctx* ctx) {
   DevPtrs& p = c->dp;
   cudaStream_t s = c->stream;
 
-  CU(cudaMemcpyAsync((void*)p.tail, h_tail.data(), A * 4, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync((void*)p.in_ptr, h_inptr.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync((void*)p.out_ptr, h_outptr.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync((void*)p.out_arc, h_outarc.data(), A * 4, cudaMemcpyHostToDevice, s));
-  CU(cudaMemcpyAsync((void*)p.out_head, h_outhead.data(), A * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.tail, c->h_tail.data(), A * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.in_ptr, c->h_inptr.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.out_ptr, c->h_outptr.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.out_arc, c->h_outarc.data(), A * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.out_head, c->h_outhead.data(), A * 4, cudaMemcpyHostToDevice, s));
+  {
+    const TileMeta& tm = c->tm;
+    const size_t nt = (size_t)c->ntiles;
+    CU(cudaMemcpyAsync((void*)tm.tile_ptr, c->h_tile_ptr.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)tm.hin_ptr, c->h_hin_ptr.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)tm.hout_ptr, c->h_hout_ptr.data(), (nt + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (!c->h_hin_node.empty())
+      CU(cudaMemcpyAsync((void*)tm.hin_node, c->h_hin_node.data(), c->h_hin_node.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!c->h_hout_node.empty())
+      CU(cudaMemcpyAsync((void*)tm.hout_node, c->h_hout_node.data(), c->h_hout_node.size() * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)tm.in_hidx, c->h_in_hidx.data(), A * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)tm.out_hidx, c->h_out_hidx.data(), A * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaMemsetAsync(tm.cnt, 0, nt * 4, s));
+    CU(cudaMemsetAsync(c->wc.cnt, 0, ((size_t)c->N + 1) * 4, s));
+  }
 
   const bool f32 = c->prec == MMF_FP32;
   const size_t sm = c->sm(), se = c->se();
@@ -726,9 +1112,35 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_graph = value != 0;
   else if (k == "profile")
     ctx->opt_profile = value != 0;
-  else if (k == "reorder") {
-    if (ctx->inited) return fail(ctx, MMF_ESTATE, "reorder must be set before mmf_init");
-    ctx->opt_reorder = value != 0;
+  else if (k == "reorder" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+    if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
+    if (k == "reorder") ctx->opt_reorder = value != 0;
+    if (k == "kernels") {
+      if (value < 1 || value > 3) return fail(ctx, MMF_EINVAL, "kernels must be 1, 2 or 3");
+      ctx->opt_kernels = (int)value;
+    }
+    if (k == "tile") {
+      if (value < 1 || value > 256) return fail(ctx, MMF_EINVAL, "tile must be in [1, 256]");
+      ctx->opt_tile = (int)value;
+    }
+    if (k == "order") {
+      if (value < 0 || value > 2) return fail(ctx, MMF_EINVAL, "order must be 0, 1 or 2");
+      ctx->opt_order = (int)value;
+    }
+    if (k == "cpc") {
+      if (value < 0) return fail(ctx, MMF_EINVAL, "cpc must be >= 0");
+      ctx->opt_cpc = (int)value;
+    }
+    if (k == "halo") {
+      if (value < 0 || value > 4096) return fail(ctx, MMF_EINVAL, "halo must be in [0, 4096]");
+      ctx->opt_halo = (int)value;
+    }
+    if (k == "cpt") {
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+        return fail(ctx, MMF_EINVAL, "cpt must be 0, 1, 2, 4 or 8");
+      ctx->opt_cpt = (int)value;
+    }
+    ctx->prepared = false;
   } else
     return fail(ctx, MMF_EINVAL, "unknown option " + k);
   return MMF_OK;
@@ -754,6 +1166,7 @@ mmf_status mmf_set_graph(mmf_ctx* ctx, int32_t N, int64_t n_arcs, const int32_t*
   ctx->tail.assign(tail, tail + n_arcs);
   ctx->head.assign(head, head + n_arcs);
   ctx->have_cost = ctx->have_cap = false;
+  ctx->prepared = false;
   return MMF_OK;
 }
 
@@ -853,12 +1266,13 @@ mmf_status mmf_workspace_bytes(const mmf_ctx* cctx, size_t* bytes) {
   if (!cctx || !bytes) return MMF_EINVAL;
   mmf_ctx* ctx = const_cast<mmf_ctx*>(cctx);
   if (!ready_for_layout(ctx)) return fail(ctx, MMF_ESTATE, "graph, costs, capacity and marginals must be set");
-  DevPtrs saved = ctx->dp;
-  int mdi = ctx->maxdeg_in;
+  prepare(ctx);
   derive_shapes(ctx);
+  DevPtrs saved = ctx->dp;
+  TileMeta savedt = ctx->tm;
   *bytes = layout(ctx, nullptr);
   ctx->dp = saved;
-  ctx->maxdeg_in = mdi;
+  ctx->tm = savedt;
   return MMF_OK;
 }
 

@@ -25,8 +25,10 @@ template <> struct FPB<double> {
   static __device__ __forceinline__ double from(U u) { return __longlong_as_double((long long)u); }
 };
 
-// exponent of an exact zero; sums of two zero exponents and an arc exponent still fit in int32
-constexpr int EZERO = -30000;
+// exponent of an exact zero.  Stored message exponents lie in [-ELIM, ELIM] or equal EZERO, and arc
+// exponents used by the packed fp32 path are clamped to [-ELIM, ELIM], so a message exponent plus an
+// arc exponent always fits in int16 (the sm_100a 16x2 SIMD max-plus VIADDMNMX.S16x2 relies on it).
+constexpr int EZERO = -16384;
 // largest |e| a stored message may carry before MMF_ERANGE (int16 plane: +-16000)
 constexpr int ELIM = 16000;
 

@@ -132,3 +132,22 @@ def test_validation_errors():
         with pytest.raises(MMFError) as e:
             Solver(q, prec="fp64")
         assert e.value.name == "MMF_EINVAL"
+
+
+@pytest.mark.parametrize("prec,opts", [("fp32", dict(kernels=1)), ("fp64", dict(kernels=1)), ("fp32", dict(kernels=2)),
+                                       ("fp64", dict(kernels=2)), ("fp32", dict(kernels=2, cpt=4, tile=9)),
+                                       ("fp32", dict(kernels=2, cpc=1)), ("fp32", dict(cpt=1)), ("fp32", dict(cpt=2)),
+                                       ("fp32", dict(cpt=4)), ("fp32", dict(cpt=8)), ("fp64", dict(cpt=1)),
+                                       ("fp64", dict(cpt=2)), ("fp32", dict(tile=1)), ("fp32", dict(tile=7)),
+                                       ("fp64", dict(tile=128)), ("fp32", dict(reorder=0))])
+def test_kernel_variants(prec, opts):
+    """Every kernel configuration (reference per-node kernels, lane widths, tile sizes, no reordering)
+    meets the same parity bar; several tiles, several chunks and a ragged commodity tail."""
+    p = grid_problem(6, 7, 9, 150, 0.2, seed=26, cap=(0.3, 1.5))
+    assert_parity(p, 6, prec, options=opts)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_dense_time_varying_closed(prec):
+    p = grid_problem(5, 6, 7, 70, 0.25, seed=27, marginals="dense", time_varying=True, closed_arcs=2)
+    assert_parity(p, 8, prec)
