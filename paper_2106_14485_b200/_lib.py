@@ -41,8 +41,10 @@ class mmf_stats(C.Structure):
 _lib = None
 
 
-def load(path: str = LIB_PATH):
-    """Load libmmf.so (raises if it was not built: there is no fallback path)."""
+def load(path: str = None):
+    """Load libmmf.so (raises if it was not built: there is no fallback path).  MMF_LIB overrides the
+    path (profiling builds of the same sources)."""
+    path = path or os.environ.get("MMF_LIB", LIB_PATH)
     global _lib
     if _lib is not None:
         return _lib

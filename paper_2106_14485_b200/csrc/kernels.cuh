@@ -48,6 +48,26 @@ struct DevPtrs {
   unsigned* err;        // sticky error word
   unsigned long long* errloc;  // first error (commodity << 32 | node)
   double* stats;        // [8] accumulators
+  void* inrec;          // [T][A] ArcKW<M> per internal (in-CSR) arc: tail, K_t W_t      (or null)
+  void* outrec;         // [T][A] ArcKW<M> per out-CSR position: head, K_t W_t, arc id    (or null)
+  const int* opos;      // [A] internal arc -> out-CSR position
+};
+
+// per-step arc record: gathered node, arc factor K_t W_t as XF (km = 0: zero factor), aux word
+// (outrec: arc id, bit 31 set when the arc is uncapacitated at step t)
+template <class M> struct ArcKW;
+template <> struct __align__(16) ArcKW<float> {
+  int node;
+  int ke;
+  int aux;
+  float km;
+};
+template <> struct __align__(8) ArcKW<double> {
+  int node;
+  int ke;
+  int aux;
+  int pad;
+  double km;
 };
 
 template <class T_> struct View {
@@ -163,6 +183,43 @@ template <class T_> __global__ void k_flow(DevPtrs p, int t, int capped_only) {
 // capacity-dual update of one arc (eq:sinkhorn_graph_Vineq):
 //   W_t[a] <- min(W_t[a] d_t[a] / F_t[a], 1);  d = inf -> unchanged (= 1); d = 0 -> 0; F = 0 -> 1
 // computed in fp64 (one value per arc), stored as XF.
+// refresh the records of arc a at step t from K_t and the given W_t = (wm, we)
+template <class T_>
+__device__ __forceinline__ void write_recs(const DevPtrs& p, int t, int a, typename T_::M wm, int we) {
+  typedef typename T_::M M;
+  View<T_> v(p);
+  M m = v.Km(t)[a] * wm;
+  int e = v.Ke(t)[a] + we;
+  if (!(m > M(0)) || e < -ELIM) {
+    m = M(0);
+    e = -ELIM;
+  }
+  if (e > ELIM) e = ELIM;
+  ArcKW<M>* ir = (ArcKW<M>*)p.inrec + (size_t)t * p.A;
+  ArcKW<M>* orr = (ArcKW<M>*)p.outrec + (size_t)t * p.A;
+  const int q = p.opos[a];
+  ArcKW<M> r;
+  r.node = p.tail[a];
+  r.ke = e;
+  r.aux = 0;
+  r.km = m;
+  if constexpr (sizeof(M) == 8) r.pad = 0;
+  ir[a] = r;
+  r.node = p.out_head[q];
+  r.aux = a | (isinf(v.dcap(t)[a]) ? (int)0x80000000u : 0);
+  orr[q] = r;
+}
+
+template <class T_> __global__ void k_init_recs(DevPtrs p) {
+  typedef typename T_::M M;
+  View<T_> v(p);
+  const size_t n = (size_t)p.T * p.A;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(idx / p.A), a = (int)(idx % p.A);
+    write_recs<T_>(p, t, a, v.Wm(t)[a], v.We(t)[a]);
+  }
+}
+
 template <class T_> __device__ __forceinline__ void dual_update(const DevPtrs& p, int t, int a, double F) {
   typedef typename T_::M M;
   View<T_> v(p);
@@ -197,6 +254,7 @@ template <class T_> __device__ __forceinline__ void dual_update(const DevPtrs& p
   }
   Wm[a] = wm;
   We[a] = we;
+  if (p.inrec) write_recs<T_>(p, t, a, wm, we);
 }
 
 // sum the group partials of every arc: F[a] = sum_g part[g][a]

@@ -97,6 +97,7 @@ struct mmf_ctx {
   int opt_halo = 0;     // max in-/out-halo nodes per tile (0 = auto: 2 * tile)
   int opt_cpc = 0;      // commodity chunks per CTA (0 = auto)
   int opt_order = 2;    // node order (kernels >= 2): 0 input order, 1 reverse Cuthill-McKee, 2 BFS tiles
+  int opt_prefetch = 0; // wide kernels: L1 prefetch of significand rows in pass 1
 
   // ---- derived
   int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
@@ -341,6 +342,7 @@ void derive_shapes(mmf_ctx* c) {
     c->wc.npc = (WIDE_THREADS / 32) / cp;
     c->wc.ngroup = (c->nch + cp - 1) / cp;
     c->wc.nch = c->nch;
+    c->wc.prefetch = c->opt_prefetch;
     int mo = 0;
     if (!c->h_outptr.empty())
       for (int j0 = 0; j0 < c->N; j0 += c->wc.npc)
@@ -529,6 +531,13 @@ size_t layout(mmf_ctx* c, char* base) {
   c->wc.cnt = (int*)at(L.take(((size_t)c->N + 1) * 4));
   tm.part = at(L.take(A * (size_t)c->nch * sm));
   c->wc.part = tm.part;
+  {
+    const bool recs = c->opt_kernels == 3;
+    const size_t rb = c->prec == MMF_FP32 ? sizeof(ArcKW<float>) : sizeof(ArcKW<double>);
+    p.inrec = recs ? at(L.take(T * A * rb)) : nullptr;
+    p.outrec = recs ? at(L.take(T * A * rb)) : nullptr;
+    p.opos = (const int*)at(L.take(A * 4));
+  }
   tm.ntiles = c->ntiles;
   tm.max_hin = c->max_hin;
   tm.max_hout = c->max_hout;
@@ -820,6 +829,11 @@ template <class T_> struct Eng {
       size_t n = (size_t)c->T * c->A;
       k_init_w<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
     }
+    if (p.inrec) {
+      LaunchScope ls(c, K_OTHER, s);
+      size_t n = (size_t)c->T * c->A;
+      k_init_recs<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
+    }
     if (!c->point) {
       LaunchScope ls(c, K_OTHER, s);
       size_t n = (size_t)c->N * c->Lp;
@@ -961,6 +975,12 @@ mmf_status finalize(mmf_ctx* ctx) {
   CU(cudaMemcpyAsync((void*)p.out_ptr, c->h_outptr.data(), (N + 1) * 4, cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync((void*)p.out_arc, c->h_outarc.data(), A * 4, cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync((void*)p.out_head, c->h_outhead.data(), A * 4, cudaMemcpyHostToDevice, s));
+  {
+    std::vector<int> opos(A);
+    for (int64_t k = 0; k < A; ++k) opos[c->h_outarc[k]] = (int)k;
+    CU(cudaMemcpyAsync((void*)p.opos, opos.data(), A * 4, cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+  }
   {
     const TileMeta& tm = c->tm;
     const size_t nt = (size_t)c->ntiles;
@@ -1112,6 +1132,16 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_graph = value != 0;
   else if (k == "profile")
     ctx->opt_profile = value != 0;
+  else if (k == "prefetch") {
+    ctx->opt_prefetch = value != 0;
+    ctx->wc.prefetch = ctx->opt_prefetch;
+    if (ctx->gexec) {  // the captured graph bakes kernel arguments: recapture
+      cudaGraphExecDestroy(ctx->gexec);
+      cudaGraphDestroy(ctx->graph);
+      ctx->gexec = nullptr;
+      ctx->graph = nullptr;
+    }
+  }
   else if (k == "reorder" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;

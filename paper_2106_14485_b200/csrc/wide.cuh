@@ -30,10 +30,22 @@ struct WideCfg {
   int max_oa;  // largest out-arc count of a node group (shared-memory sizing)
   int* cnt;    // [node groups] arrival counters
   void* part;  // [A][ngroup] partial flows (M)
+  int prefetch;  // 1: pass 1 also prefetches the significand rows into L1
 };
 
 constexpr int WIDE_THREADS = 256;
 constexpr int WARP_ARCS = 64;  // arcs per warp scratch batch
+#ifndef MMF_U1
+#define MMF_U1 4  // unroll of the exponent pass (loads in flight per warp)
+#endif
+#ifndef MMF_U2
+#define MMF_U2 2  // unroll of the accumulation pass
+#endif
+constexpr int kUnroll1 = MMF_U1;
+constexpr int kUnroll2 = MMF_U2;
+#ifndef MMF_WIDE_MINB
+#define MMF_WIDE_MINB 3  // CTAs per SM the register budget is sized for
+#endif
 
 // compacted per-warp arc list: gathered node, K W factor, position of the arc (flow slot)
 template <class M> struct WarpArcs {
@@ -60,34 +72,28 @@ __device__ __forceinline__ void kw_factor(const View<T_>& v, int t, int a, typen
   if (e > ELIM) e = ELIM;
 }
 
-// Fill the warp scratch with arcs [k0, k0 + n) (n <= WARP_ARCS), keeping only those with a nonzero
-// factor (and, if cap_only, a finite capacity).  arc id = indirect ? arc_of[k] : k; gathered node =
-// node_arr[k]; pos = k - pos0.  Returns the kept count (warp-uniform).
-template <class T_>
-__device__ __forceinline__ int warp_arcs(const View<T_>& v, int t, const int* arc_of, const int* node_arr, int k0,
-                                         int n, int pos0, WarpArcs<typename T_::M>& w, int lane, bool indirect,
+// Fill the warp scratch with the records rec[k0, k0 + n) (n <= WARP_ARCS), keeping only arcs with a
+// nonzero factor (and, if cap_only, a finite capacity: aux bit 31 clear); pos = k - pos0.
+// One 16-byte record load per lane, no dependent loads.  Returns the kept count (warp-uniform).
+template <class M>
+__device__ __forceinline__ int warp_arcs(const ArcKW<M>* rec, int k0, int n, int pos0, WarpArcs<M>& w, int lane,
                                          bool cap_only) {
-  typedef typename T_::M M;
   int kept = 0;
   for (int base = 0; base < n; base += 32) {
     const int q = base + lane;
     bool keep = false;
-    M m = M(0);
-    int e = 0, nd = 0, k = k0 + q;
+    ArcKW<M> r;
     if (q < n) {
-      const int a = indirect ? arc_of[k] : k;
-      kw_factor<T_>(v, t, a, m, e);
-      keep = m > M(0);
-      if (cap_only && isinf(v.dcap(t)[a])) keep = false;
-      nd = node_arr[k];
+      r = rec[k0 + q];
+      keep = r.km > M(0) && !(cap_only && r.aux < 0);
     }
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (keep) {
       const int slot = kept + __popc(bal & ((1u << lane) - 1u));
-      w.node[slot] = nd;
-      w.ke[slot] = e;
-      w.pos[slot] = k - pos0;
-      w.km[slot] = m;
+      w.node[slot] = r.node;
+      w.ke[slot] = r.ke;
+      w.pos[slot] = k0 + q - pos0;
+      w.km[slot] = r.km;
     }
     kept += __popc(bal);
   }
@@ -98,7 +104,8 @@ __device__ __forceinline__ int warp_arcs(const View<T_>& v, int t, const int* ar
 // extended-range row sum over gathered global rows: out = sum_q KW_q x[node_q] (q < n, all nonzero)
 template <class T_, int CPT>
 __device__ __forceinline__ void gather_sum(const typename T_::M* gm, const typename T_::E* ge, int Lp, size_t col,
-                                          int n, const WarpArcs<typename T_::M>& w, typename T_::M* s, int* E) {
+                                          int n, const WarpArcs<typename T_::M>& w, typename T_::M* s, int* E,
+                                          int prefetch = 0) {
   typedef typename T_::M M;
   typedef typename T_::E Ex;
   if constexpr (sizeof(M) == 4 && sizeof(Ex) == 2 && CPT % 2 == 0) {
@@ -108,9 +115,10 @@ __device__ __forceinline__ void gather_sum(const typename T_::M* gm, const typen
 #pragma unroll
     for (int k = 0; k < NP; ++k) E2[k] = 0x80008000u;
     // pass 1: per-commodity max exponent (packed 16x2 max-plus)
-#pragma unroll 4
+#pragma unroll kUnroll1
     for (int q = 0; q < n; ++q) {
       const unsigned k2 = pack2(w.ke[q]);
+      if (prefetch) asm volatile("prefetch.global.L1 [%0];" ::"l"(gm + (size_t)w.node[q] * Lp + col));
       const VE ev = __ldg(reinterpret_cast<const VE*>(ge + (size_t)w.node[q] * Lp + col));
       const unsigned* ew = reinterpret_cast<const unsigned*>(&ev);
 #pragma unroll
@@ -128,7 +136,7 @@ __device__ __forceinline__ void gather_sum(const typename T_::M* gm, const typen
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.f;
     // pass 2: sum x * K W 2^(e - E)
-#pragma unroll 2
+#pragma unroll kUnroll2
     for (int q = 0; q < n; ++q) {
       const unsigned kb = __float_as_uint((float)w.km[q]);
       const int ke = w.ke[q];
@@ -163,21 +171,21 @@ __device__ __forceinline__ void gather_sum(const typename T_::M* gm, const typen
   }
 }
 
-// full SpMM row of one node (any degree: batches of WARP_ARCS through the scratch, merged in XF)
+// full SpMM row of one node over records rec[k0, k1) (any degree: batches of WARP_ARCS through the
+// scratch, merged in XF)
 template <class T_, int CPT>
-__device__ __forceinline__ void node_sum(const View<T_>& v, int t, const int* arc_of, const int* node_arr, int k0,
-                                        int k1, const typename T_::M* gm, const typename T_::E* ge, int Lp,
-                                        size_t col, WarpArcs<typename T_::M>& w, int lane, bool indirect,
-                                        typename T_::M* s, int* E) {
+__device__ __forceinline__ void node_sum(const ArcKW<typename T_::M>* rec, int k0, int k1, const typename T_::M* gm,
+                                        const typename T_::E* ge, int Lp, size_t col, WarpArcs<typename T_::M>& w,
+                                        int lane, typename T_::M* s, int* E, int prefetch) {
   typedef typename T_::M M;
   if (k1 - k0 <= WARP_ARCS) {
-    const int n = warp_arcs<T_>(v, t, arc_of, node_arr, k0, k1 - k0, k0, w, lane, indirect, false);
-    gather_sum<T_, CPT>(gm, ge, Lp, col, n, w, s, E);
+    const int n = warp_arcs<M>(rec, k0, k1 - k0, k0, w, lane, false);
+    gather_sum<T_, CPT>(gm, ge, Lp, col, n, w, s, E, prefetch);
     return;
   }
   XAcc<M> tot[CPT];
   for (int b = k0; b < k1; b += WARP_ARCS) {
-    const int n = warp_arcs<T_>(v, t, arc_of, node_arr, b, min(WARP_ARCS, k1 - b), b, w, lane, indirect, false);
+    const int n = warp_arcs<M>(rec, b, min(WARP_ARCS, k1 - b), b, w, lane, false);
     M bs[CPT];
     int bE[CPT];
     gather_sum<T_, CPT>(gm, ge, Lp, col, n, w, bs, bE);
@@ -195,7 +203,7 @@ __device__ __forceinline__ void node_sum(const View<T_>& v, int t, const int* ar
 // MODE 0: t = 0 (a2 fused, or U0 reload in readout); MODE 1: 0 < t < T; MODE 2: t = T (a4 fused)
 // FMODE: 0 dual update in place, 1 write Fsum (multi-GPU), 2 readout (Fout[t], all arcs)
 template <class T_, int CPT, int MODE, int FMODE>
-__global__ void __launch_bounds__(WIDE_THREADS) k_fwd_wide(DevPtrs p, WideCfg wc, int t) {
+__global__ void __launch_bounds__(WIDE_THREADS, MMF_WIDE_MINB) k_fwd_wide(DevPtrs p, WideCfg wc, int t) {
   typedef typename T_::M M;
   typedef typename T_::E E;
   constexpr int LC = 32 * CPT;
@@ -233,8 +241,8 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_fwd_wide(DevPtrs p, WideCfg wc
     } else {
       M s[CPT];
       int Ex[CPT];
-      node_sum<T_, CPT>(v, t - 1, nullptr, p.tail, p.in_ptr[j], p.in_ptr[j + 1], v.am(t - 1), v.ae(t - 1), p.Lp,
-                        col, wa, lane, false, s, Ex);
+      node_sum<T_, CPT>((const ArcKW<M>*)p.inrec + (size_t)(t - 1) * p.A, p.in_ptr[j], p.in_ptr[j + 1], v.am(t - 1),
+                        v.ae(t - 1), p.Lp, col, wa, lane, s, Ex, wc.prefetch);
       norm_lane<T_, CPT>(p, s, Ex, a, l0, j);
     }
     a.store(v.am(t) + g, v.ae(t) + g);
@@ -249,8 +257,8 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_fwd_wide(DevPtrs p, WideCfg wc
       const int k0 = p.out_ptr[j], k1 = p.out_ptr[j + 1];
       __syncwarp();
       for (int b = k0; b < k1; b += WARP_ARCS) {
-        const int n = warp_arcs<T_>(v, t, p.out_arc, p.out_head, b, min(WARP_ARCS, k1 - b), oq0, wa, lane, true,
-                                    FMODE != 2);
+        const int n = warp_arcs<M>((const ArcKW<M>*)p.outrec + (size_t)t * p.A, b, min(WARP_ARCS, k1 - b), oq0, wa,
+                                   lane, FMODE != 2);
         for (int q = 0; q < n; ++q) {
           const size_t gg = (size_t)wa.node[q] * p.Lp + col;
           Lane<M, E, CPT> bb;
@@ -308,7 +316,7 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_fwd_wide(DevPtrs p, WideCfg wc
 
 // backward step: beta_t[i] = sum_{a: i_a = i} K_t[a] W_t[a] beta_{t+1}[j_a]   (eq:psi P:1038-1043)
 template <class T_, int CPT>
-__global__ void __launch_bounds__(WIDE_THREADS) k_bwd_wide(DevPtrs p, WideCfg wc, int t) {
+__global__ void __launch_bounds__(WIDE_THREADS, MMF_WIDE_MINB) k_bwd_wide(DevPtrs p, WideCfg wc, int t) {
   typedef typename T_::M M;
   typedef typename T_::E E;
   constexpr int LC = 32 * CPT;
@@ -323,8 +331,8 @@ __global__ void __launch_bounds__(WIDE_THREADS) k_bwd_wide(DevPtrs p, WideCfg wc
   const int l0 = c * LC + lane * CPT;
   M s[CPT];
   int Ex[CPT];
-  node_sum<T_, CPT>(v, t, p.out_arc, p.out_head, p.out_ptr[i], p.out_ptr[i + 1], v.bm(t + 1), v.be(t + 1), p.Lp,
-                    col, wa, lane, true, s, Ex);
+  node_sum<T_, CPT>((const ArcKW<M>*)p.outrec + (size_t)t * p.A, p.out_ptr[i], p.out_ptr[i + 1], v.bm(t + 1),
+                    v.be(t + 1), p.Lp, col, wa, lane, s, Ex, wc.prefetch);
   Lane<M, E, CPT> out;
   norm_lane<T_, CPT>(p, s, Ex, out, l0, i);
   const size_t g = (size_t)i * p.Lp + col;
