@@ -51,6 +51,12 @@ struct DevPtrs {
   void* inrec;          // [T][A] ArcKW<M> per internal (in-CSR) arc: tail, K_t W_t      (or null)
   void* outrec;         // [T][A] ArcKW<M> per out-CSR position: head, K_t W_t, arc id    (or null)
   const int* opos;      // [A] internal arc -> out-CSR position
+  // ELL copies of the records for the pipelined kernels (or null): [T][N][D] per node, unused slots node = -1
+  void* ell_in;         // in-arcs of each head: node = tail, aux = arc id | uncapacitated bit
+  void* ell_out;        // out-arcs of each tail: node = head
+  const int* ell_ipos;  // [A] internal arc -> slot in ell_in (head * Din + k)
+  const int* ell_opos;  // [A] internal arc -> slot in ell_out (tail * Dout + k)
+  int Din, Dout;
 };
 
 // per-step arc record: gathered node, arc factor K_t W_t as XF (km = 0: zero factor), aux word
@@ -201,13 +207,19 @@ __device__ __forceinline__ void write_recs(const DevPtrs& p, int t, int a, typen
   ArcKW<M> r;
   r.node = p.tail[a];
   r.ke = e;
-  r.aux = 0;
   r.km = m;
   if constexpr (sizeof(M) == 8) r.pad = 0;
+  const int uncap = isinf(v.dcap(t)[a]) ? (int)0x80000000u : 0;  // bit 31: uncapacitated at step t
+  r.aux = uncap;
   ir[a] = r;
+  if (p.ell_in) {
+    r.aux = a | uncap;
+    ((ArcKW<M>*)p.ell_in)[(size_t)t * p.N * p.Din + p.ell_ipos[a]] = r;
+  }
   r.node = p.out_head[q];
-  r.aux = a | (isinf(v.dcap(t)[a]) ? (int)0x80000000u : 0);
+  r.aux = a | uncap;
   orr[q] = r;
+  if (p.ell_out) ((ArcKW<M>*)p.ell_out)[(size_t)t * p.N * p.Dout + p.ell_opos[a]] = r;
 }
 
 template <class T_> __global__ void k_init_recs(DevPtrs p) {

@@ -8,7 +8,7 @@
 #include "../../include/mmf.h"
 #include "kernels.cuh"
 #include "tiled.cuh"
-#include "wide.cuh"
+#include "pipefwd.cuh"
 
 #include <dlfcn.h>
 
@@ -91,7 +91,8 @@ struct mmf_ctx {
 
   // ---- options
   bool opt_graph = true, opt_reorder = true, opt_profile = false;
-  int opt_kernels = 3;  // 3 = wide-lane kernels (production), 2 = smem-staged tile kernels, 1 = per-node reference kernels
+  int opt_kernels = 5;  // 5 = TMA-pipelined backward + head-flow forward (production), 4 = register-gather head-flow
+                        // kernels, 3 = wide-lane kernels, 2 = smem-staged tile kernels, 1 = per-node reference kernels
   int opt_tile = 32;    // max nodes per tile
   int opt_cpt = 0;      // commodities per lane (0 = auto: 2 for fp32, 1 for fp64)
   int opt_halo = 0;     // max in-/out-halo nodes per tile (0 = auto: 2 * tile)
@@ -111,6 +112,12 @@ struct mmf_ctx {
   TileMeta tm{};
   PipeCfg pc{1, 1};
   WideCfg wc{};
+  HeadCfg hc{};
+  PipeCfg5 pb{};      // pipelined backward kernel (opt_kernels == 5)
+  PipeCfg5 pf{};      // pipelined forward kernel
+  bool pipe_bwd = false, pipe_fwd = false;
+  int ell_din = 0;
+  int sms = 148;
 
   // ---- device
   void* ws = nullptr;
@@ -322,7 +329,12 @@ void make_tiles(int N, const std::vector<int>& tail, const std::vector<int>& hea
 
 void derive_shapes(mmf_ctx* c) {
   int cpt_auto = c->prec == MMF_FP32 ? 2 : 1;
-  if (c->opt_kernels == 3) {
+  if (c->opt_kernels == 4) {  // register-gather path: 4 fp32 commodities per lane keep 6 rows in registers
+    if (c->prec == MMF_FP32)
+      cpt_auto = c->L >= 128 ? 4 : 2;
+    else
+      cpt_auto = c->L >= 64 ? 2 : 1;
+  } else if (c->opt_kernels == 3 || c->opt_kernels == 5) {
     if (c->prec == MMF_FP32)
       cpt_auto = c->L >= 512 ? 8 : (c->L >= 128 ? 4 : 2);
     else
@@ -333,6 +345,49 @@ void derive_shapes(mmf_ctx* c) {
   if (c->opt_kernels == 2) c->CPT = std::min(c->CPT, 4);   // tile kernels: instantiated for 1, 2, 4
   c->LC = 32 * c->CPT;
   c->Lp = ((c->L + c->LC - 1) / c->LC) * c->LC;
+  // pipelined backward (fp32, ELL width <= 32): slice width SW = 256 * cp commodities, S stages of
+  // Dout rows x SW x 6 B in shared memory; the message row length Lp is padded to a multiple of SW
+  c->pipe_bwd = false;
+  if (c->opt_kernels == 5 && c->prec == MMF_FP32 && c->pb.D > 0 && c->pb.D <= 32 && c->L >= 256) {
+    // slice width SW = 256 * cp; the row ring holds R rows of SW (6 B each); want >= ~6 average items
+    // in flight (A / N rows each) plus one worst-case item
+    const size_t budget = 220 * 1024;
+    const int L256 = (c->L + 255) / 256 * 256;
+    const double avg = (double)c->A / std::max(c->N, 1);
+    const int SD = PIPE_SD;
+    auto rows_fit = [&](int SW) {
+      int R = 0;
+      while (pipe_smem(R + 1, SD, c->pb.D, SW).total <= budget) ++R;
+      return R;
+    };
+    int cp = 4;
+    while (cp > 1 && (256 * cp > L256 || rows_fit(256 * cp) < c->pb.D + (int)(4 * avg))) cp >>= 1;
+    const int SW = 256 * cp;
+    const int R = rows_fit(SW);
+    if (R >= c->pb.D) {
+      c->pipe_bwd = true;
+      c->pb.SW = SW;
+      c->pb.R = R;
+      c->pb.SD = SD;
+      const int q = std::max(SW, c->LC);
+      c->Lp = (c->L + q - 1) / q * q;
+      c->pb.ns = c->Lp / SW;
+      c->pb.nitems = c->N * c->pb.ns;
+    }
+  }
+  // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width)
+  c->pipe_fwd = false;
+  if (c->pipe_bwd && c->pb.ns == 1 && c->ell_din > 0 && c->ell_din <= 32) {
+    const size_t budget = 220 * 1024;
+    int R = 0;
+    while (pfwd_smem(R + 1, c->ell_din, c->pb.SW).total <= budget) ++R;
+    if (R >= c->ell_din + 1) {
+      c->pipe_fwd = true;
+      c->pf = c->pb;
+      c->pf.D = c->ell_din;
+      c->pf.R = R;
+    }
+  }
   c->nch = c->Lp / c->LC;
   // wide path: warps = (nodes per CTA) x (chunks per CTA) = 8
   {
@@ -348,6 +403,18 @@ void derive_shapes(mmf_ctx* c) {
       for (int j0 = 0; j0 < c->N; j0 += c->wc.npc)
         mo = std::max(mo, c->h_outptr[std::min(j0 + c->wc.npc, c->N)] - c->h_outptr[j0]);
     c->wc.max_oa = mo;
+  }
+  // head-flow path: all chunks of a node in one CTA
+  {
+    HeadCfg& h = c->hc;
+    h.nch = c->nch;
+    h.wpn = c->nch <= HF_WARPS ? c->nch : HF_WARPS;
+    h.npc = c->nch <= HF_WARPS ? std::max(1, HF_WARPS / c->nch) : 1;
+    int mi = 0;
+    if (!c->h_inptr.empty())
+      for (int j0 = 0; j0 < c->N; j0 += h.npc)
+        mi = std::max(mi, c->h_inptr[std::min(j0 + h.npc, c->N)] - c->h_inptr[j0]);
+    h.max_ia = std::max(mi, 1);
   }
   // chunk groups per tile: enough CTAs for ~4 per SM, each CTA pipelining cpc chunks
   {
@@ -434,6 +501,13 @@ void prepare(mmf_ctx* c) {
     c->h_outptr[c->h_tail[ordo[k]] + 1]++;
   }
   for (int v = 0; v < N; ++v) c->h_outptr[v + 1] += c->h_outptr[v];
+  c->pb.D = 0;
+  int din = 0;
+  for (int v = 0; v < N; ++v) {
+    c->pb.D = std::max(c->pb.D, c->h_outptr[v + 1] - c->h_outptr[v]);
+    din = std::max(din, c->h_inptr[v + 1] - c->h_inptr[v]);
+  }
+  c->ell_din = din;
 
   // halos
   std::vector<int> tile_of(N);
@@ -532,11 +606,18 @@ size_t layout(mmf_ctx* c, char* base) {
   tm.part = at(L.take(A * (size_t)c->nch * sm));
   c->wc.part = tm.part;
   {
-    const bool recs = c->opt_kernels == 3;
+    const bool recs = c->opt_kernels >= 3;
     const size_t rb = c->prec == MMF_FP32 ? sizeof(ArcKW<float>) : sizeof(ArcKW<double>);
     p.inrec = recs ? at(L.take(T * A * rb)) : nullptr;
     p.outrec = recs ? at(L.take(T * A * rb)) : nullptr;
     p.opos = (const int*)at(L.take(A * 4));
+    const bool ell = c->pipe_bwd;
+    p.Din = ell ? c->ell_din : 0;
+    p.Dout = ell ? c->pb.D : 0;
+    p.ell_in = ell ? at(L.take(T * N * (size_t)p.Din * 16)) : nullptr;
+    p.ell_out = ell ? at(L.take(T * N * (size_t)p.Dout * 16)) : nullptr;
+    p.ell_ipos = ell ? (const int*)at(L.take(A * 4)) : nullptr;
+    p.ell_opos = ell ? (const int*)at(L.take(A * 4)) : nullptr;
   }
   tm.ntiles = c->ntiles;
   tm.max_hin = c->max_hin;
@@ -750,9 +831,38 @@ template <class T_> struct Eng {
     dim3 grid((c->N + c->wc.npc - 1) / c->wc.npc, c->wc.ngroup);
     k_bwd_wide<T_, CPT><<<grid, WIDE_THREADS, wide_smem<M>(0, 1), s>>>(c->dp, c->wc, t);
   }
+  // ---------------- head-flow register-gather path (opt_kernels == 4)
+  template <int CPT, int MODE, bool KEEP> static void launch_fwd_head(mmf_ctx* c, cudaStream_t s, int t) {
+    const HeadCfg& h = c->hc;
+    dim3 grid((c->N + h.npc - 1) / h.npc);
+    k_fwd_head<T_, CPT, MODE, KEEP><<<grid, h.npc * h.wpn * 32, head_smem<M>(h.max_ia, h.nch), s>>>(c->dp, h, t);
+  }
+  template <int CPT> static void head_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
+    const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
+    const bool keep = c->hc.nch <= HF_WARPS;
+    switch (mode * 2 + (keep ? 1 : 0)) {
+      case 0: launch_fwd_head<CPT, 0, false>(c, s, t); break;
+      case 1: launch_fwd_head<CPT, 0, true>(c, s, t); break;
+      case 2: launch_fwd_head<CPT, 1, false>(c, s, t); break;
+      case 3: launch_fwd_head<CPT, 1, true>(c, s, t); break;
+      case 4: launch_fwd_head<CPT, 2, false>(c, s, t); break;
+      default: launch_fwd_head<CPT, 2, true>(c, s, t); break;
+    }
+  }
+  static void head_fwd(mmf_ctx* c, cudaStream_t s, int t) {
+    LaunchScope ls(c, K_FUSED, s);
+    if (c->CPT == 1) head_fwd_cpt<1>(c, s, t);
+    else if (c->CPT == 2 || !is_f32()) head_fwd_cpt<2>(c, s, t);
+    else if (c->CPT == 4) head_fwd_cpt<is_f32() ? 4 : 2>(c, s, t);
+    else head_fwd_cpt<is_f32() ? 8 : 2>(c, s, t);
+  }
+  template <int CPT> static void head_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
+    const size_t warps = (size_t)c->N * c->hc.nch;
+    k_bwd_head<T_, CPT><<<(unsigned)((warps + HF_WARPS - 1) / HF_WARPS), HF_WARPS * 32, 0, s>>>(c->dp, c->hc, t);
+  }
   static void tiled_fwd(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
     LaunchScope ls(c, K_FUSED, s);
-    if (c->opt_kernels == 3) {
+    if (c->opt_kernels >= 3) {
       if (c->CPT == 1) wide_fwd_cpt<1>(c, s, t, fmode);
       else if (c->CPT == 2 || !is_f32()) wide_fwd_cpt<2>(c, s, t, fmode);
       else if (c->CPT == 4) wide_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
@@ -763,8 +873,48 @@ template <class T_> struct Eng {
     else if (c->CPT == 2) tiled_fwd_cpt<2>(c, s, t, fmode);
     else tiled_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
   }
+  template <int CPT, int MODE> static void pipe_fwd_launch(mmf_ctx* c, cudaStream_t s, int t) {
+    const PipeCfg5& pc = c->pf;
+    const unsigned grid = (unsigned)std::min(c->N, c->sms);
+    k_fwd_pipe<CPT, MODE><<<grid, PIPE_THREADS, pfwd_smem(pc.R, pc.D, pc.SW).total, s>>>(c->dp, pc, t);
+  }
+  static void pipe_fwd(mmf_ctx* c, cudaStream_t s, int t) {
+    if constexpr (sizeof(M) == 4) {
+      if (t == 0) {  // a2: elementwise, the head kernel's MODE 0
+        head_fwd(c, s, 0);
+        return;
+      }
+      LaunchScope ls(c, K_FUSED, s);
+      const int cp = c->pf.SW / 256;
+      const bool last = t == c->T;
+      if (cp == 4) last ? pipe_fwd_launch<4, 2>(c, s, t) : pipe_fwd_launch<4, 1>(c, s, t);
+      else if (cp == 2) last ? pipe_fwd_launch<2, 2>(c, s, t) : pipe_fwd_launch<2, 1>(c, s, t);
+      else last ? pipe_fwd_launch<1, 2>(c, s, t) : pipe_fwd_launch<1, 1>(c, s, t);
+    }
+  }
+  template <int CPT> static void pipe_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
+    const PipeCfg5& pc = c->pb;
+    const unsigned grid = (unsigned)std::min(pc.nitems, c->sms);
+    k_bwd_pipe<CPT><<<grid, PIPE_THREADS, pipe_smem(pc.R, pc.SD, pc.D, pc.SW).total, s>>>(c->dp, pc, t);
+  }
   static void tiled_bwd(mmf_ctx* c, cudaStream_t s, int t) {
     LaunchScope ls(c, K_BWD, s);
+    if constexpr (sizeof(M) == 4) {
+      if (c->pipe_bwd) {
+        const int cp = c->pb.SW / 256;
+        if (cp == 4) pipe_bwd_cpt<4>(c, s, t);
+        else if (cp == 2) pipe_bwd_cpt<2>(c, s, t);
+        else pipe_bwd_cpt<1>(c, s, t);
+        return;
+      }
+    }
+    if (c->opt_kernels >= 4) {
+      if (c->CPT == 1) head_bwd_cpt<1>(c, s, t);
+      else if (c->CPT == 2 || !is_f32()) head_bwd_cpt<2>(c, s, t);
+      else if (c->CPT == 4) head_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
+      else head_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
+      return;
+    }
     if (c->opt_kernels == 3) {
       if (c->CPT == 1) wide_bwd_cpt<1>(c, s, t);
       else if (c->CPT == 2 || !is_f32()) wide_bwd_cpt<2>(c, s, t);
@@ -795,6 +945,16 @@ template <class T_> struct Eng {
   }
 
   static mmf_status enqueue_sweep(mmf_ctx* c, cudaStream_t s) {
+    if (c->opt_kernels == 5 && c->pipe_fwd && !c->comm) {
+      for (int t = 0; t <= c->T; ++t) pipe_fwd(c, s, t);       // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
+      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      return MMF_OK;
+    }
+    if (c->opt_kernels == 4 && !c->comm) {
+      for (int t = 0; t <= c->T; ++t) head_fwd(c, s, t);       // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
+      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      return MMF_OK;
+    }
     if (c->opt_kernels >= 2) {
       const int fmode = c->comm ? 1 : 0;
       for (int t = 0; t <= c->T; ++t) {  // a2 fused in t = 0, a4 fused in t = T
@@ -823,6 +983,23 @@ template <class T_> struct Eng {
     if (c->opt_kernels == 2) {
       mmf_status st = tiled_attrs(c);
       if (st != MMF_OK) return st;
+    }
+    if constexpr (sizeof(M) == 4) {
+      if (c->pipe_bwd) {
+        const int sm = (int)pipe_smem(c->pb.R, c->pb.SD, c->pb.D, c->pb.SW).total;
+        CU(cudaFuncSetAttribute(k_bwd_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_bwd_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_bwd_pipe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      }
+      if (c->pipe_fwd) {
+        const int sm = (int)pfwd_smem(c->pf.R, c->pf.D, c->pf.SW).total;
+        CU(cudaFuncSetAttribute(k_fwd_pipe<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_fwd_pipe<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_fwd_pipe<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_fwd_pipe<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_fwd_pipe<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_fwd_pipe<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+      }
     }
     {
       LaunchScope ls(c, K_OTHER, s);
@@ -853,6 +1030,11 @@ template <class T_> struct Eng {
   static mmf_status readout(mmf_ctx* ctx, cudaStream_t s) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
+    if (c->pipe_fwd && p.inrec) {  // the pipelined forward kernel maintains only the ELL records
+      LaunchScope ls(c, K_OTHER, s);
+      size_t n = (size_t)c->T * c->A;
+      k_init_recs<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
+    }
     if (c->opt_kernels >= 2) {
       for (int t = 0; t <= c->T; ++t) {
         tiled_fwd(c, s, t, 2);
@@ -979,6 +1161,21 @@ mmf_status finalize(mmf_ctx* ctx) {
     std::vector<int> opos(A);
     for (int64_t k = 0; k < A; ++k) opos[c->h_outarc[k]] = (int)k;
     CU(cudaMemcpyAsync((void*)p.opos, opos.data(), A * 4, cudaMemcpyHostToDevice, s));
+    std::vector<int> eip, eop;
+    if (p.ell_in) {
+      eip.resize(A);
+      eop.resize(A);
+      for (int64_t k = 0; k < A; ++k) {
+        const int hd = c->h_head[k], tl = c->h_tail[k];
+        eip[k] = hd * p.Din + (int)(k - c->h_inptr[hd]);
+        eop[k] = tl * p.Dout + (opos[k] - c->h_outptr[tl]);
+      }
+      CU(cudaMemcpyAsync((void*)p.ell_ipos, eip.data(), A * 4, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync((void*)p.ell_opos, eop.data(), A * 4, cudaMemcpyHostToDevice, s));
+      // unused ELL slots: node = -1, km = NaN (never > 0)
+      CU(cudaMemsetAsync(p.ell_in, 0xff, (size_t)c->T * N * p.Din * 16, s));
+      CU(cudaMemsetAsync(p.ell_out, 0xff, (size_t)c->T * N * p.Dout * 16, s));
+    }
     CU(cudaStreamSynchronize(s));
   }
   {
@@ -1113,6 +1310,8 @@ mmf_status mmf_create(mmf_ctx** out, int device, mmf_prec prec, void* cuda_strea
   mmf_ctx* c = new mmf_ctx();
   c->device = device;
   c->prec = prec;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  if (c->sms <= 0) c->sms = 148;
   c->stream = (cudaStream_t)cuda_stream;
   if (cudaStreamCreateWithFlags(&c->priv, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_user, cudaEventDisableTiming) != cudaSuccess ||
@@ -1146,7 +1345,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "kernels") {
-      if (value < 1 || value > 3) return fail(ctx, MMF_EINVAL, "kernels must be 1, 2 or 3");
+      if (value < 1 || value > 5) return fail(ctx, MMF_EINVAL, "kernels must be 1, 2, 3, 4 or 5");
       ctx->opt_kernels = (int)value;
     }
     if (k == "tile") {
@@ -1514,22 +1713,27 @@ mmf_status mmf_read_kernel_stats(mmf_ctx* ctx, int64_t* launches, double* ms, in
 
 mmf_status mmf_sweep_bytes(const mmf_ctx* ctx, double* total, double* per_kind, int n) {
   if (!ctx) return MMF_EINVAL;
-  // SURVEY §8(d) byte model with B_e = significand + exponent bytes, true L (not padded):
-  //   bwd step : read beta_{t+1}, write beta_t            = 2 N L B_e + arc data
-  //   fwd flow : read alpha_t, beta_{t+1}                 = 2 N L B_e
-  //   fwd spmm : read alpha_t, write alpha_{t+1}          = 2 N L B_e
-  // (a fused forward kernel needs 3 N L B_e: alpha_t once, beta_{t+1}, alpha_{t+1})
+  // Algorithmic bytes (SURVEY §8(d) byte model; what the method must move with no cross-step reuse), with
+  // B_e = significand + exponent bytes of a message element, B_w = W significand + exponent, true L:
+  //   forward step : read alpha_{t-1}, read beta_t, write alpha_t  = 3 N L B_e + 2 |A| B_w (W read + write)
+  //   backward step: read beta_{t+1}, write beta_t                 = 2 N L B_e +   |A| B_w
+  //   boundaries   : 4 N L B_e for dense marginals (a2 / a4), ~0 for point masses
+  // per sweep = T (5 N L B_e + 3 |A| B_w) + boundaries.  Per-kind entries attribute the same bytes to the
+  // kernel kinds of the production path (fused forward, backward); the split reference kernels
+  // (kernels=1) get their own shares for their attribution passes.
   const double Be = (double)(ctx->sm() + ctx->se());
   const double NL = (double)ctx->N * ctx->L;
-  const double arcs = (double)ctx->A * (ctx->sm() + 4) * 2;  // K and W significand + exponent
+  const double Bw = (double)(ctx->sm() + 4);
+  const double A = (double)ctx->A;
+  const double bnd = ctx->point ? 0.0 : 4 * NL * Be;
   double k[K_NKINDS] = {};
-  k[K_BWD] = ctx->T * (2 * NL * Be + arcs);
-  k[K_FLOW] = ctx->T * (2 * NL * Be + arcs);
-  k[K_UPDATE] = ctx->T * (2 * NL * Be + arcs);
-  k[K_REDUCE] = ctx->T * ((double)ctx->G * ctx->A * ctx->sm() + arcs);
-  k[K_BOUNDARY] = ctx->point ? 2 * NL * Be : 6 * NL * Be;
-  k[K_FUSED] = ctx->T * (3 * NL * Be + arcs);
-  double tot = k[K_BWD] + k[K_FLOW] + k[K_UPDATE] + k[K_REDUCE] + k[K_BOUNDARY];
+  k[K_FUSED] = ctx->T * (3 * NL * Be + 2 * A * Bw) + bnd;
+  k[K_BWD] = ctx->T * (2 * NL * Be + A * Bw);
+  k[K_FLOW] = ctx->T * (2 * NL * Be + A * Bw);
+  k[K_UPDATE] = ctx->T * (2 * NL * Be + A * Bw);
+  k[K_REDUCE] = ctx->T * (2 * A * Bw);
+  k[K_BOUNDARY] = bnd;
+  const double tot = ctx->T * (5 * NL * Be + 3 * A * Bw) + bnd;
   if (total) *total = tot;
   for (int q = 0; q < n && q < K_NKINDS; ++q)
     if (per_kind) per_kind[q] = k[q];

@@ -139,7 +139,9 @@ def test_validation_errors():
                                        ("fp32", dict(kernels=2, cpc=1)), ("fp32", dict(cpt=1)), ("fp32", dict(cpt=2)),
                                        ("fp32", dict(cpt=4)), ("fp32", dict(cpt=8)), ("fp64", dict(cpt=1)),
                                        ("fp64", dict(cpt=2)), ("fp32", dict(tile=1)), ("fp32", dict(tile=7)),
-                                       ("fp64", dict(tile=128)), ("fp32", dict(reorder=0))])
+                                       ("fp64", dict(tile=128)), ("fp32", dict(reorder=0)),
+                                       ("fp32", dict(kernels=3)), ("fp64", dict(kernels=3)),
+                                       ("fp32", dict(kernels=3, cpt=8)), ("fp32", dict(kernels=4, cpt=8))])
 def test_kernel_variants(prec, opts):
     """Every kernel configuration (reference per-node kernels, lane widths, tile sizes, no reordering)
     meets the same parity bar; several tiles, several chunks and a ragged commodity tail."""
@@ -151,3 +153,42 @@ def test_kernel_variants(prec, opts):
 def test_dense_time_varying_closed(prec):
     p = grid_problem(5, 6, 7, 70, 0.25, seed=27, marginals="dense", time_varying=True, closed_arcs=2)
     assert_parity(p, 8, prec)
+
+
+@pytest.mark.parametrize("prec,cpt", [("fp32", 1), ("fp32", 2), ("fp64", 1)])
+def test_many_chunks_streaming_path(prec, cpt):
+    """More than 8 commodity chunks per node: the forward kernel's warps loop over chunks and re-gather
+    (no register-held rows); also nodes of in-degree above the register batch (the 3x3 grid has degree 5)."""
+    p = grid_problem(5, 6, 7, 300, 0.25, seed=28, cap=(0.2, 0.8))
+    assert_parity(p, 6, prec, options=dict(cpt=cpt))
+
+
+FIXTURES = [("cfg3", 3, "fp32"), ("cfg3", 10, "fp32"), ("cfg4lite", 3, "fp32"), ("cfg4lite", 20, "fp32"),
+            ("cfg5lite", 3, "fp32"), ("cfg5lite", 20, "fp32"), ("cfg4pipe", 2, "fp32"), ("cfg5pipe", 3, "fp32"),
+            ("cfg2", 100, "fp64"), ("cfg2", 100, "fp32")]
+
+
+@pytest.mark.parametrize("name,k,prec", FIXTURES)
+def test_config_parity_against_stored_oracle(name, k, prec):
+    """BASELINE configs too slow for a live oracle: the GPU path (default launch configuration, as
+    bench.py runs it) vs the float64 oracle's outputs stored by tests/golden/make_oracle_fixtures.py
+    (which calls only oracle/ and workloads/), on 20,000 uniformly sampled (t, a) entries.
+    cfg3 = config [3] at full size; cfg4pipe / cfg5pipe = the full [4] / [5] graphs at L >= 256 (the
+    pipelined kernels' slice widths) on short horizons; *lite = the full graphs and horizons at small L."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"fixture {name} not generated")
+    z = np.load(path)
+    if f"F_{k}" not in z:
+        pytest.skip(f"fixture {name} has no snapshot {k}")
+    from tests.golden.make_oracle_fixtures import JOBS
+    cfg, kw, _ = JOBS[name]
+    p = gen(cfg, **kw)
+    assert (p.L, p.T, p.A, p.N) == (int(z["L"]), int(z["T"]), int(z["A"]), int(z["N"]))
+    Fg, Wg, sg = run_gpu(p, k, prec)
+    idx = z["idx"]
+    ef = max_rel_err(Fg.reshape(-1)[idx], z[f"F_{k}"], flow_floor(p))
+    ew = max_rel_err(Wg.reshape(-1)[idx], z[f"W_{k}"], W_FLOOR)
+    assert ef < TOL[prec] and ew < TOL[prec], (name, k, ef, ew)
+    assert abs(sg["mass"] - float(z[f"mass_{k}"])) <= 10 * TOL[prec] * abs(float(z[f"mass_{k}"]))
