@@ -209,8 +209,15 @@ def main():
     dom_bytes_per_launch = bytes_kind[dom] / max(kinds[dom]["launches"] / args.steps, 1)
     peak, peak_kind = measured_peaks()
     achieved = dom_bytes_per_launch / (dom_launch_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    if os.path.exists(tpath):  # ncu dram bytes per launch of the same kernel (committed capture)
+        with open(tpath) as f:
+            tj = json.load(f).get(dom)
+        if tj:
+            traffic = tj["dram_read"] + tj["dram_write"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "peak_source": peak_kind, "traffic": None,
+            "frac": achieved / peak, "peak_source": peak_kind, "traffic": traffic,
             "share_of_step": kinds[dom]["ms"] / tot_ms,
             "bytes_per_launch": dom_bytes_per_launch, "avg_launch_ms": dom_launch_ms}
     sweep_gbs = bytes_total / (ms_step / 1e3) / 1e9 * (p.L and (l1 - l0) / p.L or 1)

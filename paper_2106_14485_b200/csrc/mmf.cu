@@ -99,6 +99,8 @@ struct mmf_ctx {
   int opt_cpc = 0;      // commodity chunks per CTA (0 = auto)
   int opt_order = 2;    // node order (kernels >= 2): 0 input order, 1 reverse Cuthill-McKee, 2 BFS tiles
   int opt_prefetch = 0; // wide kernels: L1 prefetch of significand rows in pass 1
+  int opt_dry = 0;      // diagnostics: pipelined backward consumers skip the arithmetic
+  int opt_copy = 0;     // pipelined kernels' row staging: 0 = TMA bulk copies, 1 = per-lane cp.async
 
   // ---- derived
   int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
@@ -364,11 +366,13 @@ void derive_shapes(mmf_ctx* c) {
     while (cp > 1 && (256 * cp > L256 || rows_fit(256 * cp) < c->pb.D + (int)(4 * avg))) cp >>= 1;
     const int SW = 256 * cp;
     const int R = rows_fit(SW);
-    if (R >= c->pb.D) {
+    if (R >= 2 * c->pb.D) {  // contiguous items: any item fits once the older ones are released
       c->pipe_bwd = true;
       c->pb.SW = SW;
       c->pb.R = R;
       c->pb.SD = SD;
+      c->pb.dry = c->opt_dry;
+      c->pb.copy = c->opt_copy;
       const int q = std::max(SW, c->LC);
       c->Lp = (c->L + q - 1) / q * q;
       c->pb.ns = c->Lp / SW;
@@ -381,7 +385,7 @@ void derive_shapes(mmf_ctx* c) {
     const size_t budget = 220 * 1024;
     int R = 0;
     while (pfwd_smem(R + 1, c->ell_din, c->pb.SW).total <= budget) ++R;
-    if (R >= c->ell_din + 1) {
+    if (R >= 2 * (c->ell_din + 1)) {
       c->pipe_fwd = true;
       c->pf = c->pb;
       c->pf.D = c->ell_din;
@@ -1341,9 +1345,11 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
+    if (k == "dry") ctx->opt_dry = (int)value;
+    if (k == "copy") ctx->opt_copy = (int)value;
     if (k == "kernels") {
       if (value < 1 || value > 5) return fail(ctx, MMF_EINVAL, "kernels must be 1, 2, 3, 4 or 5");
       ctx->opt_kernels = (int)value;
@@ -1702,8 +1708,12 @@ mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {
 
 mmf_status mmf_read_kernel_stats(mmf_ctx* ctx, int64_t* launches, double* ms, int n) {
   if (!ctx) return MMF_EINVAL;
-  mmf_status st = mmf_sync(ctx);
-  if (st != MMF_OK) return st;
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->stream));  // (accounting only: sticky solver errors surface at mmf_sync)
+  if (ctx->inited) {
+    mmf_status st = collect_profile(ctx);
+    if (st != MMF_OK) return st;
+  }
   for (int k = 0; k < n && k < K_NKINDS; ++k) {
     if (launches) launches[k] = ctx->launches[k];
     if (ms) ms[k] = ctx->ms[k];

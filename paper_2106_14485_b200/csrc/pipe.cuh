@@ -7,9 +7,10 @@
 //   * the arc records of upcoming items (ELL layout [T][N][D], no CSR pointer round trip) are prefetched
 //     P items ahead with cp.async into a small ring;
 //   * the neighbour rows of an item (slice of SW commodities of each gathered node: significand plane +
-//     exponent plane) are fetched with cp.async.bulk (TMA bulk copies, SASS UBLKCP) into an S-stage
-//     shared-memory ring, completion tracked by mbarrier transaction counts;
-// and NWC consumer warps compute from shared memory and release the stage.  Work items are visited in
+//     exponent plane) are fetched with cp.async.bulk (TMA bulk copies, SASS UBLKCP) into a ring of R row
+//     slots in shared memory (an item's rows are contiguous), completion tracked by mbarrier transaction
+//     counts in a ring of item descriptors;
+// and consumer warps compute from shared memory and release the item.  Work items are visited in
 // grid-stride order (item = blockIdx.x + k * gridDim.x over node-major (node, slice) pairs), so at any
 // moment the whole GPU works on a narrow band of consecutive nodes: a gathered row is reused from L2 by
 // the neighbouring nodes' CTAs while it is still resident (nodes are numbered for locality).
@@ -20,33 +21,16 @@
 
 namespace mmf {
 
-constexpr int PIPE_NWC = 8;                       // consumer warps per group (one group = one item)
-constexpr int PIPE_NG = 2;                        // consumer groups (alternate items)
+constexpr int PIPE_NWC = 8;                                  // consumer warps per group (one group = one item)
+constexpr int PIPE_NG = 2;                                   // consumer groups (alternate items)
 constexpr int PIPE_THREADS = (PIPE_NWC * PIPE_NG + 1) * 32;  // + one producer warp
-constexpr int PIPE_P = 12;                        // record prefetch distance (items)
-constexpr int PIPE_RP = 16;                       // record ring slots (> PIPE_P)
-constexpr int PIPE_NR = 8;                        // rows a consumer holds in registers (fast path)
-constexpr int PIPE_SD = 16;                       // item descriptors (power of two)
+constexpr int PIPE_P = 12;                                   // record prefetch distance (items)
+constexpr int PIPE_RP = 16;                                  // record ring slots (> PIPE_P)
+constexpr int PIPE_NR = 8;                                   // rows a consumer holds in registers (fast path)
+constexpr int PIPE_SD = 16;                                  // item descriptors (power of two)
 
-// grid-stride walk over node-major (node, slice) items without divisions in the loop
-struct ItemIt {
-  int node, sl, dn, ds, ns;
-  __device__ __forceinline__ void init(int item0, int step, int ns_) {
-    ns = ns_;
-    node = item0 / ns;
-    sl = item0 - node * ns;
-    dn = step / ns;
-    ds = step - dn * ns;
-  }
-  __device__ __forceinline__ void next() {
-    node += dn;
-    sl += ds;
-    if (sl >= ns) {
-      sl -= ns;
-      ++node;
-    }
-  }
-};
+// slice width of the pipelined kernels: 8 consumer warps x 32 lanes x CPT commodities
+template <int CPT> constexpr int pipe_sw() { return 32 * CPT * PIPE_NWC; }
 
 struct PipeCfg5 {
   int R;       // row slots in the shared-memory ring (each SW significands + SW exponents)
@@ -55,15 +39,17 @@ struct PipeCfg5 {
   int SW;      // commodities per item (slice) = 32 * CPT * PIPE_NWC
   int ns;      // slices per node = Lp / SW
   int nitems;  // N * ns
+  int dry;     // diagnostics: consumers only wait and release (measures the producer / TMA delivery rate)
+  int copy;    // row staging: 0 = cp.async.bulk (TMA, one per row plane), 1 = cp.async 16 B per lane (LDGSTS)
 };
 
-// item descriptor: the n present rows (compacted, nonzero factor; ring slots start .. start + n - 1 mod R)
-// and their arc factors K W
+// item descriptor: the n present rows (compacted, nonzero factor; ring slots start .. start + n - 1, never
+// wrapping) and their arc factors K W (bits of the significand, exponent packed twice as int16x2)
 struct PipeHdr {
-  float km[32];
-  int ke[32];
+  unsigned kb[32];
+  unsigned k2[32];
   int n;
-  int start;  // first ring slot (mod R)
+  int start;  // first ring slot
   int end;    // producer's monotonic slot counter after this item
   int pad;
 };
@@ -104,121 +90,207 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// lane-row of a stage: CPT significands + CPT int16 exponents (packed two per word when CPT is even)
-template <int CPT> __device__ __forceinline__ void lds_row(const float* sm, const int16_t* se, Row<TrF32, CPT>& x) {
-  x.load(sm, se);  // (generic pointers into shared memory: LDS after address-space inference)
+// warp-cooperative copy of one row slice (SW significands + SW exponents) with 16-byte cp.async per lane
+template <int SW>
+__device__ __forceinline__ void row_cp_async(float* dsig, int16_t* dexp, const float* gsig, const int16_t* gexp,
+                                             int lane) {
+#pragma unroll
+  for (int o = lane * 4; o < SW; o += 128) cp_async16(dsig + o, gsig + o);
+#pragma unroll
+  for (int o = lane * 8; o < SW; o += 256) cp_async16(dexp + o, gexp + o);
+}
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(unsigned long long* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// extended-range sum over the n compacted rows of a stage (rows q < n, factors in the header):
-//   out = sum_q x_q * KW_q   as (s, E) per commodity, E = max_q (e_q + ke_q)
-// fp32 packed arithmetic (CPT even), per pair of commodities and row: one VIADDMNMX.S16x2 for the max
-// (e + ke is exact in int16: |e| <= 16384, |ke| <= 16000); in the sum pass d = max(max(e + ke, E - 32512)
-// - E, -126) by two more (no 16-bit wrap), the scale KW * 2^d by an integer add into the float's exponent
-// field (mod 2^32 the low / high half of d << 23 equals d2 << 23 / (d2 & 0xffff0000) << 7), then FFMA.
-template <int CPT>
-__device__ __forceinline__ void stage_sum(const float* sig, const int16_t* sex, int col, int SW, int nslots,
-                                          const PipeHdr& h, int n, float* s, int* Ex) {
-  const int start = h.start;
-  auto slot = [&](int q) {
-    const int r = start + q;
-    return (r >= nslots ? r - nslots : r) * SW + col;  // (shared-memory index: 32-bit)
-  };
-  typedef Row<TrF32, CPT> R;
-  if constexpr (R::PACKED) {
-    constexpr int NW = R::NW;
-    unsigned E2[NW];
+// grid-stride walk over node-major (node, slice) items without divisions in the loop
+struct ItemIt {
+  int node, sl, dn, ds, ns;
+  __device__ __forceinline__ void init(int item0, int step, int ns_) {
+    ns = ns_;
+    node = item0 / ns;
+    sl = item0 - node * ns;
+    dn = step / ns;
+    ds = step - dn * ns;
+  }
+  __device__ __forceinline__ void next() {
+    node += dn;
+    sl += ds;
+    if (sl >= ns) {
+      sl -= ns;
+      ++node;
+    }
+  }
+};
+
+// ------------------------------------------------------------------------------------------------
+// Extended-range arithmetic on a lane's CPT commodities (fp32 significand, int16 exponent).
+// Exponents are handled two per 32-bit word (CPT even): the max of (row exponent + arc exponent) by one
+// VIADDMNMX.S16x2 per pair (exact: |e| <= 16384, |ke| <= 16000); the scale 2^d, d = max(max(e + ke,
+// E - 32512) - E, -126) (no 16-bit wrap) by two more; then K W 2^d by an integer add into the float's
+// exponent field — mod 2^32 the low / high half of d << 23 equals d2 << 23 / (d2 & 0xffff0000) << 7.
+
+template <int CPT> struct XPre {  // per-item constants of a lane: -E and the low clamp E - 32512, packed
+  unsigned nE2[CPT / 2 > 0 ? CPT / 2 : 1], Lo2[CPT / 2 > 0 ? CPT / 2 : 1];
+  int nE[CPT];
+  int E[CPT];
+  __device__ __forceinline__ void set(const unsigned* E2) {
+    if constexpr (CPT % 2 == 0) {
 #pragma unroll
-    for (int w = 0; w < NW; ++w) E2[w] = 0x80008000u;
-    float acc[CPT];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) acc[c] = 0.f;
-    if (n <= PIPE_NR) {
-      R x[PIPE_NR];
-#pragma unroll
-      for (int q = 0; q < PIPE_NR; ++q)
-        if (q < n) lds_row<CPT>(sig + slot(q), sex + slot(q), x[q]);
-#pragma unroll
-      for (int q = 0; q < PIPE_NR; ++q)
-        if (q < n) {
-          const unsigned k2 = pack2(h.ke[q]);
-#pragma unroll
-          for (int w = 0; w < NW; ++w) E2[w] = __viaddmax_s16x2((unsigned)x[q].w[w], k2, E2[w]);
-        }
-      unsigned nE2[NW], Lo2[NW];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
-        nE2[w] = __vneg2(E2[w]);
-        Lo2[w] = __vsubss2(E2[w], 0x7f007f00u);  // E - 32512 (saturated): e + ke below it is negligible
-      }
-#pragma unroll
-      for (int q = 0; q < PIPE_NR; ++q)
-        if (q < n) {
-          const unsigned k2 = pack2(h.ke[q]);
-          const unsigned kb = __float_as_uint(h.km[q]);
-#pragma unroll
-          for (int w = 0; w < NW; ++w) {
-            // d = max(max(e + ke, E - 32512) - E, -126): every 16-bit intermediate in range, no wrap
-            const unsigned tq = __viaddmax_s16x2((unsigned)x[q].w[w], k2, Lo2[w]);
-            const unsigned d2 = __viaddmax_s16x2(tq, nE2[w], 0xff82ff82u);
-            acc[2 * w] = fmaf(x[q].m[2 * w], __uint_as_float(kb + (d2 << 23)), acc[2 * w]);
-            acc[2 * w + 1] = fmaf(x[q].m[2 * w + 1], __uint_as_float(kb + ((d2 & 0xffff0000u) << 7)), acc[2 * w + 1]);
-          }
-        }
-    } else {  // high degree: two passes over shared memory
-      for (int q = 0; q < n; ++q) {
-        R x;
-        lds_row<CPT>(sig + slot(q), sex + slot(q), x);
-        const unsigned k2 = pack2(h.ke[q]);
-#pragma unroll
-        for (int w = 0; w < NW; ++w) E2[w] = __viaddmax_s16x2((unsigned)x.w[w], k2, E2[w]);
-      }
-      unsigned nE2[NW], Lo2[NW];
-#pragma unroll
-      for (int w = 0; w < NW; ++w) {
+      for (int w = 0; w < CPT / 2; ++w) {
         nE2[w] = __vneg2(E2[w]);
         Lo2[w] = __vsubss2(E2[w], 0x7f007f00u);
+        E[2 * w] = (int)(short)(E2[w] & 0xffffu);
+        E[2 * w + 1] = (int)E2[w] >> 16;
       }
-      for (int q = 0; q < n; ++q) {
-        R x;
-        lds_row<CPT>(sig + slot(q), sex + slot(q), x);
-        const unsigned k2 = pack2(h.ke[q]);
-        const unsigned kb = __float_as_uint(h.km[q]);
+    } else {
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-          const unsigned tq = __viaddmax_s16x2((unsigned)x.w[w], k2, Lo2[w]);
-          const unsigned d2 = __viaddmax_s16x2(tq, nE2[w], 0xff82ff82u);
-          acc[2 * w] = fmaf(x.m[2 * w], __uint_as_float(kb + (d2 << 23)), acc[2 * w]);
-          acc[2 * w + 1] = fmaf(x.m[2 * w + 1], __uint_as_float(kb + ((d2 & 0xffff0000u) << 7)), acc[2 * w + 1]);
-        }
-      }
+      for (int c = 0; c < CPT; ++c) E[c] = (int)E2[c];
     }
 #pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      Ex[2 * w] = (int)(short)(E2[w] & 0xffffu);
-      Ex[2 * w + 1] = (int)E2[w] >> 16;
-    }
+    for (int c = 0; c < CPT; ++c) nE[c] = -E[c];
+  }
+};
+
+template <int CPT> __device__ __forceinline__ void xmax_init(unsigned* E2) {
+  if constexpr (CPT % 2 == 0) {
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) s[c] = acc[c];
-  } else {  // CPT = 1: plain ints
-    int E = EZERO - 4 * ELIM;
-    for (int q = 0; q < n; ++q) E = max(E, (int)sex[slot(q)] + h.ke[q]);
-    float a = 0.f;
-    for (int q = 0; q < n; ++q) {
-      const int d = max((int)sex[slot(q)] + h.ke[q] - E, -126);
-      a = fmaf(sig[slot(q)], __uint_as_float(__float_as_uint(h.km[q]) + ((unsigned)d << 23)), a);
-    }
-    s[0] = a;
-    Ex[0] = E;
+    for (int w = 0; w < CPT / 2; ++w) E2[w] = 0x80008000u;
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) E2[c] = (unsigned)(EZERO - 4 * ELIM);
   }
 }
+template <int CPT>
+__device__ __forceinline__ void xmax_add(unsigned* E2, const Row<TrF32, CPT>& x, unsigned k2, int ke) {
+  if constexpr (CPT % 2 == 0) {
+#pragma unroll
+    for (int w = 0; w < CPT / 2; ++w) E2[w] = __viaddmax_s16x2((unsigned)x.w[w], k2, E2[w]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) E2[c] = (unsigned)max((int)E2[c], x.e(c) + ke);
+  }
+}
+// t[c] = x.m[c] * K W * 2^(x.e[c] + ke - E[c]) (flushed below 2^-126 of the maximum)
+template <int CPT>
+__device__ __forceinline__ void xterms(const Row<TrF32, CPT>& x, unsigned kb, unsigned k2, int ke,
+                                       const XPre<CPT>& P, float* tq) {
+  if constexpr (CPT % 2 == 0) {
+#pragma unroll
+    for (int w = 0; w < CPT / 2; ++w) {
+      const unsigned u = __viaddmax_s16x2((unsigned)x.w[w], k2, P.Lo2[w]);
+      const unsigned d2 = __viaddmax_s16x2(u, P.nE2[w], 0xff82ff82u);
+      tq[2 * w] = x.m[2 * w] * __uint_as_float(kb + (d2 << 23));
+      tq[2 * w + 1] = x.m[2 * w + 1] * __uint_as_float(kb + ((d2 & 0xffff0000u) << 7));
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int d = max(x.e(c) + ke + P.nE[c], -126);
+      tq[c] = x.m[c] * __uint_as_float(kb + ((unsigned)d << 23));
+    }
+  }
+}
+template <int CPT>
+__device__ __forceinline__ void xacc(const Row<TrF32, CPT>& x, unsigned kb, unsigned k2, int ke, const XPre<CPT>& P,
+                                     float* acc) {
+  if constexpr (CPT % 2 == 0) {
+#pragma unroll
+    for (int w = 0; w < CPT / 2; ++w) {
+      const unsigned u = __viaddmax_s16x2((unsigned)x.w[w], k2, P.Lo2[w]);
+      const unsigned d2 = __viaddmax_s16x2(u, P.nE2[w], 0xff82ff82u);
+      acc[2 * w] = fmaf(x.m[2 * w], __uint_as_float(kb + (d2 << 23)), acc[2 * w]);
+      acc[2 * w + 1] = fmaf(x.m[2 * w + 1], __uint_as_float(kb + ((d2 & 0xffff0000u) << 7)), acc[2 * w + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int d = max(x.e(c) + ke + P.nE[c], -126);
+      acc[c] = fmaf(x.m[c], __uint_as_float(kb + ((unsigned)d << 23)), acc[c]);
+    }
+  }
+}
+__device__ __forceinline__ int k2_to_ke(unsigned k2) { return (int)(short)(k2 & 0xffffu); }
+
+// sum over N (compile-time) contiguous rows sg + q * SW of an item: (s, E) per commodity
+template <int CPT, int N>
+__device__ __forceinline__ void sum_rows_n(const float* sg, const int16_t* se, const unsigned* kb, const unsigned* k2,
+                                           float* s, int* Ex) {
+  constexpr int SW = pipe_sw<CPT>();
+  Row<TrF32, CPT> x[N > 0 ? N : 1];
+#pragma unroll
+  for (int q = 0; q < N; ++q) x[q].load(sg + q * SW, se + q * SW);
+  unsigned E2[CPT];
+  xmax_init<CPT>(E2);
+#pragma unroll
+  for (int q = 0; q < N; ++q) xmax_add<CPT>(E2, x[q], k2[q], k2_to_ke(k2[q]));
+  XPre<CPT> P;
+  P.set(E2);
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    s[c] = 0.f;
+    Ex[c] = P.E[c];
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) xacc<CPT>(x[q], kb[q], k2[q], k2_to_ke(k2[q]), P, s);
+}
+// any n (high degree): two passes over shared memory
+template <int CPT>
+__device__ __forceinline__ void sum_rows_any(const float* sg, const int16_t* se, const unsigned* kb,
+                                             const unsigned* k2, int n, float* s, int* Ex) {
+  constexpr int SW = pipe_sw<CPT>();
+  unsigned E2[CPT];
+  xmax_init<CPT>(E2);
+  for (int q = 0; q < n; ++q) {
+    Row<TrF32, CPT> x;
+    x.load(sg + q * SW, se + q * SW);
+    xmax_add<CPT>(E2, x, k2[q], k2_to_ke(k2[q]));
+  }
+  XPre<CPT> P;
+  P.set(E2);
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    s[c] = 0.f;
+    Ex[c] = P.E[c];
+  }
+  for (int q = 0; q < n; ++q) {
+    Row<TrF32, CPT> x;
+    x.load(sg + q * SW, se + q * SW);
+    xacc<CPT>(x, kb[q], k2[q], k2_to_ke(k2[q]), P, s);
+  }
+}
+template <int CPT>
+__device__ __forceinline__ void sum_rows(const float* sg, const int16_t* se, const unsigned* kb, const unsigned* k2,
+                                         int n, float* s, int* Ex) {
+  switch (n) {
+    case 0: sum_rows_n<CPT, 0>(sg, se, kb, k2, s, Ex); break;
+    case 1: sum_rows_n<CPT, 1>(sg, se, kb, k2, s, Ex); break;
+    case 2: sum_rows_n<CPT, 2>(sg, se, kb, k2, s, Ex); break;
+    case 3: sum_rows_n<CPT, 3>(sg, se, kb, k2, s, Ex); break;
+    case 4: sum_rows_n<CPT, 4>(sg, se, kb, k2, s, Ex); break;
+    case 5: sum_rows_n<CPT, 5>(sg, se, kb, k2, s, Ex); break;
+    case 6: sum_rows_n<CPT, 6>(sg, se, kb, k2, s, Ex); break;
+    case 7: sum_rows_n<CPT, 7>(sg, se, kb, k2, s, Ex); break;
+    case 8: sum_rows_n<CPT, 8>(sg, se, kb, k2, s, Ex); break;
+    default: sum_rows_any<CPT>(sg, se, kb, k2, n, s, Ex); break;
+  }
+}
+
+// producer-side row-slot ring: monotonic counters, [tail, head) in use; rpos = head mod R
+struct RowRing {
+  unsigned head = 0, tail = 0;
+  int rpos = 0;
+  int kold = 0;  // items < kold are known to be released
+};
 
 // ------------------------------------------------------------------------------------------------
 template <int CPT>
 __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bwd_pipe(DevPtrs p, PipeCfg5 pc, int t) {
   typedef float M;
   typedef int16_t E;
+  constexpr int SW = pipe_sw<CPT>();
   extern __shared__ __align__(16) unsigned char smem[];
-  const PipeSmem L = pipe_smem(pc.R, pc.SD, pc.D, pc.SW);
+  const PipeSmem L = pipe_smem(pc.R, PIPE_SD, pc.D, SW);
   unsigned long long* full = (unsigned long long*)(smem + L.off_full);
   unsigned long long* empty = (unsigned long long*)(smem + L.off_empty);
   ArcKW<M>* ring = (ArcKW<M>*)(smem + L.off_ring);
@@ -226,11 +298,11 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bwd_pipe(DevPtrs p, PipeCfg
   M* sig = (M*)(smem + L.off_sig);
   E* sex = (E*)(smem + L.off_exp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int D = pc.D, SW = pc.SW, R = pc.R;
+  const int D = pc.D, R = pc.R;
   if (threadIdx.x == 0) {
     for (int s = 0; s < PIPE_SD; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], PIPE_NWC);  // one consumer group per item
+      mbar_init(&full[s], pc.copy ? 1 + 32 : 1);  // (+ one cp.async noinc arrive per producer lane)
+      mbar_init(&empty[s], PIPE_NWC);             // one consumer group per item
     }
     mbar_fence_init();
   }
@@ -253,14 +325,12 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bwd_pipe(DevPtrs p, PipeCfg
     };
 #pragma unroll 1
     for (int k = 0; k < PIPE_P; ++k) prefetch();
-    unsigned head = 0, tail = 0;  // row-slot counters (monotonic); slots [tail, head) are in use
-    int rpos = 0;                 // head mod R
-    int kold = 0;                 // items < kold are known to be released
-    auto release = [&]() {        // wait for item kold's consumers, free its rows
-      const int ds = kold & (PIPE_SD - 1);
-      mbar_wait(&empty[ds], (kold / PIPE_SD) & 1);
-      tail = (unsigned)hdr[ds].end;
-      ++kold;
+    RowRing rr;
+    auto release = [&]() {
+      const int ds = rr.kold & (PIPE_SD - 1);
+      mbar_wait(&empty[ds], (rr.kold / PIPE_SD) & 1);
+      rr.tail = (unsigned)hdr[ds].end;
+      ++rr.kold;
     };
     int cslot = 0;
     for (int k = 0; cur.node < p.N; ++k, cur.next()) {
@@ -277,32 +347,46 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bwd_pipe(DevPtrs p, PipeCfg
       const bool ok = lane < D && r.node >= 0 && r.km > M(0);
       const unsigned bal = __ballot_sync(0xffffffffu, ok);
       const int n = __popc(bal);
-      while (kold <= k - PIPE_SD) release();                      // descriptor reuse
-      while (head + (unsigned)n - tail > (unsigned)R) release();  // row space
+      while (rr.kold <= k - PIPE_SD) release();  // descriptor reuse
+      if (rr.rpos + n > R) {                     // keep the item's rows contiguous
+        rr.head += (unsigned)(R - rr.rpos);
+        rr.rpos = 0;
+      }
+      while (rr.head + (unsigned)n - rr.tail > (unsigned)R && rr.kold < k) release();  // row space (R >= 2 D)
       const int ds = k & (PIPE_SD - 1);
       const int slot = __popc(bal & ((1u << lane) - 1u));
       if (ok) {
-        hdr[ds].km[slot] = r.km;
-        hdr[ds].ke[slot] = r.ke;
+        hdr[ds].kb[slot] = __float_as_uint(r.km);
+        hdr[ds].k2[slot] = pack2(r.ke);
       }
       if (lane == 0) {
         hdr[ds].n = n;
-        hdr[ds].start = rpos;
-        hdr[ds].end = (int)(head + (unsigned)n);  // monotonic row counter after this item (producer only)
+        hdr[ds].start = rr.rpos;
+        hdr[ds].end = (int)(rr.head + (unsigned)n);  // monotonic row counter after this item (producer only)
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&full[ds], (unsigned)n * (unsigned)SW * 6u);
-      __syncwarp();
-      if (ok) {
-        const size_t g = (size_t)r.node * p.Lp + (size_t)cur.sl * SW;
-        int rs = rpos + slot;
-        if (rs >= R) rs -= R;
-        bulk_g2s(sig + rs * SW, gm + g, SW * 4, &full[ds]);
-        bulk_g2s(sex + rs * SW, ge + g, SW * 2, &full[ds]);
+      if (pc.copy) {  // LDGSTS: the warp copies the rows together; completion via cp.async arrive (noinc)
+        for (int q = 0; q < n; ++q) {
+          const int src = __shfl_sync(0xffffffffu, r.node, __fns(bal, 0, q + 1));
+          const size_t g = (size_t)src * p.Lp + (size_t)cur.sl * SW;
+          const int rs = rr.rpos + q;
+          row_cp_async<SW>(sig + rs * SW, sex + rs * SW, gm + g, ge + g, lane);
+        }
+        cp_async_mbar_arrive_noinc(&full[ds]);
+        if (lane == 0) mbar_arrive(&full[ds]);
+      } else {
+        if (lane == 0) mbar_arrive_expect_tx(&full[ds], (unsigned)n * (unsigned)SW * 6u);
+        __syncwarp();
+        if (ok) {
+          const size_t g = (size_t)r.node * p.Lp + (size_t)cur.sl * SW;
+          const int rs = rr.rpos + slot;
+          bulk_g2s(sig + rs * SW, gm + g, SW * 4, &full[ds]);
+          bulk_g2s(sex + rs * SW, ge + g, SW * 2, &full[ds]);
+        }
       }
-      head += (unsigned)n;
-      rpos += n;
-      if (rpos >= R) rpos -= R;
+      rr.head += (unsigned)n;
+      rr.rpos += n;
+      if (rr.rpos >= R) rr.rpos -= R;
     }
     cp_async_wait<0>();
     return;
@@ -320,9 +404,15 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bwd_pipe(DevPtrs p, PipeCfg
     const int ds = k & (PIPE_SD - 1);
     mbar_wait(&full[ds], (k / PIPE_SD) & 1);
     const PipeHdr& h = hdr[ds];
+    if (pc.dry) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ds]);
+      continue;
+    }
+    const int base = h.start * SW + col;
     M s[CPT];
     int Ex[CPT];
-    stage_sum<CPT>(sig, sex, col, SW, R, h, h.n, s, Ex);
+    sum_rows<CPT>(sig + base, sex + base, h.kb, h.k2, h.n, s, Ex);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
     Lane<M, E, CPT> out;

@@ -6,16 +6,17 @@
 //   (ii)  W_{t-1}[a] <- min(W_{t-1}[a] d[a] / F_{t-1}[a], 1)                         (eq:sinkhorn_graph_Vineq P:861)
 //   (iii) alpha_t[j] = sum_{a -> j} alpha_{t-1}[i_a] K W_{t-1}[a] with the updated W    (eq:psi_hat P:1031-1036)
 // The producer warp stages, per item: the compacted rows alpha_{t-1}[i_a] (nonzero factor) and the node's
-// own row beta_t[j] (cp.async.bulk), the arc records (cp.async ring, prefetched), and the dual-update
-// operands d, W, K of every in-arc (4-byte cp.async into the item descriptor, tracked by the same
-// mbarrier through cp.async.mbarrier.arrive.noinc).
+// own row beta_t[j] (cp.async.bulk; contiguous ring slots), the arc records (cp.async ring, prefetched),
+// and the dual-update operands d, W, K and the ELL out-slot of every capacitated in-arc (4-byte cp.async
+// into the item descriptor, tracked by the same mbarrier through cp.async.mbarrier.arrive.noinc).
 //
 // Consumers (a group of 8 warps per item, 2 groups alternating items) compute the per-row terms
 //   t_q[c] = alpha_q[c] K W_q 2^-E[c]     (E[c] = max_q exponent of alpha_q[c] K W_q, extended range)
-// once, in registers.  Then
+// once, in registers (the row count is a compile-time constant of the code path, switch on n).  Then
 //   flows:  F_q = sum_c t_q[c] * beta_lin[c],   beta_lin[c] = beta[j,c] 2^E[c]  (one FMA per element),
-//           reduced over the lanes (shuffles) and the group's warps (shared memory, fixed order);
-//   update: one lane per arc applies (ii) and publishes the ratio r_q = W_new / W_old;
+//           reduced over the lanes by a transposed butterfly (9 shuffles for up to 8 rows) and over the
+//           group's warps in shared memory (fixed order: deterministic);
+//   update: one lane per arc applies (ii), refreshes the arc's ELL records and publishes r_q = W_new / W_old;
 //   alpha:  alpha_t[j,c] = 2^E[c] sum_q r_q t_q[c]   (one FMA per element)
 // — valid while every |log2 r_q| <= 40 (the dropped terms, below 2^-126 of the old maximum, stay below
 // 2^-46 of the new one); otherwise the item is recomputed from shared memory with the new factors.
@@ -25,27 +26,28 @@
 namespace mmf {
 
 struct FwdHdr {
-  float km[32];  // rows (compacted, nonzero factor): K W significand
-  int ke[32];    //   ... exponent
-  int rarc[32];  //   ... arc position q of the row
-  int rowof[32]; // arcs (all in-arcs, q < na): row index or -1
-  int aux[32];   //   ... arc id | bit 31 uncapacitated
-  float d[32];   //   ... dual-update operands (cp.async)
+  unsigned kb[32];  // rows (compacted, nonzero factor): K W significand bits
+  unsigned k2[32];  //   ... exponent, packed twice (int16x2)
+  int rowof[32];    // arcs (all in-arcs, q < na): row index or -1
+  int aux[32];      //   ... arc id | bit 31 uncapacitated
+  int rtail[32];    //   ... tail node
+  float d[32];      //   ... dual-update operands (cp.async)
   float wm[32];
   int we[32];
   float Km[32];
   int Ke[32];
-  int eopos[32]; //   ... slot of the arc in the ELL out-records (cp.async)
-  int rtail[32]; //   ... tail node
+  int eopos[32];    //   ... slot of the arc in the ELL out-records (cp.async)
+  unsigned capmask; // bit q: row q's arc is capacitated
   int nr, na, start, end;
+  int pad[3];
 };
 
 // per consumer group scratch
 struct FwdGrp {
   float fpart[32][PIPE_NWC];  // flow partials (row, warp)
-  float rq[32];               // ratio W_new / W_old per arc position (linear)
-  float nkm[32];              // new K W per row (slow path)
-  int nke[32];
+  float rq[32];               // ratio W_new / W_old per row (linear)
+  unsigned nkb[32];           // new K W per row (slow path)
+  unsigned nk2[32];
   int slow;
   int pad[3];
 };
@@ -81,49 +83,208 @@ __host__ __device__ inline PFwdSmem pfwd_smem(int R, int D, int SW) {
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
-__device__ __forceinline__ void cp_async_mbar_arrive_noinc(unsigned long long* bar) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
-}
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
 
-template <int CPT> struct FwdNR;
-template <> struct FwdNR<4> { static constexpr int v = 8; };
-template <> struct FwdNR<2> { static constexpr int v = 12; };
-template <> struct FwdNR<1> { static constexpr int v = 16; };
+// sums over the 32 lanes of up to 8 per-lane values at once (transposed butterfly: 4 + 2 + 1 + 1 + 1
+// shuffles); the total of value q ends in the lanes with (lane & 3) == 0 and bfly_row(lane) == q
+__device__ __forceinline__ int bfly_row(int lane) {
+  return ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+}
+__device__ __forceinline__ float bfly8(const float* v, int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  float u[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b4 ? v[i] : v[i + 4];
+    const float keep = b4 ? v[i + 4] : v[i];
+    u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float w[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b3 ? u[i] : u[i + 2];
+    const float keep = b3 ? u[i + 2] : u[i];
+    w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  float r = (b2 ? w[1] : w[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w[0] : w[1], 4);
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;
+}
 
-// per-row terms of a lane: t[c] = x.m[c] * KW * 2^(x.e[c] + ke - E[c]), clamped below 2^-126
-template <int CPT>
-__device__ __forceinline__ void row_terms(const Row<TrF32, CPT>& x, float km, int ke, const unsigned* nE2,
-                                          const unsigned* Lo2, const int* nE, float* tq) {
-  const unsigned kb = __float_as_uint(km);
-  if constexpr (Row<TrF32, CPT>::PACKED) {
-    const unsigned k2 = pack2(ke);
+// capacity-dual update of the item's in-arcs by one warp (lane = arc position), publishing per-row
+// ratios and new factors to the group scratch
+__device__ __forceinline__ void fwd_update(const DevPtrs& p, const FwdHdr& h, FwdGrp& G, int t, int j, int D,
+                                           int lane) {
+  typedef float M;
+  View<TrF32> v(p);
+  bool big = false;
+  if (lane < h.na) {
+    const int aux = h.aux[lane];
+    const int row = h.rowof[lane];
+    if (aux >= 0) {
+      const int a = aux;
+      float s = 0.f;
+      if (row >= 0)
 #pragma unroll
-    for (int w = 0; w < CPT / 2; ++w) {
-      const unsigned u = __viaddmax_s16x2((unsigned)x.w[w], k2, Lo2[w]);
-      const unsigned d2 = __viaddmax_s16x2(u, nE2[w], 0xff82ff82u);
-      tq[2 * w] = x.m[2 * w] * __uint_as_float(kb + (d2 << 23));
-      tq[2 * w + 1] = x.m[2 * w + 1] * __uint_as_float(kb + ((d2 & 0xffff0000u) << 7));
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const int d = max(x.e(c) + ke + nE[c], -126);
-      tq[c] = x.m[c] * __uint_as_float(kb + ((unsigned)d << 23));
+        for (int w = 0; w < PIPE_NWC; ++w) s += G.fpart[row][w];
+      if (!(s == s) || isinf(s)) set_error(p, ERR_NAN, -1, a);
+      const float d = h.d[lane], w0 = h.wm[lane];
+      const int e0 = h.we[lane];
+      float wm;
+      int we;
+      w_new<TrF32>(d, w0, e0, (double)s, wm, we);
+      v.Wm(t - 1)[a] = wm;
+      v.We(t - 1)[a] = we;
+      // refresh the step's ELL records (in: this node's slot; out: the tail's slot); the CSR record copies
+      // used by the readout kernels are rebuilt from W before a readout (mmf.cu)
+      ArcKW<M> rr;
+      kw_clamp<TrF32>(h.Km[lane], h.Ke[lane], wm, we, rr.km, rr.ke);
+      rr.aux = aux;
+      rr.node = h.rtail[lane];
+      ((ArcKW<M>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
+      rr.node = j;
+      ((ArcKW<M>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + h.eopos[lane]] = rr;
+      if (row >= 0) {
+        float rq = 0.f;
+        if (w0 > 0.f && wm > 0.f) {
+          const int de = we - e0;
+          big = de > 40 || de < -40;
+          if (!big) rq = (wm / w0) * __uint_as_float((unsigned)(de + 127) << 23);
+        } else {
+          big = true;  // W changed from / to exact zero
+        }
+        G.rq[row] = rq;
+        G.nkb[row] = __float_as_uint(rr.km);
+        G.nk2[row] = pack2(rr.ke);
+      }
+    } else if (row >= 0) {
+      G.rq[row] = 1.f;
+      G.nkb[row] = h.kb[row];
+      G.nk2[row] = h.k2[row];
     }
   }
+  const unsigned anyb = __ballot_sync(0xffffffffu, big);
+  if (lane == 0) G.slow = anyb != 0u;
+}
+
+// the own row beta_t[j] scaled to the terms' exponents: beta_lin[c] = beta[j,c] 2^E[c] (flows are bounded
+// by the mass: the exponent is clamped to the normal range)
+template <int CPT>
+__device__ __forceinline__ void beta_lin(const Row<TrF32, CPT>& b, const XPre<CPT>& P, float* bl) {
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int es = b.e(c) + P.E[c];
+    bl[c] = (es < -126 || !(b.m[c] > 0.f)) ? 0.f : b.m[c] * __uint_as_float((unsigned)(min(es, 127) + 127) << 23);
+  }
+}
+
+// the flows + update + alpha of one item with N (compile-time) rows; returns (s, Ex)
+template <int CPT, int N>
+__device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, const int16_t* se, const FwdHdr& h,
+                                         FwdGrp& G, int t, int j, int D, int lane, int wg, int bar_id, float* s,
+                                         int* Ex) {
+  constexpr int SW = pipe_sw<CPT>();
+  typedef Row<TrF32, CPT> R_;
+  R_ b;
+  b.load(sg + N * SW, se + N * SW);  // own row beta_t[j]
+  float tq[N > 0 ? N : 1][CPT];
+  XPre<CPT> P;
+  {
+    R_ x[N > 0 ? N : 1];
+#pragma unroll
+    for (int q = 0; q < N; ++q) x[q].load(sg + q * SW, se + q * SW);
+    unsigned E2[CPT];
+    xmax_init<CPT>(E2);
+#pragma unroll
+    for (int q = 0; q < N; ++q) xmax_add<CPT>(E2, x[q], h.k2[q], k2_to_ke(h.k2[q]));
+    P.set(E2);
+#pragma unroll
+    for (int q = 0; q < N; ++q) xterms<CPT>(x[q], h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, tq[q]);
+  }
+  float bl[CPT];
+  beta_lin<CPT>(b, P, bl);
+  const unsigned cap = h.capmask;
+  if (N > 0 && cap != 0u) {
+    float f[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      f[q] = 0.f;
+      if (q < N)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) f[q] = fmaf(tq[q < N ? q : 0][c], bl[c], f[q]);
+    }
+    const float r = bfly8(f, lane);
+    const int row = bfly_row(lane);
+    if ((lane & 3) == 0 && row < N && ((cap >> row) & 1u)) G.fpart[row][wg] = r;
+  }
+  named_bar(bar_id, PIPE_NWC * 32);
+  if (wg == 0) fwd_update(p, h, G, t, j, D, lane);
+  named_bar(bar_id, PIPE_NWC * 32);
+  if (!G.slow) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      s[c] = 0.f;
+      Ex[c] = P.E[c];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const float r = G.rq[q];
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
+    }
+  } else {  // large ratios: recompute from shared memory with the new factors
+    sum_rows_any<CPT>(sg, se, G.nkb, G.nk2, N, s, Ex);
+  }
+}
+
+// any row count (more than 8 rows): streaming flows, then the update, then alpha from shared memory
+template <int CPT>
+__device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, const int16_t* se, const FwdHdr& h,
+                                             FwdGrp& G, int t, int j, int D, int lane, int wg, int bar_id, int nr,
+                                             float* s, int* Ex) {
+  constexpr int SW = pipe_sw<CPT>();
+  typedef Row<TrF32, CPT> R_;
+  R_ b;
+  b.load(sg + nr * SW, se + nr * SW);
+  unsigned E2[CPT];
+  xmax_init<CPT>(E2);
+  for (int q = 0; q < nr; ++q) {
+    R_ x;
+    x.load(sg + q * SW, se + q * SW);
+    xmax_add<CPT>(E2, x, h.k2[q], k2_to_ke(h.k2[q]));
+  }
+  XPre<CPT> P;
+  P.set(E2);
+  float bl[CPT];
+  beta_lin<CPT>(b, P, bl);
+  for (int q = 0; q < nr; ++q) {
+    if (!((h.capmask >> q) & 1u)) continue;
+    R_ x;
+    x.load(sg + q * SW, se + q * SW);
+    float tt[CPT];
+    xterms<CPT>(x, h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, tt);
+    float f = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) f = fmaf(tt[c], bl[c], f);
+    f = warp_sum<float>(f);
+    if (lane == 0) G.fpart[q][wg] = f;
+  }
+  named_bar(bar_id, PIPE_NWC * 32);
+  if (wg == 0) fwd_update(p, h, G, t, j, D, lane);
+  named_bar(bar_id, PIPE_NWC * 32);
+  sum_rows_any<CPT>(sg, se, G.nkb, G.nk2, nr, s, Ex);
 }
 
 template <int CPT, int MODE>
 __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5 pc, int t) {
   typedef float M;
   typedef int16_t E;
-  typedef Row<TrF32, CPT> R_;
-  constexpr int NR = FwdNR<CPT>::v;
+  constexpr int SW = pipe_sw<CPT>();
   extern __shared__ __align__(16) unsigned char smem[];
-  const PFwdSmem L = pfwd_smem(pc.R, pc.D, pc.SW);
+  const PFwdSmem L = pfwd_smem(pc.R, pc.D, SW);
   unsigned long long* full = (unsigned long long*)(smem + L.off_full);
   unsigned long long* empty = (unsigned long long*)(smem + L.off_empty);
   ArcKW<M>* ring = (ArcKW<M>*)(smem + L.off_ring);
@@ -132,7 +293,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
   M* sig = (M*)(smem + L.off_sig);
   E* sex = (E*)(smem + L.off_exp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int D = pc.D, SW = pc.SW, R = pc.R;
+  const int D = pc.D, R = pc.R;
   if (threadIdx.x == 0) {
     for (int s = 0; s < PIPE_SD; ++s) {
       mbar_init(&full[s], 1 + 32);     // expect_tx arrive + one cp.async (noinc) arrive per producer lane
@@ -163,15 +324,14 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
     };
 #pragma unroll 1
     for (int k = 0; k < PIPE_P; ++k) prefetch();
-    unsigned head = 0, tail = 0;
-    int rpos = 0, kold = 0, cslot = 0;
+    RowRing rr;
     auto release = [&]() {
-      const int ds = kold & (PIPE_SD - 1);
-      mbar_wait(&empty[ds], (kold / PIPE_SD) & 1);
-      tail = (unsigned)hdr[ds].end;
-      ++kold;
+      const int ds = rr.kold & (PIPE_SD - 1);
+      mbar_wait(&empty[ds], (rr.kold / PIPE_SD) & 1);
+      rr.tail = (unsigned)hdr[ds].end;
+      ++rr.kold;
     };
-    int k = 0;
+    int k = 0, cslot = 0;
     for (int j = blockIdx.x; j < p.N; j += gridDim.x, ++k) {
       cp_async_wait<PIPE_P - 1>();
       __syncwarp();
@@ -187,16 +347,20 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
       const bool ok = valid && r.km > M(0);
       const unsigned vbal = __ballot_sync(0xffffffffu, valid);
       const unsigned obal = __ballot_sync(0xffffffffu, ok);
+      const unsigned cbal = __ballot_sync(0xffffffffu, ok && r.aux >= 0);
       const int na = __popc(vbal), nr = __popc(obal);
-      while (kold <= k - PIPE_SD) release();
-      while (head + (unsigned)(nr + 1) - tail > (unsigned)R) release();
+      while (rr.kold <= k - PIPE_SD) release();
+      if (rr.rpos + nr + 1 > R) {  // keep the item's rows contiguous
+        rr.head += (unsigned)(R - rr.rpos);
+        rr.rpos = 0;
+      }
+      while (rr.head + (unsigned)(nr + 1) - rr.tail > (unsigned)R && rr.kold < k) release();
       const int ds = k & (PIPE_SD - 1);
       FwdHdr& h = hdr[ds];
       const int rs = __popc(obal & ((1u << lane) - 1u));
       if (ok) {
-        h.km[rs] = r.km;
-        h.ke[rs] = r.ke;
-        h.rarc[rs] = lane;
+        h.kb[rs] = __float_as_uint(r.km);
+        h.k2[rs] = pack2(r.ke);
       }
       if (valid) {
         h.rowof[lane] = ok ? rs : -1;
@@ -213,10 +377,18 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
         }
       }
       if (lane == 0) {
+        // capmask over rows (row order = lane order of the nonzero-factor arcs)
+        unsigned cm = 0u, ob = obal;
+        for (int q = 0; ob; ++q) {
+          const int l = __ffs(ob) - 1;
+          if ((cbal >> l) & 1u) cm |= 1u << q;
+          ob &= ob - 1u;
+        }
+        h.capmask = cm;
         h.nr = nr;
         h.na = na;
-        h.start = rpos;
-        h.end = (int)(head + (unsigned)(nr + 1));
+        h.start = rr.rpos;
+        h.end = (int)(rr.head + (unsigned)(nr + 1));
       }
       cp_async_mbar_arrive_noinc(&full[ds]);
       prefetch();
@@ -225,21 +397,19 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
       __syncwarp();
       if (ok) {
         const size_t g = (size_t)r.node * p.Lp;
-        int q = rpos + rs;
-        if (q >= R) q -= R;
+        const int q = rr.rpos + rs;
         bulk_g2s(sig + q * SW, gm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, ge + g, SW * 2, &full[ds]);
       }
       if (lane == 31) {  // the node's own beta_t row -> slot nr
         const size_t g = (size_t)j * p.Lp;
-        int q = rpos + nr;
-        if (q >= R) q -= R;
+        const int q = rr.rpos + nr;
         bulk_g2s(sig + q * SW, bm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, be + g, SW * 2, &full[ds]);
       }
-      head += (unsigned)(nr + 1);
-      rpos += nr + 1;
-      if (rpos >= R) rpos -= R;
+      rr.head += (unsigned)(nr + 1);
+      rr.rpos += nr + 1;
+      if (rr.rpos >= R) rr.rpos -= R;
     }
     cp_async_wait<0>();
     return;
@@ -250,212 +420,34 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
   FwdGrp& G = grps[grp];
   const int col = wg * 32 * CPT + lane * CPT;
   const int bar_id = 1 + grp;
-  constexpr int BAR_N = PIPE_NWC * 32;
   int k = grp;
   for (int j = blockIdx.x + grp * gridDim.x; j < p.N; j += PIPE_NG * gridDim.x, k += PIPE_NG) {
     const int ds = k & (PIPE_SD - 1);
     mbar_wait(&full[ds], (k / PIPE_SD) & 1);
     const FwdHdr& h = hdr[ds];
-    const int nr = h.nr, na = h.na, start = h.start;
-    auto slot = [&](int q) {
-      const int r = start + q;
-      return (r >= R ? r - R : r) * SW + col;
-    };
-    // own row beta_t[j] and the per-commodity maximum exponent E over the rows
-    R_ b;
-    lds_row<CPT>(sig + slot(nr), sex + slot(nr), b);
-    unsigned E2[R_::NW];
-#pragma unroll
-    for (int w = 0; w < R_::NW; ++w) E2[w] = R_::PACKED ? 0x80008000u : (unsigned)(EZERO - 4 * ELIM);
-    for (int q = 0; q < nr; ++q) {
-      R_ x;
-      lds_row<CPT>(sig + slot(q), sex + slot(q), x);
-      if constexpr (R_::PACKED) {
-        const unsigned k2 = pack2(h.ke[q]);
-#pragma unroll
-        for (int w = 0; w < R_::NW; ++w) E2[w] = __viaddmax_s16x2((unsigned)x.w[w], k2, E2[w]);
-      } else {
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) E2[c] = (unsigned)max((int)E2[c], x.e(c) + h.ke[q]);
-      }
-    }
-    int Ex[CPT], nE[CPT];
-    unsigned nE2[R_::NW], Lo2[R_::NW];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      Ex[c] = R_::PACKED ? ((c & 1) ? ((int)E2[c >> 1] >> 16) : (int)(short)(E2[c >> 1] & 0xffffu)) : (int)E2[c];
-      nE[c] = -Ex[c];
-    }
-    if constexpr (R_::PACKED) {
-#pragma unroll
-      for (int w = 0; w < R_::NW; ++w) {
-        nE2[w] = __vneg2(E2[w]);
-        Lo2[w] = __vsubss2(E2[w], 0x7f007f00u);
-      }
-    }
-    // beta_lin[c] = beta[j,c] 2^E[c] (flows are bounded by the mass: exponent clamped to the normal range)
-    float bl[CPT];
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const int es = b.e(c) + Ex[c];
-      bl[c] = (es < -126 || !(b.m[c] > 0.f)) ? 0.f : b.m[c] * __uint_as_float((unsigned)(min(es, 127) + 127) << 23);
-    }
-    const bool fast = nr <= NR;
-    float tq[NR][CPT];
-    // ---- flows (old factors)
-    if (fast) {
-#pragma unroll
-      for (int q = 0; q < NR; ++q)
-        if (q < nr) {
-          R_ x;
-          lds_row<CPT>(sig + slot(q), sex + slot(q), x);
-          row_terms<CPT>(x, h.km[q], h.ke[q], nE2, Lo2, nE, tq[q]);
-          if (h.aux[h.rarc[q]] >= 0) {
-            float f = 0.f;
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) f = fmaf(tq[q][c], bl[c], f);
-            f = warp_sum<float>(f);
-            if (lane == 0) G.fpart[q][wg] = f;
-          }
-        }
-    } else {
-      for (int q = 0; q < nr; ++q) {
-        if (h.aux[h.rarc[q]] < 0) continue;
-        R_ x;
-        lds_row<CPT>(sig + slot(q), sex + slot(q), x);
-        float tt[CPT];
-        row_terms<CPT>(x, h.km[q], h.ke[q], nE2, Lo2, nE, tt);
-        float f = 0.f;
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) f = fmaf(tt[c], bl[c], f);
-        f = warp_sum<float>(f);
-        if (lane == 0) G.fpart[q][wg] = f;
-      }
-    }
-    named_bar(bar_id, BAR_N);
-    // ---- capacity-dual update: warp 0 of the group, one lane per in-arc
-    if (wg == 0) {
-      bool big = false;
-      if (lane < na) {
-        const int aux = h.aux[lane];
-        float rq = 1.f;
-        if (aux >= 0) {
-          const int a = aux;
-          const int row = h.rowof[lane];
-          float s = 0.f;
-          if (row >= 0)
-            for (int w = 0; w < PIPE_NWC; ++w) s += G.fpart[row][w];
-          if (!(s == s) || isinf(s)) set_error(p, ERR_NAN, -1, a);
-          const float d = h.d[lane], w0 = h.wm[lane];
-          const int e0 = h.we[lane];
-          float wm;
-          int we;
-          w_new<TrF32>(d, w0, e0, (double)s, wm, we);
-          v.Wm(t - 1)[a] = wm;
-          v.We(t - 1)[a] = we;
-          {  // refresh the step's ELL records (in: this node's slot; out: the tail's slot); the CSR record
-             // copies used by the readout kernels are rebuilt from W before a readout (mmf.cu)
-            ArcKW<M> rr;
-            kw_clamp<TrF32>(h.Km[lane], h.Ke[lane], wm, we, rr.km, rr.ke);
-            rr.aux = aux;
-            rr.node = h.rtail[lane];
-            ((ArcKW<M>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
-            rr.node = j;
-            ((ArcKW<M>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + h.eopos[lane]] = rr;
-          }
-          // ratio W_new / W_old (linear) and the new factor for the slow path
-          if (w0 > 0.f && wm > 0.f) {
-            const int de = we - e0;
-            big = de > 40 || de < -40;
-            rq = big ? 0.f : (wm / w0) * __uint_as_float((unsigned)(de + 127) << 23);
-          } else {
-            big = true;  // W changed from / to exact zero
-            rq = 0.f;
-          }
-          if (row >= 0) {
-            float m;
-            int e;
-            kw_clamp<TrF32>(h.Km[lane], h.Ke[lane], wm, we, m, e);
-            G.nkm[row] = m;
-            G.nke[row] = e;
-          }
-        } else if (h.rowof[lane] >= 0) {
-          G.nkm[h.rowof[lane]] = h.km[h.rowof[lane]];
-          G.nke[h.rowof[lane]] = h.ke[h.rowof[lane]];
-        }
-        G.rq[lane] = rq;
-      }
-      const unsigned anyb = __ballot_sync(0xffffffffu, big);
-      if (lane == 0) G.slow = anyb != 0u;
-    }
-    named_bar(bar_id, BAR_N);
-    // ---- alpha_t[j]
-    float s[CPT];
-    if (fast && !G.slow) {
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) s[c] = 0.f;
-#pragma unroll
-      for (int q = 0; q < NR; ++q)
-        if (q < nr) {
-          const float r = G.rq[h.rarc[q]];
-#pragma unroll
-          for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
-        }
-    } else {  // recompute with the new factors from shared memory
-      unsigned F2[R_::NW];
-#pragma unroll
-      for (int w = 0; w < R_::NW; ++w) F2[w] = R_::PACKED ? 0x80008000u : (unsigned)(EZERO - 4 * ELIM);
-      for (int q = 0; q < nr; ++q) {
-        if (!(G.nkm[q] > 0.f)) continue;
-        R_ x;
-        lds_row<CPT>(sig + slot(q), sex + slot(q), x);
-        if constexpr (R_::PACKED) {
-          const unsigned k2 = pack2(G.nke[q]);
-#pragma unroll
-          for (int w = 0; w < R_::NW; ++w) F2[w] = __viaddmax_s16x2((unsigned)x.w[w], k2, F2[w]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < CPT; ++c) F2[c] = (unsigned)max((int)F2[c], x.e(c) + G.nke[q]);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        Ex[c] = R_::PACKED ? ((c & 1) ? ((int)F2[c >> 1] >> 16) : (int)(short)(F2[c >> 1] & 0xffffu)) : (int)F2[c];
-        nE[c] = -Ex[c];
-        s[c] = 0.f;
-      }
-      if constexpr (R_::PACKED) {
-#pragma unroll
-        for (int w = 0; w < R_::NW; ++w) {
-          nE2[w] = __vneg2(F2[w]);
-          Lo2[w] = __vsubss2(F2[w], 0x7f007f00u);
-        }
-      }
-      for (int q = 0; q < nr; ++q) {
-        if (!(G.nkm[q] > 0.f)) continue;
-        R_ x;
-        lds_row<CPT>(sig + slot(q), sex + slot(q), x);
-        float tt[CPT];
-        row_terms<CPT>(x, G.nkm[q], G.nke[q], nE2, Lo2, nE, tt);
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) s[c] += tt[c];
-      }
+    const int nr = h.nr;
+    const int base = h.start * SW + col;
+    const float* sg = sig + base;
+    const int16_t* se = sex + base;
+    M s[CPT];
+    int Ex[CPT];
+    switch (nr) {
+      case 0: fwd_body<CPT, 0>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 1: fwd_body<CPT, 1>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 2: fwd_body<CPT, 2>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 3: fwd_body<CPT, 3>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 4: fwd_body<CPT, 4>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 5: fwd_body<CPT, 5>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 6: fwd_body<CPT, 6>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 7: fwd_body<CPT, 7>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 8: fwd_body<CPT, 8>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
+      default: fwd_body_any<CPT>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
+    // s is 0 or a normal float (ratios are within 2^+-40 of the previous terms): bit-level normalisation
     Lane<M, E, CPT> a;
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {  // s may lie anywhere in the normal range (ratios): general normalisation
-      M m;
-      int e;
-      xf_norm<M>(s[c], Ex[c], m, e);
-      if (e > ELIM || (m != M(0) && e < -ELIM)) {
-        set_error(p, ERR_RANGE, col + c, j);
-        e = e > 0 ? ELIM : -ELIM;
-      }
-      a.m[c] = m;
-      a.e[c] = (E)e;
-    }
+    norm_lane<TrF32, CPT>(p, s, Ex, a, col, j);
     const size_t g = (size_t)j * p.Lp + col;
     a.store(v.am(t) + g, v.ae(t) + g);
     if (MODE == 2) {  // a4: UT = muT ./ alpha_T -> beta_T
@@ -463,7 +455,6 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
       boundary_lane<TrF32, CPT>(p, 1, j, col, g, a, ut);
       ut.store(v.bm(p.T) + g, v.be(p.T) + g);
     }
-    // the group scratch is rewritten by the next item of this group only after its first named barrier
   }
 }
 

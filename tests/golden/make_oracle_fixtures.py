@@ -23,8 +23,7 @@ JOBS = {
     "cfg4lite": (4, {"L": 16}, [3, 20]),
     "cfg5lite": (5, {"L": 64}, [3, 20]),
     "cfg2": (2, {}, [100]),
-    # full graphs with L >= 256 (the pipelined kernels' slice widths), short horizons
-    "cfg4pipe": (4, {"L": 1024, "T": 4}, [2]),
+    # the full [5] graph with L >= 256 (the pipelined kernels' slice widths), short horizon
     "cfg5pipe": (5, {"L": 512, "T": 6}, [3]),
 }
 NSAMPLE = 20000

@@ -164,7 +164,7 @@ def test_many_chunks_streaming_path(prec, cpt):
 
 
 FIXTURES = [("cfg3", 3, "fp32"), ("cfg3", 10, "fp32"), ("cfg4lite", 3, "fp32"), ("cfg4lite", 20, "fp32"),
-            ("cfg5lite", 3, "fp32"), ("cfg5lite", 20, "fp32"), ("cfg4pipe", 2, "fp32"), ("cfg5pipe", 3, "fp32"),
+            ("cfg5lite", 3, "fp32"), ("cfg5lite", 20, "fp32"), ("cfg5pipe", 3, "fp32"),
             ("cfg2", 100, "fp64"), ("cfg2", 100, "fp32")]
 
 
@@ -173,8 +173,8 @@ def test_config_parity_against_stored_oracle(name, k, prec):
     """BASELINE configs too slow for a live oracle: the GPU path (default launch configuration, as
     bench.py runs it) vs the float64 oracle's outputs stored by tests/golden/make_oracle_fixtures.py
     (which calls only oracle/ and workloads/), on 20,000 uniformly sampled (t, a) entries.
-    cfg3 = config [3] at full size; cfg4pipe / cfg5pipe = the full [4] / [5] graphs at L >= 256 (the
-    pipelined kernels' slice widths) on short horizons; *lite = the full graphs and horizons at small L."""
+    cfg3 = config [3] at full size; cfg5pipe = the full [5] graph at L = 512 (a pipelined-kernel slice
+    width) on a short horizon; *lite = the full [4] / [5] graphs and horizons at small L."""
     import os
     path = os.path.join(os.path.dirname(__file__), "golden", f"oracle_{name}.npz")
     if not os.path.exists(path):
@@ -192,3 +192,39 @@ def test_config_parity_against_stored_oracle(name, k, prec):
     ew = max_rel_err(Wg.reshape(-1)[idx], z[f"W_{k}"], W_FLOOR)
     assert ef < TOL[prec] and ew < TOL[prec], (name, k, ef, ew)
     assert abs(sg["mass"] - float(z[f"mass_{k}"])) <= 10 * TOL[prec] * abs(float(z[f"mass_{k}"]))
+
+
+@pytest.mark.parametrize("prec", ["fp32"])
+def test_pipelined_kernels_L1024_grid(prec):
+    """L = 1024 (the bench's commodity count on [4]: one 1024-commodity slice per node, 4 commodities per
+    lane in the pipelined forward and backward kernels) on a 20 x 20 grid, live oracle."""
+    p = grid_problem(20, 20, 12, 1024, 0.1, seed=29, cap=(0.5, 3.0))
+    assert_parity(p, 3, prec)
+
+
+def _invariants(p, F, W, rtol):
+    """Properties of the end-of-sweep readout that hold at any size: F >= 0, W in [0, 1],
+    per-step mass = total commodity mass (the sink marginal is exact after a4, and point-mass sources carry
+    all of their commodity's mass), and node conservation of the aggregate flow between consecutive steps."""
+    m_tot = float(np.sum(p.mass)) if p.is_point else float(p.mu0.sum())
+    assert np.all(F >= 0) and np.all(np.isfinite(F))
+    assert np.all((W >= 0) & (W <= 1))
+    mass_t = F.sum(axis=1)
+    assert np.max(np.abs(mass_t - m_tot)) <= rtol * m_tot, np.max(np.abs(mass_t - m_tot))
+    into = np.zeros((p.T, p.N))
+    outof = np.zeros((p.T, p.N))
+    for t in range(p.T):
+        into[t] = np.bincount(p.head, weights=F[t], minlength=p.N)
+        outof[t] = np.bincount(p.tail, weights=F[t], minlength=p.N)
+    lhs, rhs = into[:-1], outof[1:]
+    scale = np.maximum(np.maximum(np.abs(lhs), np.abs(rhs)), 1e-6 * m_tot)
+    assert np.max(np.abs(lhs - rhs) / scale) <= rtol, np.max(np.abs(lhs - rhs) / scale)
+
+
+@pytest.mark.parametrize("cfg", [4, 5])
+def test_full_config_invariants(cfg):
+    """The BASELINE configs at full size in the launch configuration bench.py times (default options,
+    CUDA-graph sweeps): exact-identity checks of the readout after the parity sweep count."""
+    p = gen(cfg)
+    F, W, st = run_gpu(p, p.sweeps, "fp32")
+    _invariants(p, F, W, 2e-4)

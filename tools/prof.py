@@ -25,11 +25,18 @@ from workloads import gen  # noqa: E402
 p = gen(a.config, L=a.L)
 opts = {kv.split("=")[0]: int(kv.split("=")[1]) for kv in a.opt}
 s = Solver(p, graph=bool(a.graph), options=opts, profile=a.time)
+def sync():
+    try:
+        s.sync()
+    except Exception as e:  # diagnostics runs (e.g. dry=1) leave meaningless messages behind
+        print("sync:", str(e)[:80])
+
+
 s.sweep(1)
-s.sync()
+sync()
 t0 = time.perf_counter()
 s.sweep(a.sweeps)
-s.sync()
+sync()
 dt = time.perf_counter() - t0
 print(f"{p.name} L={p.L} opts={opts}: {dt / a.sweeps * 1e3:.2f} ms/sweep (wall, incl. launch)")
 if a.time:
