@@ -211,9 +211,9 @@ def main():
     achieved = dom_bytes_per_launch / (dom_launch_ms / 1e3) / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "r01", "traffic.json")
-    if os.path.exists(tpath):  # ncu dram bytes per launch of the same kernel (committed capture)
+    if os.path.exists(tpath):  # ncu dram bytes per launch of the same kernel and workload (committed capture)
         with open(tpath) as f:
-            tj = json.load(f).get(dom)
+            tj = json.load(f).get(workload_name(p, args.config), {}).get(dom)
         if tj:
             traffic = tj["dram_read"] + tj["dram_write"]
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -159,11 +159,16 @@ def capacity_update(logd_t: np.ndarray, log_ks: np.ndarray) -> np.ndarray:
     return om
 
 
-def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None) -> None:
+def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
+                 reduce_lse: Optional[Callable] = None) -> None:
     """One Gauss-Seidel sweep in Algorithm 2's order.
 
     on_block(kind, t, mass) is called after every dual block update (kind in {"U0", "W", "UT"}),
-    with the tensor mass <K, U> at that moment, for the BCA-monotonicity pin (prp:sinkhorn)."""
+    with the tensor mass <K, U> at that moment, for the BCA-monotonicity pin (prp:sinkhorn).
+
+    reduce_lse(v) -> v_global: when the state holds only a slice of the commodities, combines the
+    per-arc log flow sums log sum_l exp(X[l, a]) over all slices (the commodities couple only
+    through this sum in the capacity update, rem:multi_tensor_scheme P:1139-1147)."""
     p = st.problem
     oi = st.in_seg[0]
     tail_i = p.tail[oi]
@@ -175,7 +180,10 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None) -> None:
     # a3: forward loop
     for t in range(p.T):
         X = st.a[t][:, p.tail] + st.lK[t][None, :] + st.b[t + 1][:, p.head]      # [L, A], no W
-        st.omega[t] = capacity_update(st.logd[t], _lse_rows(X))
+        lse = _lse_rows(X)
+        if reduce_lse is not None:
+            lse = reduce_lse(lse)
+        st.omega[t] = capacity_update(st.logd[t], lse)
         if on_block is not None:
             on_block("W", t, float(np.exp(X + st.omega[t][None, :]).sum()))
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]

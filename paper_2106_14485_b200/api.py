@@ -5,6 +5,7 @@ sweep happens in libmmf.so.  Commodity sharding: pass ``l_begin``/``l_count`` an
 """
 from __future__ import annotations
 
+import os
 from typing import Optional
 
 import numpy as np
@@ -33,7 +34,10 @@ class Solver:
             L.mmf_set_option(self.ctx, "graph", int(graph))
             L.mmf_set_option(self.ctx, "reorder", int(reorder))
             L.mmf_set_option(self.ctx, "profile", int(profile))
-            for k, v in (options or {}).items():
+            opts = dict(options or {})
+            if "kernels" not in opts and os.environ.get("MMF_KERNELS"):  # test / profiling override
+                opts["kernels"] = int(os.environ["MMF_KERNELS"])
+            for k, v in opts.items():
                 L.mmf_set_option(self.ctx, k, int(v))
             self.upload(problem, l_begin, l_count)
             if nccl_uid is not None:

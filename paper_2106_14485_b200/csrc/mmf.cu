@@ -8,9 +8,10 @@
 #include "../../include/mmf.h"
 #include "kernels.cuh"
 #include "tiled.cuh"
-#include "pipefwd.cuh"
+#include "win.cuh"
 
 #include <dlfcn.h>
+#include <cstdlib>
 
 #include <algorithm>
 #include <cmath>
@@ -91,7 +92,8 @@ struct mmf_ctx {
 
   // ---- options
   bool opt_graph = true, opt_reorder = true, opt_profile = false;
-  int opt_kernels = 5;  // 5 = TMA-pipelined backward + head-flow forward (production), 4 = register-gather head-flow
+  int opt_kernels = 6;  // 6 = sliding-window backward + pipelined forward (production), 5 = TMA-pipelined backward
+                        // + head-flow forward, 4 = register-gather head-flow
                         // kernels, 3 = wide-lane kernels, 2 = smem-staged tile kernels, 1 = per-node reference kernels
   int opt_tile = 32;    // max nodes per tile
   int opt_cpt = 0;      // commodities per lane (0 = auto: 2 for fp32, 1 for fp64)
@@ -118,6 +120,12 @@ struct mmf_ctx {
   PipeCfg5 pb{};      // pipelined backward kernel (opt_kernels == 5)
   PipeCfg5 pf{};      // pipelined forward kernel
   bool pipe_bwd = false, pipe_fwd = false;
+  // sliding-window kernels (opt_kernels == 6)
+  bool win_bwd = false;
+  int win_cpt = 2, win_Wb = 0;  // chosen with the node order in prepare()
+  WinCfg wcb{};                 // backward window configuration
+  WinDir wdo{};                 // out-direction tables (device pointers)
+  std::vector<int> h_wsrc_out, h_wfptr_out, h_wfnode_out;
   int ell_din = 0;
   int sms = 148;
 
@@ -329,6 +337,8 @@ void make_tiles(int N, const std::vector<int>& tail, const std::vector<int>& hea
   }
 }
 
+void build_window_tables(mmf_ctx* c);
+
 void derive_shapes(mmf_ctx* c) {
   int cpt_auto = c->prec == MMF_FP32 ? 2 : 1;
   if (c->opt_kernels == 4) {  // register-gather path: 4 fp32 commodities per lane keep 6 rows in registers
@@ -336,7 +346,7 @@ void derive_shapes(mmf_ctx* c) {
       cpt_auto = c->L >= 128 ? 4 : 2;
     else
       cpt_auto = c->L >= 64 ? 2 : 1;
-  } else if (c->opt_kernels == 3 || c->opt_kernels == 5) {
+  } else if (c->opt_kernels == 3 || c->opt_kernels >= 5) {
     if (c->prec == MMF_FP32)
       cpt_auto = c->L >= 512 ? 8 : (c->L >= 128 ? 4 : 2);
     else
@@ -350,7 +360,7 @@ void derive_shapes(mmf_ctx* c) {
   // pipelined backward (fp32, ELL width <= 32): slice width SW = 256 * cp commodities, S stages of
   // Dout rows x SW x 6 B in shared memory; the message row length Lp is padded to a multiple of SW
   c->pipe_bwd = false;
-  if (c->opt_kernels == 5 && c->prec == MMF_FP32 && c->pb.D > 0 && c->pb.D <= 32 && c->L >= 256) {
+  if (c->opt_kernels >= 5 && c->prec == MMF_FP32 && c->pb.D > 0 && c->pb.D <= 32 && c->L >= 256) {
     // slice width SW = 256 * cp; the row ring holds R rows of SW (6 B each); want >= ~6 average items
     // in flight (A / N rows each) plus one worst-case item
     const size_t budget = 220 * 1024;
@@ -377,6 +387,29 @@ void derive_shapes(mmf_ctx* c) {
       c->Lp = (c->L + q - 1) / q * q;
       c->pb.ns = c->Lp / SW;
       c->pb.nitems = c->N * c->pb.ns;
+    }
+  }
+  // sliding-window backward (kernels == 6): tables depend on the order chosen in prepare()
+  c->win_bwd = false;
+  if (c->opt_kernels == 6 && c->prec == MMF_FP32 && c->L >= 32 && !c->h_outptr.empty()) {
+    build_window_tables(c);
+    const int SW = 32 * c->win_cpt;
+    const int q = std::max(SW, c->LC);
+    const int Lp = std::max(c->Lp, (c->L + q - 1) / q * q);
+    WinCfg& w = c->wcb;
+    w.ns = Lp / SW;
+    w.nseg = std::max(1, c->sms / w.ns);
+    w.segB = (w.nblk + w.nseg - 1) / w.nseg;
+    w.nseg = (w.nblk + w.segB - 1) / w.segB;
+    const size_t sm = c->win_cpt == 4 ? win_smem<4>(w).total : c->win_cpt == 2 ? win_smem<2>(w).total : win_smem<1>(w).total;
+    // (many narrow slices re-stream the window and records once per slice: the pipelined kernel wins there)
+    if (sm <= 227 * 1024 && Lp % SW == 0 && w.ns <= 64) {
+      c->win_bwd = true;
+      c->Lp = Lp;
+      if (c->pipe_bwd) {
+        c->pb.ns = c->Lp / c->pb.SW;
+        c->pb.nitems = c->N * c->pb.ns;
+      }
     }
   }
   // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width)
@@ -437,13 +470,173 @@ void derive_shapes(mmf_ctx* c) {
 
 // host-side graph structures: node order (tiles), internal arc order (in-CSR by head), out-CSR,
 // tile halos and halo-local indices.  Depends on the graph and options only.
+// ---- sliding-window node order (opt_kernels == 6) -------------------------------------------------
+// Candidates: the input order, reverse Cuthill-McKee, and "strip" versions of both (the order cut into rows
+// of its 90th-percentile bandwidth, then strips of w columns visited strip by strip, row by row: on a
+// row-major grid this is the classic strip order, bandwidth w instead of the row length).  For each
+// candidate and window half-width Wb (in 32-node blocks) the fraction f of moving arcs whose endpoints
+// lie more than Wb blocks apart is measured; cost = (|A|/N) f + 2 Wb / (blocks per segment) (+ a small
+// penalty for 32-commodity slices), subject to the window fitting in shared memory.
+std::vector<int> strip_newid(const std::vector<int>& rank, int b, int w) {
+  const int N = (int)rank.size();
+  std::vector<int> ord(N);
+  std::iota(ord.begin(), ord.end(), 0);
+  b = std::max(b, 1);
+  std::sort(ord.begin(), ord.end(), [&](int x, int y) {
+    const int rx = rank[x] / b, cx = rank[x] % b, ry = rank[y] / b, cy = rank[y] % b;
+    const int sx = cx / w, sy = cy / w;
+    if (sx != sy) return sx < sy;
+    if (rx != ry) return rx < ry;
+    return cx < cy;
+  });
+  std::vector<int> nid(N);
+  for (int k = 0; k < N; ++k) nid[ord[k]] = k;
+  return nid;
+}
+
+size_t win_bwd_smem(int cpt, int Wb, int farmax, int maxrec, int segB) {
+  WinCfg wc{};
+  wc.RBa = 2 * Wb + 1 + WIN_PD;
+  wc.farmax = std::max(farmax, 1);
+  wc.maxrec = maxrec;
+  wc.segB = segB;
+  return cpt == 4 ? win_smem<4>(wc).total : cpt == 2 ? win_smem<2>(wc).total : win_smem<1>(wc).total;
+}
+
+void choose_window_order(mmf_ctx* c) {
+  const int N = c->N;
+  const size_t A = c->tail.size();
+  std::vector<std::vector<int>> cands;
+  cands.emplace_back(N);
+  std::iota(cands[0].begin(), cands[0].end(), 0);
+  cands.push_back(rcm_newid(N, c->tail, c->head));
+  for (int base = 0; base < 2; ++base) {
+    std::vector<int> d;
+    for (size_t a = 0; a < A; ++a)
+      if (c->tail[a] != c->head[a]) d.push_back(std::abs(cands[base][c->tail[a]] - cands[base][c->head[a]]));
+    if (d.empty()) continue;
+    // the "row length" of the order: the 90th percentile of |i - j| over moving arcs (robust to a few
+    // percent of long-range arcs such as highways)
+    std::nth_element(d.begin(), d.begin() + (size_t)(0.90 * (d.size() - 1)), d.end());
+    const int b90 = d[(size_t)(0.90 * (d.size() - 1))];
+    for (int w : {32, 64})
+      if (b90 > 2 * w) cands.push_back(strip_newid(cands[base], b90, w));
+  }
+  const double deg = (double)A / std::max(N, 1);
+  const int nblk = (N + WIN_BR - 1) / WIN_BR;
+  const size_t budget = 225 * 1024;
+  double best = 1e30;
+  int bi = 0, bW = 0, bc = 2;
+  std::vector<int> mark(N, -1), nfar(nblk);
+  for (size_t ci = 0; ci < cands.size(); ++ci) {
+    const std::vector<int>& nid = cands[ci];
+    // records of each block (out-direction: grouped by tail)
+    std::vector<int> recs(nblk, 0);
+    int moving = 0;
+    for (size_t a = 0; a < A; ++a) {
+      recs[nid[c->tail[a]] / WIN_BR]++;
+      moving += c->tail[a] != c->head[a];
+    }
+    const int maxrec = *std::max_element(recs.begin(), recs.end());
+    for (int Wb = 0; Wb <= 12; ++Wb) {
+      // far fraction and the largest per-block count of distinct far rows at this half-width
+      std::fill(nfar.begin(), nfar.end(), 0);
+      std::fill(mark.begin(), mark.end(), -1);
+      int far = 0;
+      for (size_t a = 0; a < A; ++a) {
+        const int bt = nid[c->tail[a]] / WIN_BR, k = nid[c->head[a]];
+        if (std::abs(k / WIN_BR - bt) <= Wb) continue;
+        ++far;
+        if (mark[k] != bt) {
+          mark[k] = bt;
+          nfar[bt]++;
+        }
+      }
+      const int farmax = *std::max_element(nfar.begin(), nfar.end());
+      const double f = moving ? (double)far / moving : 0.0;
+      for (int cpt : {4, 2, 1}) {
+        const int SW = 32 * cpt;
+        if (SW > 2 * c->L && cpt > 1) continue;  // (slices wider than the commodity count waste lanes)
+        const int ns = (c->L + SW - 1) / SW;
+        const int nseg = std::max(1, c->sms / std::max(ns, 1));
+        const int segB = (nblk + nseg - 1) / nseg;
+        const size_t sm = win_bwd_smem(cpt, Wb, farmax, maxrec, segB);
+        if (sm > budget) continue;
+        const double cost = deg * f + 2.0 * Wb / std::max(segB, 1) + (cpt == 4 ? 0.0 : cpt == 2 ? 0.08 : 0.3);
+        if (getenv("MMF_VERBOSE") && Wb <= 4)
+          fprintf(stderr, "[mmf] order cand %zu cpt %d Wb %d far %.4f farmax %d cost %.3f smem %zu\n", ci, cpt, Wb, f,
+                  farmax, cost, sm);
+        if (cost < best) {
+          best = cost;
+          bi = (int)ci;
+          bW = Wb;
+          bc = cpt;
+        }
+      }
+    }
+  }
+  c->newid = cands[bi];
+  c->win_Wb = bW;
+  c->win_cpt = bc;
+}
+
+// window tables of the out-direction (backward gathers): per out-CSR record the window slot or far index
+void build_window_tables(mmf_ctx* c) {
+  const int N = c->N, Wb = c->win_Wb, RBa = 2 * Wb + 1 + WIN_PD;
+  const int nblk = (N + WIN_BR - 1) / WIN_BR;
+  const int64_t A = c->A;
+  c->h_wsrc_out.assign(A, 0);
+  c->h_wfptr_out.assign(nblk + 1, 0);
+  c->h_wfnode_out.clear();
+  int farmax = 0, maxrec = 0;
+  std::vector<int> seen(N, -1);
+  for (int b = 0; b < nblk; ++b) {
+    const int v0 = b * WIN_BR, v1 = std::min(N, v0 + WIN_BR);
+    maxrec = std::max(maxrec, c->h_outptr[v1] - c->h_outptr[v0]);
+    int nf = 0;
+    for (int v = v0; v < v1; ++v)
+      for (int q = c->h_outptr[v]; q < c->h_outptr[v + 1]; ++q) {
+        const int k = c->h_outhead[q];
+        const int rb = k / WIN_BR;
+        if (std::abs(rb - b) <= Wb) {
+          c->h_wsrc_out[q] = (rb % RBa) * WIN_BR + k % WIN_BR;
+        } else {
+          if (seen[k] != b) {
+            seen[k] = b;
+            c->h_wfnode_out.push_back(k);
+            ++nf;
+          }
+          int idx = 0;
+          for (int f = c->h_wfptr_out[b]; f < (int)c->h_wfnode_out.size(); ++f)
+            if (c->h_wfnode_out[f] == k) {
+              idx = f - c->h_wfptr_out[b];
+              break;
+            }
+          c->h_wsrc_out[q] = RBa * WIN_BR + idx;
+        }
+      }
+    c->h_wfptr_out[b + 1] = (int)c->h_wfnode_out.size();
+    farmax = std::max(farmax, nf);
+  }
+  c->wcb.Wb = Wb;
+  c->wcb.RBa = RBa;
+  c->wcb.farmax = std::max(farmax, 1);
+  c->wcb.maxrec = std::max(maxrec, 1);
+  c->wcb.nblk = nblk;
+}
+
 void prepare(mmf_ctx* c) {
   if (c->prepared) return;
   const int N = c->N;
   const int64_t A = c->A;
   std::vector<int> order;
   const int B = c->opt_kernels >= 2 ? c->opt_tile : std::max(N, 1);
-  if (c->opt_kernels >= 2 && c->opt_order == 2) {
+  if (c->opt_kernels == 6 && c->opt_reorder) {
+    choose_window_order(c);
+    c->h_tile_ptr.assign(1, 0);
+    for (int v = B; v < N; v += B) c->h_tile_ptr.push_back(v);
+    c->h_tile_ptr.push_back(N);
+  } else if (c->opt_kernels >= 2 && c->opt_order == 2) {
     make_tiles(N, c->tail, c->head, B, c->opt_halo > 0 ? c->opt_halo : 2 * B, c->opt_reorder, order, c->h_tile_ptr);
     c->newid.assign(N, 0);
     for (int k = 0; k < N; ++k) c->newid[order[k]] = k;
@@ -615,6 +808,10 @@ size_t layout(mmf_ctx* c, char* base) {
     p.inrec = recs ? at(L.take(T * A * rb)) : nullptr;
     p.outrec = recs ? at(L.take(T * A * rb)) : nullptr;
     p.opos = (const int*)at(L.take(A * 4));
+    c->wdo.ptr = p.out_ptr;
+    c->wdo.src = c->win_bwd ? (const int*)at(L.take(A * 4)) : nullptr;
+    c->wdo.fptr = c->win_bwd ? (const int*)at(L.take(c->h_wfptr_out.size() * 4)) : nullptr;
+    c->wdo.fnode = c->win_bwd ? (const int*)at(L.take(c->h_wfnode_out.size() * 4 + 4)) : nullptr;
     const bool ell = c->pipe_bwd;
     p.Din = ell ? c->ell_din : 0;
     p.Dout = ell ? c->pb.D : 0;
@@ -904,6 +1101,17 @@ template <class T_> struct Eng {
   static void tiled_bwd(mmf_ctx* c, cudaStream_t s, int t) {
     LaunchScope ls(c, K_BWD, s);
     if constexpr (sizeof(M) == 4) {
+      if (c->win_bwd) {
+        const WinCfg& w = c->wcb;
+        const unsigned grid = (unsigned)(w.ns * w.nseg);
+        if (c->win_cpt == 4)
+          k_bwd_win<4><<<grid, WIN_THREADS, win_smem<4>(w).total, s>>>(c->dp, w, c->wdo, t);
+        else if (c->win_cpt == 2)
+          k_bwd_win<2><<<grid, WIN_THREADS, win_smem<2>(w).total, s>>>(c->dp, w, c->wdo, t);
+        else
+          k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(c->dp, w, c->wdo, t);
+        return;
+      }
       if (c->pipe_bwd) {
         const int cp = c->pb.SW / 256;
         if (cp == 4) pipe_bwd_cpt<4>(c, s, t);
@@ -949,7 +1157,7 @@ template <class T_> struct Eng {
   }
 
   static mmf_status enqueue_sweep(mmf_ctx* c, cudaStream_t s) {
-    if (c->opt_kernels == 5 && c->pipe_fwd && !c->comm) {
+    if (c->opt_kernels >= 5 && c->pipe_fwd && !c->comm) {
       for (int t = 0; t <= c->T; ++t) pipe_fwd(c, s, t);       // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
       for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
       return MMF_OK;
@@ -995,6 +1203,18 @@ template <class T_> struct Eng {
         CU(cudaFuncSetAttribute(k_bwd_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CU(cudaFuncSetAttribute(k_bwd_pipe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       }
+      if (c->win_bwd) {
+        if (c->win_cpt == 4)
+          CU(cudaFuncSetAttribute(k_bwd_win<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem<4>(c->wcb).total));
+        else if (c->win_cpt == 2)
+          CU(cudaFuncSetAttribute(k_bwd_win<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem<2>(c->wcb).total));
+        else
+          CU(cudaFuncSetAttribute(k_bwd_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem<1>(c->wcb).total));
+        if (getenv("MMF_VERBOSE"))
+          fprintf(stderr, "[mmf] window bwd: cpt %d Wb %d RBa %d ns %d nseg %d segB %d farmax %d maxrec %d smem %zu\n",
+                  c->win_cpt, c->wcb.Wb, c->wcb.RBa, c->wcb.ns, c->wcb.nseg, c->wcb.segB, c->wcb.farmax,
+                  c->wcb.maxrec, c->win_cpt == 4 ? win_smem<4>(c->wcb).total : c->win_cpt == 2 ? win_smem<2>(c->wcb).total : win_smem<1>(c->wcb).total);
+      }
       if (c->pipe_fwd) {
         const int sm = (int)pfwd_smem(c->pf.R, c->pf.D, c->pf.SW).total;
         CU(cudaFuncSetAttribute(k_fwd_pipe<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1034,11 +1254,6 @@ template <class T_> struct Eng {
   static mmf_status readout(mmf_ctx* ctx, cudaStream_t s) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
-    if (c->pipe_fwd && p.inrec) {  // the pipelined forward kernel maintains only the ELL records
-      LaunchScope ls(c, K_OTHER, s);
-      size_t n = (size_t)c->T * c->A;
-      k_init_recs<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
-    }
     if (c->opt_kernels >= 2) {
       for (int t = 0; t <= c->T; ++t) {
         tiled_fwd(c, s, t, 2);
@@ -1165,6 +1380,13 @@ mmf_status finalize(mmf_ctx* ctx) {
     std::vector<int> opos(A);
     for (int64_t k = 0; k < A; ++k) opos[c->h_outarc[k]] = (int)k;
     CU(cudaMemcpyAsync((void*)p.opos, opos.data(), A * 4, cudaMemcpyHostToDevice, s));
+    if (c->win_bwd) {
+      CU(cudaMemcpyAsync((void*)c->wdo.src, c->h_wsrc_out.data(), A * 4, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync((void*)c->wdo.fptr, c->h_wfptr_out.data(), c->h_wfptr_out.size() * 4, cudaMemcpyHostToDevice, s));
+      if (!c->h_wfnode_out.empty())
+        CU(cudaMemcpyAsync((void*)c->wdo.fnode, c->h_wfnode_out.data(), c->h_wfnode_out.size() * 4,
+                           cudaMemcpyHostToDevice, s));
+    }
     std::vector<int> eip, eop;
     if (p.ell_in) {
       eip.resize(A);
@@ -1351,7 +1573,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     if (k == "dry") ctx->opt_dry = (int)value;
     if (k == "copy") ctx->opt_copy = (int)value;
     if (k == "kernels") {
-      if (value < 1 || value > 5) return fail(ctx, MMF_EINVAL, "kernels must be 1, 2, 3, 4 or 5");
+      if (value < 1 || value > 6) return fail(ctx, MMF_EINVAL, "kernels must be 1 .. 6");
       ctx->opt_kernels = (int)value;
     }
     if (k == "tile") {

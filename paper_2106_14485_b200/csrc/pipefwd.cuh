@@ -28,6 +28,7 @@ namespace mmf {
 struct FwdHdr {
   unsigned kb[32];  // rows (compacted, nonzero factor): K W significand bits
   unsigned k2[32];  //   ... exponent, packed twice (int16x2)
+  int rarc[32];     //   ... arc position of the row
   int rowof[32];    // arcs (all in-arcs, q < na): row index or -1
   int aux[32];      //   ... arc id | bit 31 uncapacitated
   int rtail[32];    //   ... tail node
@@ -37,19 +38,16 @@ struct FwdHdr {
   float Km[32];
   int Ke[32];
   int eopos[32];    //   ... slot of the arc in the ELL out-records (cp.async)
+  int copos[32];    //   ... position of the arc in the out-CSR records (cp.async)
   unsigned capmask; // bit q: row q's arc is capacitated
   int nr, na, start, end;
   int pad[3];
 };
 
-// per consumer group scratch
+// per consumer group scratch: flow partials (row, warp), double-buffered by the group's item parity (a
+// warp may start the group's next item while another still reads this item's partials)
 struct FwdGrp {
-  float fpart[32][PIPE_NWC];  // flow partials (row, warp)
-  float rq[32];               // ratio W_new / W_old per row (linear)
-  unsigned nkb[32];           // new K W per row (slow path)
-  unsigned nk2[32];
-  int slow;
-  int pad[3];
+  float fpart[2][32][PIPE_NWC];
 };
 
 struct PFwdSmem {
@@ -114,60 +112,102 @@ __device__ __forceinline__ float bfly8(const float* v, int lane) {
   return r;
 }
 
-// capacity-dual update of the item's in-arcs by one warp (lane = arc position), publishing per-row
-// ratios and new factors to the group scratch
-__device__ __forceinline__ void fwd_update(const DevPtrs& p, const FwdHdr& h, FwdGrp& G, int t, int j, int D,
-                                           int lane) {
+// capacity-dual update of the item's in-arcs, lane = arc position.  Every warp of the group evaluates it
+// (cheap, and no second barrier is needed); warp 0 alone stores W and refreshes the records.  Returns, in
+// the arc's lane, the ratio r = W_new / W_old (linear; 1 for uncapacitated arcs) and the new factor K W;
+// *big: some |log2 r| > 40 (the item then takes the recompute path).
+struct FwdUpd {
+  float rq;
+  unsigned nkb, nk2;
+};
+__device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, const float (*fp)[PIPE_NWC], int t,
+                                             int j, int D, int lane, bool writer, bool* big_out) {
   typedef float M;
   View<TrF32> v(p);
   bool big = false;
+  FwdUpd u{1.f, 0x3f800000u, 0u};
   if (lane < h.na) {
     const int aux = h.aux[lane];
     const int row = h.rowof[lane];
+    if (row >= 0) {
+      u.nkb = h.kb[row];
+      u.nk2 = h.k2[row];
+    }
     if (aux >= 0) {
       const int a = aux;
       float s = 0.f;
       if (row >= 0)
 #pragma unroll
-        for (int w = 0; w < PIPE_NWC; ++w) s += G.fpart[row][w];
-      if (!(s == s) || isinf(s)) set_error(p, ERR_NAN, -1, a);
+        for (int w = 0; w < PIPE_NWC; ++w) s += fp[row][w];
       const float d = h.d[lane], w0 = h.wm[lane];
       const int e0 = h.we[lane];
       float wm;
       int we;
       w_new<TrF32>(d, w0, e0, (double)s, wm, we);
-      v.Wm(t - 1)[a] = wm;
-      v.We(t - 1)[a] = we;
-      // refresh the step's ELL records (in: this node's slot; out: the tail's slot); the CSR record copies
-      // used by the readout kernels are rebuilt from W before a readout (mmf.cu)
       ArcKW<M> rr;
       kw_clamp<TrF32>(h.Km[lane], h.Ke[lane], wm, we, rr.km, rr.ke);
-      rr.aux = aux;
-      rr.node = h.rtail[lane];
-      ((ArcKW<M>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
-      rr.node = j;
-      ((ArcKW<M>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + h.eopos[lane]] = rr;
+      if (writer) {
+        if (!(s == s) || isinf(s)) set_error(p, ERR_NAN, -1, a);
+        v.Wm(t - 1)[a] = wm;
+        v.We(t - 1)[a] = we;
+        // refresh the step's records: ELL (in: this node's slot; out: the tail's slot) and CSR (in: arc id;
+        // out: the arc's out-CSR position)
+        rr.aux = aux;
+        rr.node = h.rtail[lane];
+        ((ArcKW<M>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
+        ((ArcKW<M>*)p.inrec)[(size_t)(t - 1) * p.A + a] = rr;
+        rr.node = j;
+        ((ArcKW<M>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + h.eopos[lane]] = rr;
+        ((ArcKW<M>*)p.outrec)[(size_t)(t - 1) * p.A + h.copos[lane]] = rr;
+      }
       if (row >= 0) {
-        float rq = 0.f;
+        u.rq = 0.f;
         if (w0 > 0.f && wm > 0.f) {
           const int de = we - e0;
           big = de > 40 || de < -40;
-          if (!big) rq = (wm / w0) * __uint_as_float((unsigned)(de + 127) << 23);
+          if (!big) u.rq = (wm / w0) * __uint_as_float((unsigned)(de + 127) << 23);
         } else {
           big = true;  // W changed from / to exact zero
         }
-        G.rq[row] = rq;
-        G.nkb[row] = __float_as_uint(rr.km);
-        G.nk2[row] = pack2(rr.ke);
+        u.nkb = __float_as_uint(rr.km);
+        u.nk2 = pack2(rr.ke);
       }
-    } else if (row >= 0) {
-      G.rq[row] = 1.f;
-      G.nkb[row] = h.kb[row];
-      G.nk2[row] = h.k2[row];
     }
   }
-  const unsigned anyb = __ballot_sync(0xffffffffu, big);
-  if (lane == 0) G.slow = anyb != 0u;
+  *big_out = __any_sync(0xffffffffu, big);
+  return u;
+}
+
+// alpha from the new factors (gathered from the arcs' lanes), two passes over shared memory
+template <int CPT>
+__device__ __forceinline__ void fwd_alpha_new(const float* sg, const int16_t* se, const FwdHdr& h, const FwdUpd& u,
+                                              int nr, int lane, float* s, int* Ex) {
+  constexpr int SW = pipe_sw<CPT>();
+  unsigned E2[CPT];
+  xmax_init<CPT>(E2);
+  for (int q = 0; q < nr; ++q) {
+    const int src = h.rarc[q];
+    const unsigned kb = __shfl_sync(0xffffffffu, u.nkb, src), k2 = __shfl_sync(0xffffffffu, u.nk2, src);
+    if (!(__uint_as_float(kb) > 0.f)) continue;
+    Row<TrF32, CPT> x;
+    x.load(sg + q * SW, se + q * SW);
+    xmax_add<CPT>(E2, x, k2, k2_to_ke(k2));
+  }
+  XPre<CPT> P;
+  P.set(E2);
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    s[c] = 0.f;
+    Ex[c] = P.E[c];
+  }
+  for (int q = 0; q < nr; ++q) {
+    const int src = h.rarc[q];
+    const unsigned kb = __shfl_sync(0xffffffffu, u.nkb, src), k2 = __shfl_sync(0xffffffffu, u.nk2, src);
+    if (!(__uint_as_float(kb) > 0.f)) continue;
+    Row<TrF32, CPT> x;
+    x.load(sg + q * SW, se + q * SW);
+    xacc<CPT>(x, kb, k2, k2_to_ke(k2), P, s);
+  }
 }
 
 // the own row beta_t[j] scaled to the terms' exponents: beta_lin[c] = beta[j,c] 2^E[c] (flows are bounded
@@ -184,8 +224,8 @@ __device__ __forceinline__ void beta_lin(const Row<TrF32, CPT>& b, const XPre<CP
 // the flows + update + alpha of one item with N (compile-time) rows; returns (s, Ex)
 template <int CPT, int N>
 __device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, const int16_t* se, const FwdHdr& h,
-                                         FwdGrp& G, int t, int j, int D, int lane, int wg, int bar_id, float* s,
-                                         int* Ex) {
+                                         float (*fp)[PIPE_NWC], int t, int j, int D, int lane, int wg, int bar_id,
+                                         float* s, int* Ex) {
   constexpr int SW = pipe_sw<CPT>();
   typedef Row<TrF32, CPT> R_;
   R_ b;
@@ -218,12 +258,12 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, cons
     }
     const float r = bfly8(f, lane);
     const int row = bfly_row(lane);
-    if ((lane & 3) == 0 && row < N && ((cap >> row) & 1u)) G.fpart[row][wg] = r;
+    if ((lane & 3) == 0 && row < N && ((cap >> row) & 1u)) fp[row][wg] = r;
   }
   named_bar(bar_id, PIPE_NWC * 32);
-  if (wg == 0) fwd_update(p, h, G, t, j, D, lane);
-  named_bar(bar_id, PIPE_NWC * 32);
-  if (!G.slow) {
+  bool big;
+  const FwdUpd u = fwd_update(p, h, fp, t, j, D, lane, wg == 0, &big);
+  if (!big) {
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       s[c] = 0.f;
@@ -231,20 +271,20 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, cons
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      const float r = G.rq[q];
+      const float r = __shfl_sync(0xffffffffu, u.rq, h.rarc[q]);
 #pragma unroll
       for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
     }
   } else {  // large ratios: recompute from shared memory with the new factors
-    sum_rows_any<CPT>(sg, se, G.nkb, G.nk2, N, s, Ex);
+    fwd_alpha_new<CPT>(sg, se, h, u, N, lane, s, Ex);
   }
 }
 
 // any row count (more than 8 rows): streaming flows, then the update, then alpha from shared memory
 template <int CPT>
 __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, const int16_t* se, const FwdHdr& h,
-                                             FwdGrp& G, int t, int j, int D, int lane, int wg, int bar_id, int nr,
-                                             float* s, int* Ex) {
+                                             float (*fp)[PIPE_NWC], int t, int j, int D, int lane, int wg, int bar_id,
+                                             int nr, float* s, int* Ex) {
   constexpr int SW = pipe_sw<CPT>();
   typedef Row<TrF32, CPT> R_;
   R_ b;
@@ -270,12 +310,12 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, 
 #pragma unroll
     for (int c = 0; c < CPT; ++c) f = fmaf(tt[c], bl[c], f);
     f = warp_sum<float>(f);
-    if (lane == 0) G.fpart[q][wg] = f;
+    if (lane == 0) fp[q][wg] = f;
   }
   named_bar(bar_id, PIPE_NWC * 32);
-  if (wg == 0) fwd_update(p, h, G, t, j, D, lane);
-  named_bar(bar_id, PIPE_NWC * 32);
-  sum_rows_any<CPT>(sg, se, G.nkb, G.nk2, nr, s, Ex);
+  bool big;
+  const FwdUpd u = fwd_update(p, h, fp, t, j, D, lane, wg == 0, &big);
+  fwd_alpha_new<CPT>(sg, se, h, u, nr, lane, s, Ex);
 }
 
 template <int CPT, int MODE>
@@ -361,6 +401,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
       if (ok) {
         h.kb[rs] = __float_as_uint(r.km);
         h.k2[rs] = pack2(r.ke);
+        h.rarc[rs] = lane;
       }
       if (valid) {
         h.rowof[lane] = ok ? rs : -1;
@@ -369,6 +410,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
         if (r.aux >= 0) {  // capacitated: dual-update operands
           const int a = r.aux;
           cp_async4(&h.eopos[lane], p.ell_opos + a);
+          cp_async4(&h.copos[lane], p.opos + a);
           cp_async4(&h.d[lane], dc + a);
           cp_async4(&h.wm[lane], Wm + a);
           cp_async4(&h.we[lane], We + a);
@@ -429,19 +471,20 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
     const int base = h.start * SW + col;
     const float* sg = sig + base;
     const int16_t* se = sex + base;
+    float (*fp)[PIPE_NWC] = G.fpart[(k / PIPE_NG) & 1];
     M s[CPT];
     int Ex[CPT];
     switch (nr) {
-      case 0: fwd_body<CPT, 0>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 1: fwd_body<CPT, 1>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 2: fwd_body<CPT, 2>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 3: fwd_body<CPT, 3>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 4: fwd_body<CPT, 4>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 5: fwd_body<CPT, 5>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 6: fwd_body<CPT, 6>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 7: fwd_body<CPT, 7>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 8: fwd_body<CPT, 8>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, s, Ex); break;
-      default: fwd_body_any<CPT>(p, sg, se, h, G, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
+      case 0: fwd_body<CPT, 0>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 1: fwd_body<CPT, 1>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 2: fwd_body<CPT, 2>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 3: fwd_body<CPT, 3>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 4: fwd_body<CPT, 4>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 5: fwd_body<CPT, 5>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 6: fwd_body<CPT, 6>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 7: fwd_body<CPT, 7>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 8: fwd_body<CPT, 8>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      default: fwd_body_any<CPT>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);

@@ -141,7 +141,8 @@ def test_validation_errors():
                                        ("fp64", dict(cpt=2)), ("fp32", dict(tile=1)), ("fp32", dict(tile=7)),
                                        ("fp64", dict(tile=128)), ("fp32", dict(reorder=0)),
                                        ("fp32", dict(kernels=3)), ("fp64", dict(kernels=3)),
-                                       ("fp32", dict(kernels=3, cpt=8)), ("fp32", dict(kernels=4, cpt=8))])
+                                       ("fp32", dict(kernels=3, cpt=8)), ("fp32", dict(kernels=4, cpt=8)),
+                                       ("fp32", dict(kernels=6)), ("fp64", dict(kernels=6))])
 def test_kernel_variants(prec, opts):
     """Every kernel configuration (reference per-node kernels, lane widths, tile sizes, no reordering)
     meets the same parity bar; several tiles, several chunks and a ragged commodity tail."""
@@ -228,3 +229,16 @@ def test_full_config_invariants(cfg):
     p = gen(cfg)
     F, W, st = run_gpu(p, p.sweeps, "fp32")
     _invariants(p, F, W, 2e-4)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_nccl_exchange_path_one_rank(prec):
+    """The library's commodity-sharded sweep (per forward step: partial flows -> ncclAllReduce -> capacity-
+    dual update) on a one-rank NCCL communicator: same kernels and exchange calls as the
+    multi-GPU run, checked against the oracle."""
+    import torch
+    torch.cuda.nccl.version()  # loads the NCCL the library resolves at run time
+    from paper_2106_14485_b200 import _lib
+    uid = _lib.mmf_nccl_unique_id()
+    p = grid_problem(6, 7, 9, 150, 0.2, seed=26, cap=(0.3, 1.5))
+    assert_parity(p, 6, prec, nccl_uid=uid, nranks=1, rank=0)
