@@ -398,6 +398,7 @@ void derive_shapes(mmf_ctx* c) {
     const int Lp = std::max(c->Lp, (c->L + q - 1) / q * q);
     WinCfg& w = c->wcb;
     w.ns = Lp / SW;
+    w.dry = c->opt_dry;
     w.nseg = std::max(1, c->sms / w.ns);
     w.segB = (w.nblk + w.nseg - 1) / w.nseg;
     w.nseg = (w.nblk + w.segB - 1) / w.segB;

@@ -6,9 +6,9 @@
 //   (ii)  W_{t-1}[a] <- min(W_{t-1}[a] d[a] / F_{t-1}[a], 1)                         (eq:sinkhorn_graph_Vineq P:861)
 //   (iii) alpha_t[j] = sum_{a -> j} alpha_{t-1}[i_a] K W_{t-1}[a] with the updated W    (eq:psi_hat P:1031-1036)
 // The producer warp stages, per item: the compacted rows alpha_{t-1}[i_a] (nonzero factor) and the node's
-// own row beta_t[j] (cp.async.bulk; contiguous ring slots), the arc records (cp.async ring, prefetched),
-// and the dual-update operands d, W, K and the ELL out-slot of every capacitated in-arc (4-byte cp.async
-// into the item descriptor, tracked by the same mbarrier through cp.async.mbarrier.arrive.noinc).
+// own row beta_t[j] (cp.async.bulk; contiguous ring slots) and the arc records (cp.async ring, prefetched);
+// the consumers load the dual-update operands d, W, K (and record slots) of their arcs with plain loads
+// at the start of the item, overlapped with the flow computation.
 //
 // Consumers (a group of 8 warps per item, 2 groups alternating items) compute the per-row terms
 //   t_q[c] = alpha_q[c] K W_q 2^-E[c]     (E[c] = max_q exponent of alpha_q[c] K W_q, extended range)
@@ -25,20 +25,14 @@
 
 namespace mmf {
 
-struct FwdHdr {
+struct __align__(16) FwdHdr {
   unsigned kb[32];  // rows (compacted, nonzero factor): K W significand bits
   unsigned k2[32];  //   ... exponent, packed twice (int16x2)
   int rarc[32];     //   ... arc position of the row
   int rowof[32];    // arcs (all in-arcs, q < na): row index or -1
   int aux[32];      //   ... arc id | bit 31 uncapacitated
   int rtail[32];    //   ... tail node
-  float d[32];      //   ... dual-update operands (cp.async)
-  float wm[32];
-  int we[32];
-  float Km[32];
-  int Ke[32];
-  int eopos[32];    //   ... slot of the arc in the ELL out-records (cp.async)
-  int copos[32];    //   ... position of the arc in the out-CSR records (cp.async)
+
   unsigned capmask; // bit q: row q's arc is capacitated
   int nr, na, start, end;
   int pad[3];
@@ -112,6 +106,46 @@ __device__ __forceinline__ float bfly8(const float* v, int lane) {
   return r;
 }
 
+// W_new = min(W_old d / F, 1) in fp32 (d = 0 -> 0, F = 0 -> 1), W = wm 2^we with wm in [1, 2):
+// the ratio d / F is formed in fp32 (its exponent range covers every flow and capacity of the fp32 mode;
+// an overflow means W_new = 1), then W_old's significand is applied and the result renormalised.
+__device__ __forceinline__ void w_new_f32(float d, float wm0, int we0, float F, float& wm, int& we) {
+  if (d == 0.f) {
+    wm = 0.f;
+    we = EZERO;
+    return;
+  }
+  if (!(F > 0.f)) {
+    wm = 1.f;
+    we = 0;
+    return;
+  }
+  const float x = wm0 * (d / F);
+  if (!(x < 3.0e38f)) {  // (inf) W d / F >= 1
+    wm = 1.f;
+    we = 0;
+    return;
+  }
+  const unsigned u = __float_as_uint(x);  // x > 0 normal or subnormal
+  int e;
+  float m;
+  if ((u >> 23) == 0u) {  // subnormal: scale up by 2^64
+    const unsigned v = __float_as_uint(x * 18446744073709551616.f);
+    m = __uint_as_float((v & 0x007fffffu) | 0x3f800000u);
+    e = we0 + (int)(v >> 23) - 127 - 64;
+  } else {
+    m = __uint_as_float((u & 0x007fffffu) | 0x3f800000u);
+    e = we0 + (int)(u >> 23) - 127;
+  }
+  if (e >= 0) {
+    wm = 1.f;
+    we = 0;
+  } else {
+    wm = m;
+    we = e;
+  }
+}
+
 // capacity-dual update of the item's in-arcs, lane = arc position.  Every warp of the group evaluates it
 // (cheap, and no second barrier is needed); warp 0 alone stores W and refreshes the records.  Returns, in
 // the arc's lane, the ratio r = W_new / W_old (linear; 1 for uncapacitated arcs) and the new factor K W;
@@ -120,8 +154,32 @@ struct FwdUpd {
   float rq;
   unsigned nkb, nk2;
 };
-__device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, const float (*fp)[PIPE_NWC], int t,
-                                             int j, int D, int lane, bool writer, bool* big_out) {
+// the dual-update operands of the lane's arc (plain loads issued at the start of the item: their latency
+// overlaps the flow computation)
+struct FwdOps {
+  float d, wm, Km;
+  int we, Ke, eopos, copos;
+};
+__device__ __forceinline__ FwdOps fwd_ops(const DevPtrs& p, const FwdHdr& h, int t, int lane) {
+  FwdOps o{0.f, 1.f, 0.f, 0, 0, 0, 0};
+  if (lane < h.na) {
+    const int aux = h.aux[lane];
+    if (aux >= 0) {
+      View<TrF32> v(p);
+      o.d = v.dcap(t - 1)[aux];
+      o.wm = v.Wm(t - 1)[aux];
+      o.we = v.We(t - 1)[aux];
+      o.Km = v.Km(t - 1)[aux];
+      o.Ke = v.Ke(t - 1)[aux];
+      o.eopos = p.ell_opos[aux];
+      o.copos = p.opos[aux];
+    }
+  }
+  return o;
+}
+__device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, const FwdOps& o,
+                                             const float (*fp)[PIPE_NWC], int t, int j, int D, int lane, bool writer,
+                                             bool* big_out) {
   typedef float M;
   View<TrF32> v(p);
   bool big = false;
@@ -139,13 +197,13 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
       if (row >= 0)
 #pragma unroll
         for (int w = 0; w < PIPE_NWC; ++w) s += fp[row][w];
-      const float d = h.d[lane], w0 = h.wm[lane];
-      const int e0 = h.we[lane];
+      const float d = o.d, w0 = o.wm;
+      const int e0 = o.we;
       float wm;
       int we;
-      w_new<TrF32>(d, w0, e0, (double)s, wm, we);
+      w_new_f32(d, w0, e0, s, wm, we);
       ArcKW<M> rr;
-      kw_clamp<TrF32>(h.Km[lane], h.Ke[lane], wm, we, rr.km, rr.ke);
+      kw_clamp<TrF32>(o.Km, o.Ke, wm, we, rr.km, rr.ke);
       if (writer) {
         if (!(s == s) || isinf(s)) set_error(p, ERR_NAN, -1, a);
         v.Wm(t - 1)[a] = wm;
@@ -157,15 +215,15 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
         ((ArcKW<M>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
         ((ArcKW<M>*)p.inrec)[(size_t)(t - 1) * p.A + a] = rr;
         rr.node = j;
-        ((ArcKW<M>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + h.eopos[lane]] = rr;
-        ((ArcKW<M>*)p.outrec)[(size_t)(t - 1) * p.A + h.copos[lane]] = rr;
+        ((ArcKW<M>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + o.eopos] = rr;
+        ((ArcKW<M>*)p.outrec)[(size_t)(t - 1) * p.A + o.copos] = rr;
       }
       if (row >= 0) {
         u.rq = 0.f;
         if (w0 > 0.f && wm > 0.f) {
           const int de = we - e0;
           big = de > 40 || de < -40;
-          if (!big) u.rq = (wm / w0) * __uint_as_float((unsigned)(de + 127) << 23);
+          if (!big) u.rq = __fdividef(wm, w0) * __uint_as_float((unsigned)(de + 127) << 23);
         } else {
           big = true;  // W changed from / to exact zero
         }
@@ -228,6 +286,7 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, cons
                                          float* s, int* Ex) {
   constexpr int SW = pipe_sw<CPT>();
   typedef Row<TrF32, CPT> R_;
+  const FwdOps o = fwd_ops(p, h, t, lane);
   R_ b;
   b.load(sg + N * SW, se + N * SW);  // own row beta_t[j]
   float tq[N > 0 ? N : 1][CPT];
@@ -262,7 +321,7 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, cons
   }
   named_bar(bar_id, PIPE_NWC * 32);
   bool big;
-  const FwdUpd u = fwd_update(p, h, fp, t, j, D, lane, wg == 0, &big);
+  const FwdUpd u = fwd_update(p, h, o, fp, t, j, D, lane, wg == 0, &big);
   if (!big) {
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -287,6 +346,7 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, 
                                              int nr, float* s, int* Ex) {
   constexpr int SW = pipe_sw<CPT>();
   typedef Row<TrF32, CPT> R_;
+  const FwdOps o = fwd_ops(p, h, t, lane);
   R_ b;
   b.load(sg + nr * SW, se + nr * SW);
   unsigned E2[CPT];
@@ -314,7 +374,7 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, 
   }
   named_bar(bar_id, PIPE_NWC * 32);
   bool big;
-  const FwdUpd u = fwd_update(p, h, fp, t, j, D, lane, wg == 0, &big);
+  const FwdUpd u = fwd_update(p, h, o, fp, t, j, D, lane, wg == 0, &big);
   fwd_alpha_new<CPT>(sg, se, h, u, nr, lane, s, Ex);
 }
 
@@ -336,7 +396,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
   const int D = pc.D, R = pc.R;
   if (threadIdx.x == 0) {
     for (int s = 0; s < PIPE_SD; ++s) {
-      mbar_init(&full[s], 1 + 32);     // expect_tx arrive + one cp.async (noinc) arrive per producer lane
+      mbar_init(&full[s], 1);          // expect_tx arrive (all rows land by TMA)
       mbar_init(&empty[s], PIPE_NWC);  // one consumer group per item
     }
     mbar_fence_init();
@@ -407,16 +467,6 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
         h.rowof[lane] = ok ? rs : -1;
         h.aux[lane] = r.aux;
         h.rtail[lane] = r.node;
-        if (r.aux >= 0) {  // capacitated: dual-update operands
-          const int a = r.aux;
-          cp_async4(&h.eopos[lane], p.ell_opos + a);
-          cp_async4(&h.copos[lane], p.opos + a);
-          cp_async4(&h.d[lane], dc + a);
-          cp_async4(&h.wm[lane], Wm + a);
-          cp_async4(&h.we[lane], We + a);
-          cp_async4(&h.Km[lane], Km + a);
-          cp_async4(&h.Ke[lane], Ke + a);
-        }
       }
       if (lane == 0) {
         // capmask over rows (row order = lane order of the nonzero-factor arcs)
@@ -432,11 +482,10 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
         h.start = rr.rpos;
         h.end = (int)(rr.head + (unsigned)(nr + 1));
       }
-      cp_async_mbar_arrive_noinc(&full[ds]);
-      prefetch();
-      __syncwarp();
+      __syncwarp();  // (the header writes of every lane precede lane 0's releasing arrive)
       if (lane == 0) mbar_arrive_expect_tx(&full[ds], (unsigned)(nr + 1) * (unsigned)SW * 6u);
       __syncwarp();
+      prefetch();
       if (ok) {
         const size_t g = (size_t)r.node * p.Lp;
         const int q = rr.rpos + rs;
