@@ -53,6 +53,7 @@ struct DevPtrs {
   const int* opos;      // [A] internal arc -> out-CSR position
   // ELL copies of the records for the pipelined kernels (or null): [T][N][D] per node, unused slots node = -1
   void* ell_in;         // in-arcs of each head: node = tail, aux = arc id | uncapacitated bit
+  void* ell_ops;        // [T][N][Din] ArcOps of the in-arcs (dual-update operands), same slots as ell_in (or null)
   void* ell_out;        // out-arcs of each tail: node = head
   const int* ell_ipos;  // [A] internal arc -> slot in ell_in (head * Din + k)
   const int* ell_opos;  // [A] internal arc -> slot in ell_out (tail * Dout + k)
@@ -74,6 +75,20 @@ template <> struct __align__(8) ArcKW<double> {
   int aux;
   int pad;
   double km;
+};
+
+// dual-update operands of an arc at step t, kept next to its in-record (fp32 mode, pipelined forward):
+// capacity, current W (significand, exponent), K (significand, exponent), and the arc's slots in the ELL
+// and CSR out-records
+struct __align__(16) ArcOps {
+  float d;
+  float wm;
+  int we;
+  float Km;
+  int Ke;
+  int eopos;
+  int copos;
+  int pad;
 };
 
 template <class T_> struct View {
@@ -215,6 +230,20 @@ __device__ __forceinline__ void write_recs(const DevPtrs& p, int t, int a, typen
   if (p.ell_in) {
     r.aux = a | uncap;
     ((ArcKW<M>*)p.ell_in)[(size_t)t * p.N * p.Din + p.ell_ipos[a]] = r;
+    if constexpr (sizeof(M) == 4) {
+      if (p.ell_ops) {
+        ArcOps o;
+        o.d = v.dcap(t)[a];
+        o.wm = wm;
+        o.we = we;
+        o.Km = v.Km(t)[a];
+        o.Ke = v.Ke(t)[a];
+        o.eopos = p.ell_opos[a];
+        o.copos = q;
+        o.pad = 0;
+        ((ArcOps*)p.ell_ops)[(size_t)t * p.N * p.Din + p.ell_ipos[a]] = o;
+      }
+    }
   }
   r.node = p.out_head[q];
   r.aux = a | uncap;

@@ -103,6 +103,7 @@ struct mmf_ctx {
   int opt_prefetch = 0; // wide kernels: L1 prefetch of significand rows in pass 1
   int opt_dry = 0;      // diagnostics: pipelined backward consumers skip the arithmetic
   int opt_copy = 0;     // pipelined kernels' row staging: 0 = TMA bulk copies, 1 = per-lane cp.async
+  int opt_wintma = 1;   // window kernels: 1 = 2-D TMA row-block loads, 0 = per-thread cp.async
 
   // ---- derived
   int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
@@ -125,6 +126,8 @@ struct mmf_ctx {
   int win_cpt = 2, win_Wb = 0;  // chosen with the node order in prepare()
   WinCfg wcb{};                 // backward window configuration
   WinDir wdo{};                 // out-direction tables (device pointers)
+  WinTmaps tmb{};               // TMA views of the beta store (backward gathers)
+  bool win_tma = false;
   std::vector<int> h_wsrc_out, h_wfptr_out, h_wfnode_out;
   int ell_din = 0;
   int sms = 148;
@@ -416,10 +419,10 @@ void derive_shapes(mmf_ctx* c) {
   // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width)
   c->pipe_fwd = false;
   if (c->pipe_bwd && c->pb.ns == 1 && c->ell_din > 0 && c->ell_din <= 32) {
-    const size_t budget = 220 * 1024;
+    const size_t budget = 220 * 1024 / FWD_NP;
     int R = 0;
     while (pfwd_smem(R + 1, c->ell_din, c->pb.SW).total <= budget) ++R;
-    if (R >= 2 * (c->ell_din + 1)) {
+    if (R >= c->ell_din + 1) {  // (an item's rows may wrap around its pipeline's ring)
       c->pipe_fwd = true;
       c->pf = c->pb;
       c->pf.D = c->ell_din;
@@ -626,6 +629,33 @@ void build_window_tables(mmf_ctx* c) {
   c->wcb.nblk = nblk;
 }
 
+// 2-D TMA tensor maps of a message store (slots x N rows of Lp commodities): box = 32 rows x SW
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+bool make_tmaps(mmf_ctx* c, void* msig, void* mexp, int slots, int SW, WinTmaps& out) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess || !f) return false;
+    fn = (EncodeTiledFn)f;
+  }
+  const cuuint64_t rows = (cuuint64_t)slots * c->N;
+  const cuuint32_t box[2] = {(cuuint32_t)SW, (cuuint32_t)WIN_BR};
+  const cuuint32_t es[2] = {1, 1};
+  cuuint64_t dim[2] = {(cuuint64_t)c->Lp, rows};
+  cuuint64_t st_s[1] = {(cuuint64_t)c->Lp * 4};
+  cuuint64_t st_e[1] = {(cuuint64_t)c->Lp * 2};
+  if (fn(&out.sig, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, msig, dim, st_s, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (fn(&out.exp, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, mexp, dim, st_e, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  return true;
+}
+
 void prepare(mmf_ctx* c) {
   if (c->prepared) return;
   const int N = c->N;
@@ -817,6 +847,7 @@ size_t layout(mmf_ctx* c, char* base) {
     p.Din = ell ? c->ell_din : 0;
     p.Dout = ell ? c->pb.D : 0;
     p.ell_in = ell ? at(L.take(T * N * (size_t)p.Din * 16)) : nullptr;
+    p.ell_ops = ell && c->prec == MMF_FP32 ? at(L.take(T * N * (size_t)p.Din * 32)) : nullptr;
     p.ell_out = ell ? at(L.take(T * N * (size_t)p.Dout * 16)) : nullptr;
     p.ell_ipos = ell ? (const int*)at(L.take(A * 4)) : nullptr;
     p.ell_opos = ell ? (const int*)at(L.take(A * 4)) : nullptr;
@@ -1077,8 +1108,8 @@ template <class T_> struct Eng {
   }
   template <int CPT, int MODE> static void pipe_fwd_launch(mmf_ctx* c, cudaStream_t s, int t) {
     const PipeCfg5& pc = c->pf;
-    const unsigned grid = (unsigned)std::min(c->N, c->sms);
-    k_fwd_pipe<CPT, MODE><<<grid, PIPE_THREADS, pfwd_smem(pc.R, pc.D, pc.SW).total, s>>>(c->dp, pc, t);
+    const unsigned grid = (unsigned)std::min((c->N + FWD_NP - 1) / FWD_NP, c->sms);
+    k_fwd_pipe<CPT, MODE><<<grid, FWD_THREADS, FWD_NP * pfwd_smem(pc.R, pc.D, pc.SW).total, s>>>(c->dp, pc, t);
   }
   static void pipe_fwd(mmf_ctx* c, cudaStream_t s, int t) {
     if constexpr (sizeof(M) == 4) {
@@ -1105,12 +1136,13 @@ template <class T_> struct Eng {
       if (c->win_bwd) {
         const WinCfg& w = c->wcb;
         const unsigned grid = (unsigned)(w.ns * w.nseg);
+        const int tma = c->win_tma ? 1 : 0;
         if (c->win_cpt == 4)
-          k_bwd_win<4><<<grid, WIN_THREADS, win_smem<4>(w).total, s>>>(c->dp, w, c->wdo, t);
+          k_bwd_win<4><<<grid, WIN_THREADS, win_smem<4>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
         else if (c->win_cpt == 2)
-          k_bwd_win<2><<<grid, WIN_THREADS, win_smem<2>(w).total, s>>>(c->dp, w, c->wdo, t);
+          k_bwd_win<2><<<grid, WIN_THREADS, win_smem<2>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
         else
-          k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(c->dp, w, c->wdo, t);
+          k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
         return;
       }
       if (c->pipe_bwd) {
@@ -1211,13 +1243,16 @@ template <class T_> struct Eng {
           CU(cudaFuncSetAttribute(k_bwd_win<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem<2>(c->wcb).total));
         else
           CU(cudaFuncSetAttribute(k_bwd_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)win_smem<1>(c->wcb).total));
+        c->win_tma = c->opt_wintma && c->win_cpt >= 2 && make_tmaps(c, c->dp.bm, c->dp.be, c->T + 1, 32 * c->win_cpt, c->tmb);
+        if (getenv("MMF_VERBOSE"))
+          fprintf(stderr, "[mmf] window tma %d\n", (int)c->win_tma);
         if (getenv("MMF_VERBOSE"))
           fprintf(stderr, "[mmf] window bwd: cpt %d Wb %d RBa %d ns %d nseg %d segB %d farmax %d maxrec %d smem %zu\n",
                   c->win_cpt, c->wcb.Wb, c->wcb.RBa, c->wcb.ns, c->wcb.nseg, c->wcb.segB, c->wcb.farmax,
                   c->wcb.maxrec, c->win_cpt == 4 ? win_smem<4>(c->wcb).total : c->win_cpt == 2 ? win_smem<2>(c->wcb).total : win_smem<1>(c->wcb).total);
       }
       if (c->pipe_fwd) {
-        const int sm = (int)pfwd_smem(c->pf.R, c->pf.D, c->pf.SW).total;
+        const int sm = FWD_NP * (int)pfwd_smem(c->pf.R, c->pf.D, c->pf.SW).total;
         CU(cudaFuncSetAttribute(k_fwd_pipe<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CU(cudaFuncSetAttribute(k_fwd_pipe<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CU(cudaFuncSetAttribute(k_fwd_pipe<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -1568,11 +1603,12 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
     if (k == "copy") ctx->opt_copy = (int)value;
+    if (k == "wintma") ctx->opt_wintma = (int)value;
     if (k == "kernels") {
       if (value < 1 || value > 6) return fail(ctx, MMF_EINVAL, "kernels must be 1 .. 6");
       ctx->opt_kernels = (int)value;

@@ -25,6 +25,17 @@
 
 namespace mmf {
 
+// The forward CTA runs FWD_NP independent pipelines, each one producer warp + one consumer group of 8 warps
+// with its own share of the shared memory (row ring, descriptors, record ring): the producer's per-item
+// serial latency (~0.9 us, mostly issuing the item's ~12 TMA copies; measured with idle consumers) is what
+// limits a single pipeline.  An item's rows may wrap around its ring (consumers resolve the wrap per row),
+// so a ring needs only D + 1 slots.
+constexpr int FWD_NG = 1;
+constexpr int FWD_NP = 2;
+constexpr int FWD_PW = PIPE_NWC * FWD_NG + 1;  // warps per pipeline
+constexpr int FWD_THREADS = FWD_NP * FWD_PW * 32;
+constexpr int FWD_SD = 8;  // item descriptors per pipeline (power of two)
+
 struct __align__(16) FwdHdr {
   unsigned kb[32];  // rows (compacted, nonzero factor): K W significand bits
   unsigned k2[32];  //   ... exponent, packed twice (int16x2)
@@ -32,6 +43,7 @@ struct __align__(16) FwdHdr {
   int rowof[32];    // arcs (all in-arcs, q < na): row index or -1
   int aux[32];      //   ... arc id | bit 31 uncapacitated
   int rtail[32];    //   ... tail node
+  ArcOps ops[32];   //   ... dual-update operands (prefetched with the records)
 
   unsigned capmask; // bit q: row q's arc is capacitated
   int nr, na, start, end;
@@ -45,30 +57,32 @@ struct FwdGrp {
 };
 
 struct PFwdSmem {
-  size_t off_full, off_empty, off_ring, off_hdr, off_grp, off_sig, off_exp, total;
+  size_t off_full, off_empty, off_ring, off_oring, off_hdr, off_grp, off_sig, off_exp, total;
 };
 
 __host__ __device__ inline PFwdSmem pfwd_smem(int R, int D, int SW) {
   PFwdSmem m;
   size_t o = 0;
   m.off_full = o;
-  o += 8 * (size_t)PIPE_SD;
+  o += 8 * (size_t)FWD_SD;
   m.off_empty = o;
-  o += 8 * (size_t)PIPE_SD;
+  o += 8 * (size_t)FWD_SD;
   o = (o + 15) / 16 * 16;
   m.off_ring = o;
   o += (size_t)PIPE_RP * D * 16;
+  m.off_oring = o;
+  o += (size_t)PIPE_RP * D * 32;
   m.off_hdr = o;
-  o += (size_t)PIPE_SD * sizeof(FwdHdr);
+  o += (size_t)FWD_SD * sizeof(FwdHdr);
   o = (o + 15) / 16 * 16;
   m.off_grp = o;
-  o += (size_t)PIPE_NG * sizeof(FwdGrp);
+  o += (size_t)FWD_NG * sizeof(FwdGrp);
   o = (o + 127) / 128 * 128;
   m.off_sig = o;
   o += (size_t)R * SW * 4;
   m.off_exp = o;
   o += (size_t)R * SW * 2;
-  m.total = o;
+  m.total = (o + 127) / 128 * 128;
   return m;
 }
 
@@ -163,17 +177,14 @@ struct FwdOps {
 __device__ __forceinline__ FwdOps fwd_ops(const DevPtrs& p, const FwdHdr& h, int t, int lane) {
   FwdOps o{0.f, 1.f, 0.f, 0, 0, 0, 0};
   if (lane < h.na) {
-    const int aux = h.aux[lane];
-    if (aux >= 0) {
-      View<TrF32> v(p);
-      o.d = v.dcap(t - 1)[aux];
-      o.wm = v.Wm(t - 1)[aux];
-      o.we = v.We(t - 1)[aux];
-      o.Km = v.Km(t - 1)[aux];
-      o.Ke = v.Ke(t - 1)[aux];
-      o.eopos = p.ell_opos[aux];
-      o.copos = p.opos[aux];
-    }
+    const ArcOps a = h.ops[lane];
+    o.d = a.d;
+    o.wm = a.wm;
+    o.we = a.we;
+    o.Km = a.Km;
+    o.Ke = a.Ke;
+    o.eopos = a.eopos;
+    o.copos = a.copos;
   }
   return o;
 }
@@ -213,6 +224,11 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
         rr.aux = aux;
         rr.node = h.rtail[lane];
         ((ArcKW<M>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
+        {
+          ArcOps* op = (ArcOps*)p.ell_ops + (size_t)(t - 1) * p.N * D + (size_t)j * D + lane;
+          op->wm = wm;
+          op->we = we;
+        }
         ((ArcKW<M>*)p.inrec)[(size_t)(t - 1) * p.A + a] = rr;
         rr.node = j;
         ((ArcKW<M>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + o.eopos] = rr;
@@ -237,10 +253,33 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
 }
 
 // alpha from the new factors (gathered from the arcs' lanes), two passes over shared memory
+// the own row beta_t[j] scaled to the terms' exponents: beta_lin[c] = beta[j,c] 2^E[c] (flows are bounded
+// by the mass: the exponent is clamped to the normal range)
 template <int CPT>
-__device__ __forceinline__ void fwd_alpha_new(const float* sg, const int16_t* se, const FwdHdr& h, const FwdUpd& u,
-                                              int nr, int lane, float* s, int* Ex) {
-  constexpr int SW = pipe_sw<CPT>();
+__device__ __forceinline__ void beta_lin(const Row<TrF32, CPT>& b, const XPre<CPT>& P, float* bl) {
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    const int es = b.e(c) + P.E[c];
+    bl[c] = (es < -126 || !(b.m[c] > 0.f)) ? 0.f : b.m[c] * __uint_as_float((unsigned)(min(es, 127) + 127) << 23);
+  }
+}
+
+// the flows + update + alpha of one item with N (compile-time) rows; returns (s, Ex)
+// ring row of an item's q-th row: items may wrap around the ring
+struct RingRows {
+  const float* sig;
+  const int16_t* sex;
+  int start, R, col, SW;
+  __device__ __forceinline__ int off(int q) const {
+    const int r = start + q;
+    return (r >= R ? r - R : r) * SW + col;
+  }
+};
+
+// alpha from the new factors (gathered from the arcs' lanes), two passes over shared memory
+template <int CPT>
+__device__ __forceinline__ void fwd_alpha_new(const RingRows& rw, const FwdHdr& h, const FwdUpd& u, int nr, int lane,
+                                              float* s, int* Ex) {
   unsigned E2[CPT];
   xmax_init<CPT>(E2);
   for (int q = 0; q < nr; ++q) {
@@ -248,7 +287,7 @@ __device__ __forceinline__ void fwd_alpha_new(const float* sg, const int16_t* se
     const unsigned kb = __shfl_sync(0xffffffffu, u.nkb, src), k2 = __shfl_sync(0xffffffffu, u.nk2, src);
     if (!(__uint_as_float(kb) > 0.f)) continue;
     Row<TrF32, CPT> x;
-    x.load(sg + q * SW, se + q * SW);
+    x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
     xmax_add<CPT>(E2, x, k2, k2_to_ke(k2));
   }
   XPre<CPT> P;
@@ -263,38 +302,25 @@ __device__ __forceinline__ void fwd_alpha_new(const float* sg, const int16_t* se
     const unsigned kb = __shfl_sync(0xffffffffu, u.nkb, src), k2 = __shfl_sync(0xffffffffu, u.nk2, src);
     if (!(__uint_as_float(kb) > 0.f)) continue;
     Row<TrF32, CPT> x;
-    x.load(sg + q * SW, se + q * SW);
+    x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
     xacc<CPT>(x, kb, k2, k2_to_ke(k2), P, s);
   }
 }
 
-// the own row beta_t[j] scaled to the terms' exponents: beta_lin[c] = beta[j,c] 2^E[c] (flows are bounded
-// by the mass: the exponent is clamped to the normal range)
-template <int CPT>
-__device__ __forceinline__ void beta_lin(const Row<TrF32, CPT>& b, const XPre<CPT>& P, float* bl) {
-#pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int es = b.e(c) + P.E[c];
-    bl[c] = (es < -126 || !(b.m[c] > 0.f)) ? 0.f : b.m[c] * __uint_as_float((unsigned)(min(es, 127) + 127) << 23);
-  }
-}
-
-// the flows + update + alpha of one item with N (compile-time) rows; returns (s, Ex)
 template <int CPT, int N>
-__device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, const int16_t* se, const FwdHdr& h,
+__device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw, const FwdHdr& h,
                                          float (*fp)[PIPE_NWC], int t, int j, int D, int lane, int wg, int bar_id,
                                          float* s, int* Ex) {
-  constexpr int SW = pipe_sw<CPT>();
   typedef Row<TrF32, CPT> R_;
   const FwdOps o = fwd_ops(p, h, t, lane);
   R_ b;
-  b.load(sg + N * SW, se + N * SW);  // own row beta_t[j]
+  b.load(rw.sig + rw.off(N), rw.sex + rw.off(N));  // own row beta_t[j]
   float tq[N > 0 ? N : 1][CPT];
   XPre<CPT> P;
   {
     R_ x[N > 0 ? N : 1];
 #pragma unroll
-    for (int q = 0; q < N; ++q) x[q].load(sg + q * SW, se + q * SW);
+    for (int q = 0; q < N; ++q) x[q].load(rw.sig + rw.off(q), rw.sex + rw.off(q));
     unsigned E2[CPT];
     xmax_init<CPT>(E2);
 #pragma unroll
@@ -335,25 +361,24 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const float* sg, cons
       for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
     }
   } else {  // large ratios: recompute from shared memory with the new factors
-    fwd_alpha_new<CPT>(sg, se, h, u, N, lane, s, Ex);
+    fwd_alpha_new<CPT>(rw, h, u, N, lane, s, Ex);
   }
 }
 
 // any row count (more than 8 rows): streaming flows, then the update, then alpha from shared memory
 template <int CPT>
-__device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, const int16_t* se, const FwdHdr& h,
+__device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& rw, const FwdHdr& h,
                                              float (*fp)[PIPE_NWC], int t, int j, int D, int lane, int wg, int bar_id,
                                              int nr, float* s, int* Ex) {
-  constexpr int SW = pipe_sw<CPT>();
   typedef Row<TrF32, CPT> R_;
   const FwdOps o = fwd_ops(p, h, t, lane);
   R_ b;
-  b.load(sg + nr * SW, se + nr * SW);
+  b.load(rw.sig + rw.off(nr), rw.sex + rw.off(nr));
   unsigned E2[CPT];
   xmax_init<CPT>(E2);
   for (int q = 0; q < nr; ++q) {
     R_ x;
-    x.load(sg + q * SW, se + q * SW);
+    x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
     xmax_add<CPT>(E2, x, h.k2[q], k2_to_ke(h.k2[q]));
   }
   XPre<CPT> P;
@@ -363,7 +388,7 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, 
   for (int q = 0; q < nr; ++q) {
     if (!((h.capmask >> q) & 1u)) continue;
     R_ x;
-    x.load(sg + q * SW, se + q * SW);
+    x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
     float tt[CPT];
     xterms<CPT>(x, h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, tt);
     float f = 0.f;
@@ -375,27 +400,31 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const float* sg, 
   named_bar(bar_id, PIPE_NWC * 32);
   bool big;
   const FwdUpd u = fwd_update(p, h, o, fp, t, j, D, lane, wg == 0, &big);
-  fwd_alpha_new<CPT>(sg, se, h, u, nr, lane, s, Ex);
+  fwd_alpha_new<CPT>(rw, h, u, nr, lane, s, Ex);
 }
 
 template <int CPT, int MODE>
-__global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5 pc, int t) {
+__global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5 pc, int t) {
   typedef float M;
   typedef int16_t E;
   constexpr int SW = pipe_sw<CPT>();
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(16) unsigned char smem_all[];
   const PFwdSmem L = pfwd_smem(pc.R, pc.D, SW);
+  const int pl = (threadIdx.x >> 5) / FWD_PW;                 // pipeline of this warp
+  unsigned char* smem = smem_all + (size_t)pl * L.total;      // its share of the shared memory
+  const int jstep = FWD_NP * gridDim.x, j0 = blockIdx.x + pl * gridDim.x;
   unsigned long long* full = (unsigned long long*)(smem + L.off_full);
   unsigned long long* empty = (unsigned long long*)(smem + L.off_empty);
   ArcKW<M>* ring = (ArcKW<M>*)(smem + L.off_ring);
+  ArcOps* oring = (ArcOps*)(smem + L.off_oring);
   FwdHdr* hdr = (FwdHdr*)(smem + L.off_hdr);
   FwdGrp* grps = (FwdGrp*)(smem + L.off_grp);
   M* sig = (M*)(smem + L.off_sig);
   E* sex = (E*)(smem + L.off_exp);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) % FWD_PW;  // (warp within the pipeline)
   const int D = pc.D, R = pc.R;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < PIPE_SD; ++s) {
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < FWD_SD; ++s) {
       mbar_init(&full[s], 1);          // expect_tx arrive (all rows land by TMA)
       mbar_init(&empty[s], PIPE_NWC);  // one consumer group per item
     }
@@ -404,7 +433,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
   __syncthreads();
   View<TrF32> v(p);
 
-  if (warp == PIPE_NWC * PIPE_NG) {  // ---------------- producer
+  if (warp == PIPE_NWC * FWD_NG) {  // ---------------- producer
     const ArcKW<M>* ell = (const ArcKW<M>*)p.ell_in + (size_t)(t - 1) * p.N * D;
     const M* gm = v.am(t - 1);
     const E* ge = v.ae(t - 1);
@@ -415,24 +444,29 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
     const int* We = v.We(t - 1);
     const M* Km = v.Km(t - 1);
     const int* Ke = v.Ke(t - 1);
-    int pnode = blockIdx.x, pslot = 0;
+    int pnode = j0, pslot = 0;
     auto prefetch = [&]() {
-      if (pnode < p.N && lane < D) cp_async16(&ring[pslot * D + lane], ell + (size_t)pnode * D + lane);
+      if (pnode < p.N && lane < D) {
+        cp_async16(&ring[pslot * D + lane], ell + (size_t)pnode * D + lane);
+        const ArcOps* go = (const ArcOps*)p.ell_ops + (size_t)(t - 1) * p.N * D + (size_t)pnode * D + lane;
+        cp_async16(&oring[pslot * D + lane], go);
+        cp_async16((char*)&oring[pslot * D + lane] + 16, (const char*)go + 16);
+      }
       cp_async_commit();
-      pnode += gridDim.x;
+      pnode += jstep;
       pslot = pslot + 1 == PIPE_RP ? 0 : pslot + 1;
     };
 #pragma unroll 1
     for (int k = 0; k < PIPE_P; ++k) prefetch();
     RowRing rr;
     auto release = [&]() {
-      const int ds = rr.kold & (PIPE_SD - 1);
-      mbar_wait(&empty[ds], (rr.kold / PIPE_SD) & 1);
+      const int ds = rr.kold & (FWD_SD - 1);
+      mbar_wait(&empty[ds], (rr.kold / FWD_SD) & 1);
       rr.tail = (unsigned)hdr[ds].end;
       ++rr.kold;
     };
     int k = 0, cslot = 0;
-    for (int j = blockIdx.x; j < p.N; j += gridDim.x, ++k) {
+    for (int j = j0; j < p.N; j += jstep, ++k) {
       cp_async_wait<PIPE_P - 1>();
       __syncwarp();
       ArcKW<M> r;
@@ -440,7 +474,11 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
       r.km = M(0);
       r.ke = 0;
       r.aux = 0;
-      if (lane < D) r = ring[cslot * D + lane];
+      ArcOps ro;
+      if (lane < D) {
+        r = ring[cslot * D + lane];
+        ro = oring[cslot * D + lane];
+      }
       cslot = cslot + 1 == PIPE_RP ? 0 : cslot + 1;
       __syncwarp();
       const bool valid = lane < D && r.node >= 0;
@@ -449,13 +487,9 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
       const unsigned obal = __ballot_sync(0xffffffffu, ok);
       const unsigned cbal = __ballot_sync(0xffffffffu, ok && r.aux >= 0);
       const int na = __popc(vbal), nr = __popc(obal);
-      while (rr.kold <= k - PIPE_SD) release();
-      if (rr.rpos + nr + 1 > R) {  // keep the item's rows contiguous
-        rr.head += (unsigned)(R - rr.rpos);
-        rr.rpos = 0;
-      }
-      while (rr.head + (unsigned)(nr + 1) - rr.tail > (unsigned)R && rr.kold < k) release();
-      const int ds = k & (PIPE_SD - 1);
+      while (rr.kold <= k - FWD_SD) release();
+      while (rr.head + (unsigned)(nr + 1) - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D + 1)
+      const int ds = k & (FWD_SD - 1);
       FwdHdr& h = hdr[ds];
       const int rs = __popc(obal & ((1u << lane) - 1u));
       if (ok) {
@@ -467,6 +501,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
         h.rowof[lane] = ok ? rs : -1;
         h.aux[lane] = r.aux;
         h.rtail[lane] = r.node;
+        h.ops[lane] = ro;
       }
       if (lane == 0) {
         // capmask over rows (row order = lane order of the nonzero-factor arcs)
@@ -488,13 +523,15 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
       prefetch();
       if (ok) {
         const size_t g = (size_t)r.node * p.Lp;
-        const int q = rr.rpos + rs;
+        int q = rr.rpos + rs;
+        if (q >= R) q -= R;
         bulk_g2s(sig + q * SW, gm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, ge + g, SW * 2, &full[ds]);
       }
       if (lane == 31) {  // the node's own beta_t row -> slot nr
         const size_t g = (size_t)j * p.Lp;
-        const int q = rr.rpos + nr;
+        int q = rr.rpos + nr;
+        if (q >= R) q -= R;
         bulk_g2s(sig + q * SW, bm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, be + g, SW * 2, &full[ds]);
       }
@@ -510,30 +547,33 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg
   const int grp = warp / PIPE_NWC, wg = warp % PIPE_NWC;
   FwdGrp& G = grps[grp];
   const int col = wg * 32 * CPT + lane * CPT;
-  const int bar_id = 1 + grp;
+  const int bar_id = 1 + pl;
   int k = grp;
-  for (int j = blockIdx.x + grp * gridDim.x; j < p.N; j += PIPE_NG * gridDim.x, k += PIPE_NG) {
-    const int ds = k & (PIPE_SD - 1);
-    mbar_wait(&full[ds], (k / PIPE_SD) & 1);
+  for (int j = j0; j < p.N; j += jstep, k += FWD_NG) {
+    const int ds = k & (FWD_SD - 1);
+    mbar_wait(&full[ds], (k / FWD_SD) & 1);
     const FwdHdr& h = hdr[ds];
+    if (pc.dry) {  // diagnostics: delivery rate of the producer / TMA alone
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ds]);
+      continue;
+    }
     const int nr = h.nr;
-    const int base = h.start * SW + col;
-    const float* sg = sig + base;
-    const int16_t* se = sex + base;
-    float (*fp)[PIPE_NWC] = G.fpart[(k / PIPE_NG) & 1];
+    const RingRows rw{sig, sex, h.start, R, col, SW};
+    float (*fp)[PIPE_NWC] = G.fpart[(k / FWD_NG) & 1];
     M s[CPT];
     int Ex[CPT];
     switch (nr) {
-      case 0: fwd_body<CPT, 0>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 1: fwd_body<CPT, 1>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 2: fwd_body<CPT, 2>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 3: fwd_body<CPT, 3>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 4: fwd_body<CPT, 4>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 5: fwd_body<CPT, 5>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 6: fwd_body<CPT, 6>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 7: fwd_body<CPT, 7>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 8: fwd_body<CPT, 8>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      default: fwd_body_any<CPT>(p, sg, se, h, fp, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
+      case 0: fwd_body<CPT, 0>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 1: fwd_body<CPT, 1>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 2: fwd_body<CPT, 2>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 3: fwd_body<CPT, 3>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 4: fwd_body<CPT, 4>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 5: fwd_body<CPT, 5>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 6: fwd_body<CPT, 6>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 7: fwd_body<CPT, 7>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 8: fwd_body<CPT, 8>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
+      default: fwd_body_any<CPT>(p, rw, h, fp, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);

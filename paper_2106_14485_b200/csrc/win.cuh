@@ -13,6 +13,7 @@
 //
 // Per-record tables (window slot or far index of the gathered row) are static and built on the host.
 #pragma once
+#include <cuda.h>
 #include "pipefwd.cuh"
 
 namespace mmf {
@@ -34,6 +35,13 @@ struct WinCfg {
   int dry;     // diagnostics: 1 = stream only (no arithmetic), 2 = no normalisation / store
 };
 
+// 2-D TMA views of the gathered message planes: significand (fp32) and exponent (u16) planes as
+// [rows = slots * N][Lp] tensors, box = 32 rows x SW commodities (one window row block per operation)
+struct WinTmaps {
+  CUtensorMap sig;
+  CUtensorMap exp;
+};
+
 struct WinDir {        // static tables of one gather direction (in-arcs or out-arcs)
   const int* ptr;      // [N + 1] CSR pointer of the direction (in_ptr / out_ptr)
   const int* src;      // [A] per CSR record: window slot (< RBa * 32) or RBa * 32 + far index
@@ -42,7 +50,7 @@ struct WinDir {        // static tables of one gather direction (in-arcs or out-
 };
 
 template <int CPT> struct WinSmem {
-  size_t off_sig, off_exp, off_rec, off_src, off_ptr, off_desc, off_flist, off_meta, total;
+  size_t off_sig, off_exp, off_rec, off_src, off_ptr, off_desc, off_flist, off_meta, off_bar, total;
   int rows;  // window rows + far rows + one zero row
 };
 // row space of the window arrays: [0, RBa*32) window ring, then (PD+1) far buffers of farmax rows, then a
@@ -53,7 +61,7 @@ template <int CPT> __host__ __device__ inline WinSmem<CPT> win_smem(const WinCfg
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t r = o;
-    o += (b + 15) / 16 * 16;
+    o += (b + 127) / 128 * 128;
     return r;
   };
   m.rows = c.RBa * WIN_BR + (WIN_PD + 1) * c.farmax + 1;
@@ -65,6 +73,7 @@ template <int CPT> __host__ __device__ inline WinSmem<CPT> win_smem(const WinCfg
   m.off_desc = take((size_t)2 * c.maxrec * 16);
   m.off_flist = take((size_t)(2 * WIN_PD + 1) * c.farmax * 4);
   m.off_meta = take((size_t)2 * (c.segB + 2 * WIN_PD + 3) * 4);
+  m.off_bar = take((size_t)c.RBa * 8);
   m.total = o;
   return m;
 }
@@ -104,9 +113,13 @@ template <int CPT> struct Win {
   int* flist;
   int* mb;   // record offset of block bs + i
   int* mf;   // far-list offset of block bs + i
+  unsigned long long* bar;  // [RBa] completion of the ring slots' TMA row-block loads
+  const WinTmaps* tm;       // (or null: cp.async row blocks)
+  int trow0;                // tensor row of node 0 of the gathered slot
   __device__ __forceinline__ Win(const DevPtrs& p_, const WinCfg& c_, const WinDir& d_, unsigned char* smem,
-                                 const ArcKW<float>* grec_, const float* gm_, const int16_t* ge_, int s, int g)
-      : p(p_), c(c_), d(d_), grec(grec_), gm(gm_), ge(ge_) {
+                                 const ArcKW<float>* grec_, const float* gm_, const int16_t* ge_, int s, int g,
+                                 const WinTmaps* tm_ = nullptr, int trow0_ = 0)
+      : p(p_), c(c_), d(d_), grec(grec_), gm(gm_), ge(ge_), tm(tm_), trow0(trow0_) {
     const WinSmem<CPT> L = win_smem<CPT>(c);
     sig = (float*)(smem + L.off_sig);
     sex = (int16_t*)(smem + L.off_exp);
@@ -115,6 +128,7 @@ template <int CPT> struct Win {
     ptr = (int*)(smem + L.off_ptr);
     desc = (WinDesc*)(smem + L.off_desc);
     flist = (int*)(smem + L.off_flist);
+    bar = (unsigned long long*)(smem + L.off_bar);
     mb = (int*)(smem + L.off_meta);
     mf = mb + (c.segB + 2 * WIN_PD + 3);
     col0 = s * SW;
@@ -139,6 +153,24 @@ template <int CPT> struct Win {
   __device__ __forceinline__ void issue_rowblock(int rb) {
     if (rb < 0 || rb >= nrb) return;
     const int slot = rb % c.RBa;
+    if (tm) {  // one 2-D TMA load per plane: rows rb*32 .. rb*32+31 of the slot, commodities col0 .. col0+SW
+      if (threadIdx.x == 0) {
+        fence_proxy_async();  // (the slot's previous generic-proxy reads precede the async-proxy write)
+        mbar_arrive_expect_tx(&bar[slot], (unsigned)(WIN_BR * SW * 6));
+        const int y = trow0 + rb * WIN_BR;
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                smem_u32(sig + slot * WIN_BR * SW)),
+            "l"(&tm->sig), "r"(col0), "r"(y), "r"(smem_u32(&bar[slot]))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+                smem_u32(sex + slot * WIN_BR * SW)),
+            "l"(&tm->exp), "r"(col0), "r"(y), "r"(smem_u32(&bar[slot]))
+            : "memory");
+      }
+      return;
+    }
     constexpr int CS = SW / 4, CE = SW / 8 > 0 ? SW / 8 : 1;  // 16-byte chunks per row
     for (int k = threadIdx.x; k < WIN_BR * CS; k += blockDim.x) {
       const int r = k / CS, q = k - r * CS;
@@ -214,6 +246,10 @@ template <int CPT> struct Win {
     }
   }
   __device__ __forceinline__ void prologue() {
+    if (tm && threadIdx.x == 0) {
+      for (int k = 0; k < c.RBa; ++k) mbar_init(&bar[k], 1);
+      mbar_fence_init();
+    }
     preload_meta();
     __syncthreads();
     for (int rb = bs - c.Wb; rb < bs + c.Wb + WIN_PD; ++rb) issue_rowblock(rb);
@@ -226,6 +262,7 @@ template <int CPT> struct Win {
     cp_async_commit();
     prepass(bs);
     cp_async_wait_n<0>();
+    for (int rb = bs - c.Wb; rb <= bs + c.Wb; ++rb) wait_rowblock(rb);
     __syncthreads();
   }
   // iteration b, after the top wait + barrier: prefetch ahead, then the descriptors of block b + 1
@@ -237,9 +274,17 @@ template <int CPT> struct Win {
     cp_async_commit();
     prepass(b + 1);
   }
+  // TMA row blocks: wait for row block rb.  This CTA loads row blocks rb0, rb0 + 1, ... in order, so the load
+  // of rb is use number (rb - rb0) / RBa of its ring slot's barrier -> phase parity
+  __device__ __forceinline__ void wait_rowblock(int rb) {
+    if (!tm || rb < 0 || rb >= nrb) return;
+    const int rb0 = max(bs - c.Wb, 0);
+    mbar_wait(&bar[rb % c.RBa], ((rb - rb0) / c.RBa) & 1);
+  }
   __device__ __forceinline__ void top(int b) {
     if (b > bs) {
       cp_async_wait_n<WIN_PD - 1>();
+      wait_rowblock(b + c.Wb);
       __syncthreads();
     }
   }
@@ -320,12 +365,14 @@ __device__ __forceinline__ void win_sum(const float* sig, const int16_t* sex, co
 
 // backward step t: beta_t[i] = sum_{a: i_a = i} K_t W_t[a] beta_{t+1}[j_a]  (eq:psi P:1038-1043)
 template <int CPT>
-__global__ void __launch_bounds__(WIN_THREADS, 1) k_bwd_win(DevPtrs p, WinCfg c, WinDir d, int t) {
+__global__ void __launch_bounds__(WIN_THREADS, 1) k_bwd_win(DevPtrs p, WinCfg c, WinDir d, const __grid_constant__ WinTmaps tmb,
+                                                            int use_tma, int t) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int s = blockIdx.x % c.ns, g = blockIdx.x / c.ns;
   if (g * c.segB >= c.nblk) return;
   View<TrF32> v(p);
-  Win<CPT> w(p, c, d, smem, (const ArcKW<float>*)p.outrec + (size_t)t * p.A, v.bm(t + 1), v.be(t + 1), s, g);
+  Win<CPT> w(p, c, d, smem, (const ArcKW<float>*)p.outrec + (size_t)t * p.A, v.bm(t + 1), v.be(t + 1), s, g,
+             use_tma ? &tmb : nullptr, (t + 1) * p.N);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   w.prologue();
   float* const bmt = v.bm(t);
