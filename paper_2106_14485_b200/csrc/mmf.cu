@@ -104,6 +104,10 @@ struct mmf_ctx {
   int opt_dry = 0;      // diagnostics: pipelined backward consumers skip the arithmetic
   int opt_copy = 0;     // pipelined kernels' row staging: 0 = TMA bulk copies, 1 = per-lane cp.async
   int opt_wintma = 1;   // window kernels: 1 = 2-D TMA row-block loads, 0 = per-thread cp.async
+  int opt_bwd = 0;      // backward kernel: 0 = auto (two-pipeline TMA kernel where it applies, else the window
+                        // kernel), 1 = two-pipeline TMA kernel, 2 = window kernel, 3 = pipe (1 pipeline)
+  PipeCfg5 pb2{};       // two-pipeline backward configuration
+  bool pipe2_bwd = false;
 
   // ---- derived
   int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
@@ -416,6 +420,22 @@ void derive_shapes(mmf_ctx* c) {
       }
     }
   }
+  // two-pipeline backward (same slices as the pipelined backward; rings of >= D rows per pipeline)
+  c->pipe2_bwd = false;
+  if (c->pipe_bwd && (c->opt_bwd == 1 || c->opt_bwd == 0)) {  // (auto: measured fastest on [3], [4], [5])
+    const size_t budget = 220 * 1024 / FWD_NP;
+    int R = 0;
+    while (pipe_smem(R + 1, FWD_SD, c->pb.D, c->pb.SW).total <= budget) ++R;
+    if (R >= c->pb.D) {
+      c->pipe2_bwd = true;
+      c->pb2 = c->pb;
+      c->pb2.R = R;
+      c->pb2.ns = c->Lp / c->pb.SW;
+      c->pb2.nitems = c->N * c->pb2.ns;
+      c->win_bwd = c->win_bwd && c->opt_bwd == 2;
+    }
+  }
+  if (c->opt_bwd == 3) c->win_bwd = false;
   // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width)
   c->pipe_fwd = false;
   if (c->pipe_bwd && c->pb.ns == 1 && c->ell_din > 0 && c->ell_din <= 32) {
@@ -1125,6 +1145,12 @@ template <class T_> struct Eng {
       else last ? pipe_fwd_launch<1, 2>(c, s, t) : pipe_fwd_launch<1, 1>(c, s, t);
     }
   }
+  template <int CPT> static void pipe2_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
+    const PipeCfg5& pc = c->pb2;
+    const size_t share = (pipe_smem(pc.R, FWD_SD, pc.D, pc.SW).total + 127) / 128 * 128;
+    const unsigned grid = (unsigned)std::min((pc.nitems + FWD_NP - 1) / FWD_NP, c->sms);
+    k_bwd_pipe2<CPT><<<grid, FWD_THREADS, FWD_NP * share, s>>>(c->dp, pc, t);
+  }
   template <int CPT> static void pipe_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     const PipeCfg5& pc = c->pb;
     const unsigned grid = (unsigned)std::min(pc.nitems, c->sms);
@@ -1143,6 +1169,13 @@ template <class T_> struct Eng {
           k_bwd_win<2><<<grid, WIN_THREADS, win_smem<2>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
         else
           k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
+        return;
+      }
+      if (c->pipe2_bwd) {
+        const int cp = c->pb2.SW / 256;
+        if (cp == 4) pipe2_bwd_cpt<4>(c, s, t);
+        else if (cp == 2) pipe2_bwd_cpt<2>(c, s, t);
+        else pipe2_bwd_cpt<1>(c, s, t);
         return;
       }
       if (c->pipe_bwd) {
@@ -1250,6 +1283,12 @@ template <class T_> struct Eng {
           fprintf(stderr, "[mmf] window bwd: cpt %d Wb %d RBa %d ns %d nseg %d segB %d farmax %d maxrec %d smem %zu\n",
                   c->win_cpt, c->wcb.Wb, c->wcb.RBa, c->wcb.ns, c->wcb.nseg, c->wcb.segB, c->wcb.farmax,
                   c->wcb.maxrec, c->win_cpt == 4 ? win_smem<4>(c->wcb).total : c->win_cpt == 2 ? win_smem<2>(c->wcb).total : win_smem<1>(c->wcb).total);
+      }
+      if (c->pipe2_bwd) {
+        const int sm = FWD_NP * (int)((pipe_smem(c->pb2.R, FWD_SD, c->pb2.D, c->pb2.SW).total + 127) / 128 * 128);
+        CU(cudaFuncSetAttribute(k_bwd_pipe2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_bwd_pipe2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_bwd_pipe2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       }
       if (c->pipe_fwd) {
         const int sm = FWD_NP * (int)pfwd_smem(c->pf.R, c->pf.D, c->pf.SW).total;
@@ -1603,12 +1642,13 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
     if (k == "copy") ctx->opt_copy = (int)value;
     if (k == "wintma") ctx->opt_wintma = (int)value;
+    if (k == "bwd") ctx->opt_bwd = (int)value;
     if (k == "kernels") {
       if (value < 1 || value > 6) return fail(ctx, MMF_EINVAL, "kernels must be 1 .. 6");
       ctx->opt_kernels = (int)value;

@@ -591,3 +591,190 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
 }
 
 }  // namespace mmf
+
+namespace mmf {
+
+// ------------------------------------------------------------------------------------------------
+// Pipelined backward with FWD_NP producer/consumer pipelines per CTA (the structure of k_fwd_pipe):
+//   beta_t[i, slice] = sum_{a: i_a = i} K_t W_t[a] beta_{t+1}[j_a, slice]   (eq:psi P:1038-1043)
+// items = (node, slice) pairs in grid-stride order, rows staged by TMA bulk copies into each pipeline's
+// ring (items may wrap), arc records prefetched with cp.async.
+template <int CPT, int N>
+__device__ __forceinline__ void ring_sum_n(const RingRows& rw, const PipeHdr& h, float* s, int* Ex) {
+  Row<TrF32, CPT> x[N > 0 ? N : 1];
+#pragma unroll
+  for (int q = 0; q < N; ++q) x[q].load(rw.sig + rw.off(q), rw.sex + rw.off(q));
+  unsigned E2[CPT];
+  xmax_init<CPT>(E2);
+#pragma unroll
+  for (int q = 0; q < N; ++q) xmax_add<CPT>(E2, x[q], h.k2[q], k2_to_ke(h.k2[q]));
+  XPre<CPT> P;
+  P.set(E2);
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    s[c] = 0.f;
+    Ex[c] = P.E[c];
+  }
+#pragma unroll
+  for (int q = 0; q < N; ++q) xacc<CPT>(x[q], h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, s);
+}
+template <int CPT>
+__device__ __forceinline__ void ring_sum_any(const RingRows& rw, const PipeHdr& h, int n, float* s, int* Ex) {
+  unsigned E2[CPT];
+  xmax_init<CPT>(E2);
+  for (int q = 0; q < n; ++q) {
+    Row<TrF32, CPT> x;
+    x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
+    xmax_add<CPT>(E2, x, h.k2[q], k2_to_ke(h.k2[q]));
+  }
+  XPre<CPT> P;
+  P.set(E2);
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) {
+    s[c] = 0.f;
+    Ex[c] = P.E[c];
+  }
+  for (int q = 0; q < n; ++q) {
+    Row<TrF32, CPT> x;
+    x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
+    xacc<CPT>(x, h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, s);
+  }
+}
+template <int CPT>
+__device__ __forceinline__ void ring_sum(const RingRows& rw, const PipeHdr& h, int n, float* s, int* Ex) {
+  switch (n) {
+    case 0: ring_sum_n<CPT, 0>(rw, h, s, Ex); break;
+    case 1: ring_sum_n<CPT, 1>(rw, h, s, Ex); break;
+    case 2: ring_sum_n<CPT, 2>(rw, h, s, Ex); break;
+    case 3: ring_sum_n<CPT, 3>(rw, h, s, Ex); break;
+    case 4: ring_sum_n<CPT, 4>(rw, h, s, Ex); break;
+    case 5: ring_sum_n<CPT, 5>(rw, h, s, Ex); break;
+    case 6: ring_sum_n<CPT, 6>(rw, h, s, Ex); break;
+    case 7: ring_sum_n<CPT, 7>(rw, h, s, Ex); break;
+    case 8: ring_sum_n<CPT, 8>(rw, h, s, Ex); break;
+    default: ring_sum_any<CPT>(rw, h, n, s, Ex); break;
+  }
+}
+
+template <int CPT>
+__global__ void __launch_bounds__(FWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg5 pc, int t) {
+  typedef float M;
+  typedef int16_t E;
+  constexpr int SW = pipe_sw<CPT>();
+  extern __shared__ __align__(16) unsigned char smem_all[];
+  const PipeSmem L = pipe_smem(pc.R, FWD_SD, pc.D, SW);
+  const size_t share = (L.total + 127) / 128 * 128;
+  const int pl = (threadIdx.x >> 5) / FWD_PW;
+  unsigned char* smem = smem_all + (size_t)pl * share;
+  unsigned long long* full = (unsigned long long*)(smem + L.off_full);
+  unsigned long long* empty = (unsigned long long*)(smem + L.off_empty);
+  ArcKW<M>* ring = (ArcKW<M>*)(smem + L.off_ring);
+  PipeHdr* hdr = (PipeHdr*)(smem + L.off_hdr);
+  M* sig = (M*)(smem + L.off_sig);
+  E* sex = (E*)(smem + L.off_exp);
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) % FWD_PW;
+  const int D = pc.D, R = pc.R;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < FWD_SD; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], PIPE_NWC);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  View<TrF32> v(p);
+  const ArcKW<M>* ell = (const ArcKW<M>*)p.ell_out + (size_t)t * p.N * D;
+  const M* gm = v.bm(t + 1);
+  const E* ge = v.be(t + 1);
+  const int step = FWD_NP * gridDim.x, item0 = blockIdx.x + pl * gridDim.x;
+
+  if (warp == PIPE_NWC) {  // ---------------- producer
+    ItemIt pf, cur;
+    pf.init(item0, step, pc.ns);
+    cur = pf;
+    int pslot = 0;
+    auto prefetch = [&]() {
+      if (pf.node < p.N && lane < D) cp_async16(&ring[pslot * D + lane], ell + (size_t)pf.node * D + lane);
+      cp_async_commit();
+      pf.next();
+      pslot = pslot + 1 == PIPE_RP ? 0 : pslot + 1;
+    };
+#pragma unroll 1
+    for (int k = 0; k < PIPE_P; ++k) prefetch();
+    RowRing rr;
+    auto release = [&]() {
+      const int ds = rr.kold & (FWD_SD - 1);
+      mbar_wait(&empty[ds], (rr.kold / FWD_SD) & 1);
+      rr.tail = (unsigned)hdr[ds].end;
+      ++rr.kold;
+    };
+    int cslot = 0;
+    for (int k = 0; cur.node < p.N; ++k, cur.next()) {
+      cp_async_wait<PIPE_P - 1>();
+      __syncwarp();
+      ArcKW<M> r;
+      r.node = -1;
+      r.km = M(0);
+      r.ke = 0;
+      if (lane < D) r = ring[cslot * D + lane];
+      cslot = cslot + 1 == PIPE_RP ? 0 : cslot + 1;
+      __syncwarp();
+      prefetch();
+      const bool ok = lane < D && r.node >= 0 && r.km > M(0);
+      const unsigned bal = __ballot_sync(0xffffffffu, ok);
+      const int n = __popc(bal);
+      while (rr.kold <= k - FWD_SD) release();
+      while (rr.head + (unsigned)n - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D)
+      const int ds = k & (FWD_SD - 1);
+      const int slot = __popc(bal & ((1u << lane) - 1u));
+      if (ok) {
+        hdr[ds].kb[slot] = __float_as_uint(r.km);
+        hdr[ds].k2[slot] = pack2(r.ke);
+      }
+      if (lane == 0) {
+        hdr[ds].n = n;
+        hdr[ds].start = rr.rpos;
+        hdr[ds].end = (int)(rr.head + (unsigned)n);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&full[ds], (unsigned)n * (unsigned)SW * 6u);
+      __syncwarp();
+      if (ok) {
+        const size_t g = (size_t)r.node * p.Lp + (size_t)cur.sl * SW;
+        int q = rr.rpos + slot;
+        if (q >= R) q -= R;
+        bulk_g2s(sig + q * SW, gm + g, SW * 4, &full[ds]);
+        bulk_g2s(sex + q * SW, ge + g, SW * 2, &full[ds]);
+      }
+      rr.head += (unsigned)n;
+      rr.rpos += n;
+      if (rr.rpos >= R) rr.rpos -= R;
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ---------------- consumers
+  const int col = warp * 32 * CPT + lane * CPT;
+  ItemIt it;
+  it.init(item0, step, pc.ns);
+  M* const bmt = v.bm(t);
+  E* const bet = v.be(t);
+  for (int k = 0; it.node < p.N; ++k, it.next()) {
+    const int ds = k & (FWD_SD - 1);
+    mbar_wait(&full[ds], (k / FWD_SD) & 1);
+    const PipeHdr& h = hdr[ds];
+    const RingRows rw{sig, sex, h.start, R, col, SW};
+    M s[CPT];
+    int Ex[CPT];
+    ring_sum<CPT>(rw, h, h.n, s, Ex);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[ds]);
+    Lane<M, E, CPT> out;
+    norm_lane<TrF32, CPT>(p, s, Ex, out, it.sl * SW + col, it.node);
+    const size_t g = (size_t)it.node * p.Lp + (size_t)(it.sl * SW + col);
+    out.store(bmt + g, bet + g);
+  }
+}
+
+}  // namespace mmf

@@ -5,6 +5,6 @@ python -c "import json; d=json.load(open('gpurun_out/bench_r01d.json')); print(d
 python tools/prof.py --config 4 --sweeps 1 > gpurun_out/plain.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k regex:k_fwd_pipe -s 5 -c 1 -o gpurun_out/ncu_fwd_r01f \
     python tools/prof.py --config 4 --sweeps 1 > gpurun_out/ncu_pfwd.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_bwd_win -s 230 -c 1 -o gpurun_out/ncu_bwd_r01f \
+ncu --set full --clock-control none --import-source on -k regex:k_bwd_pipe2 -s 230 -c 1 -o gpurun_out/ncu_bwd_r01f \
     python tools/prof.py --config 4 --sweeps 1 > gpurun_out/ncu_pbwd.log 2>&1
 echo done
