@@ -423,7 +423,7 @@ void derive_shapes(mmf_ctx* c) {
   // two-pipeline backward (same slices as the pipelined backward; rings of >= D rows per pipeline)
   c->pipe2_bwd = false;
   if (c->pipe_bwd && (c->opt_bwd == 1 || c->opt_bwd == 0)) {  // (auto: measured fastest on [3], [4], [5])
-    const size_t budget = 220 * 1024 / FWD_NP;
+    const size_t budget = 220 * 1024 / BWD_NP;
     int R = 0;
     while (pipe_smem(R + 1, FWD_SD, c->pb.D, c->pb.SW).total <= budget) ++R;
     if (R >= c->pb.D) {
@@ -1148,8 +1148,8 @@ template <class T_> struct Eng {
   template <int CPT> static void pipe2_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     const PipeCfg5& pc = c->pb2;
     const size_t share = (pipe_smem(pc.R, FWD_SD, pc.D, pc.SW).total + 127) / 128 * 128;
-    const unsigned grid = (unsigned)std::min((pc.nitems + FWD_NP - 1) / FWD_NP, c->sms);
-    k_bwd_pipe2<CPT><<<grid, FWD_THREADS, FWD_NP * share, s>>>(c->dp, pc, t);
+    const unsigned grid = (unsigned)std::min((pc.nitems + BWD_NP - 1) / BWD_NP, c->sms);
+    k_bwd_pipe2<CPT><<<grid, BWD_THREADS, BWD_NP * share, s>>>(c->dp, pc, t);
   }
   template <int CPT> static void pipe_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     const PipeCfg5& pc = c->pb;
@@ -1285,7 +1285,7 @@ template <class T_> struct Eng {
                   c->wcb.maxrec, c->win_cpt == 4 ? win_smem<4>(c->wcb).total : c->win_cpt == 2 ? win_smem<2>(c->wcb).total : win_smem<1>(c->wcb).total);
       }
       if (c->pipe2_bwd) {
-        const int sm = FWD_NP * (int)((pipe_smem(c->pb2.R, FWD_SD, c->pb2.D, c->pb2.SW).total + 127) / 128 * 128);
+        const int sm = BWD_NP * (int)((pipe_smem(c->pb2.R, FWD_SD, c->pb2.D, c->pb2.SW).total + 127) / 128 * 128);
         CU(cudaFuncSetAttribute(k_bwd_pipe2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CU(cudaFuncSetAttribute(k_bwd_pipe2<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
         CU(cudaFuncSetAttribute(k_bwd_pipe2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));

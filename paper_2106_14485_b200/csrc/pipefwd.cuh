@@ -656,8 +656,11 @@ __device__ __forceinline__ void ring_sum(const RingRows& rw, const PipeHdr& h, i
   }
 }
 
+constexpr int BWD_NP = 3;  // pipelines per CTA of the backward (56 registers per thread: three fit)
+constexpr int BWD_THREADS = BWD_NP * FWD_PW * 32;
+
 template <int CPT>
-__global__ void __launch_bounds__(FWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg5 pc, int t) {
+__global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg5 pc, int t) {
   typedef float M;
   typedef int16_t E;
   constexpr int SW = pipe_sw<CPT>();
@@ -686,7 +689,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
   const ArcKW<M>* ell = (const ArcKW<M>*)p.ell_out + (size_t)t * p.N * D;
   const M* gm = v.bm(t + 1);
   const E* ge = v.be(t + 1);
-  const int step = FWD_NP * gridDim.x, item0 = blockIdx.x + pl * gridDim.x;
+  const int step = BWD_NP * gridDim.x, item0 = blockIdx.x + pl * gridDim.x;
 
   if (warp == PIPE_NWC) {  // ---------------- producer
     ItemIt pf, cur;
