@@ -106,8 +106,22 @@ mmf_status mmf_attach_nccl(mmf_ctx* ctx, const void* unique_id128, int nranks, i
 /* Fill out128 with a fresh ncclUniqueId (call on one rank, then broadcast the 128 bytes). */
 mmf_status mmf_nccl_unique_id(void* out128);
 
-/* Options (call before mmf_init): key "graph" (1 = capture one sweep as a CUDA graph, default 1),
- * "reorder" (1 = locality node reordering, default 1), "profile" (1 = per-kernel CUDA-event timing). */
+/* Options (call before mmf_init unless noted; unknown key or out-of-range value -> MMF_EINVAL, a
+ * pre-init key after mmf_init -> MMF_ESTATE).  All kernel selections compute the same sweep (parity
+ * tested); they differ only in speed.
+ *   "graph"    1 = capture one sweep as a CUDA graph (default 1; may be changed any time)
+ *   "profile"  1 = per-kernel CUDA-event timing for mmf_read_kernel_stats (any time)
+ *   "prefetch" 1 = L2 prefetch hints in the wide-lane kernels (any time; recaptures the graph)
+ *   "reorder"  1 = locality node reordering (default 1)
+ *   "kernels"  kernel family 1..6 (default 6 = TMA-pipelined forward (2 pipelines / CTA) and
+ *              backward (3 pipelines / CTA); 5 single-pipeline; 4 register head-flow; 3 wide-lane;
+ *              2 smem node tiles; 1 per-node reference kernels)
+ *   "bwd"      backward kernel with kernels >= 5: 0 auto, 1 three-pipeline, 2 sliding window, 3 single
+ *   "wintma"   window backward row blocks by 2-D tensor TMA (1) or cp.async (0)
+ *   "order"    node order (kernels >= 2): 0 input, 1 reverse Cuthill-McKee, 2 BFS tiles (default)
+ *   "cpt"      commodities per thread 0 (auto), 1, 2, 4, 8
+ *   "tile", "halo", "cpc"  tile sizes of the kernels = 2 family
+ *   "dry", "copy"  profiling modes of the pipelined kernels (results invalid; never in production) */
 mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);
 
 /* W = 1, UT = 1 on supp(muT), one backward pass (Alg. 2 "Initialize").  Async. */
