@@ -104,6 +104,9 @@ struct mmf_ctx {
   int opt_dry = 0;      // diagnostics: pipelined backward consumers skip the arithmetic
   int opt_copy = 0;     // pipelined kernels' row staging: 0 = TMA bulk copies, 1 = per-lane cp.async
   int opt_wintma = 1;   // window kernels: 1 = 2-D TMA row-block loads, 0 = per-thread cp.async
+  int opt_fgw = 0;      // pipelined forward: warps per consumer group (0 auto, 8, 4, 2)
+  int opt_fng = 0;      // pipelined forward: consumer groups per pipeline (0 auto, 1 .. 6)
+  int opt_fnp = 0;      // pipelined forward: pipelines per CTA (0 auto, 1, 2)
   int opt_bwd = 0;      // backward kernel: 0 = auto (two-pipeline TMA kernel where it applies, else the window
                         // kernel), 1 = two-pipeline TMA kernel, 2 = window kernel, 3 = pipe (1 pipeline)
   PipeCfg5 pb2{};       // two-pipeline backward configuration
@@ -124,6 +127,7 @@ struct mmf_ctx {
   HeadCfg hc{};
   PipeCfg5 pb{};      // pipelined backward kernel (opt_kernels == 5)
   PipeCfg5 pf{};      // pipelined forward kernel
+  int pf_gw = 8, pf_ng = 1, pf_np = 2;  // its consumer groups: GW warps each, NG per pipeline, NP pipelines
   bool pipe_bwd = false, pipe_fwd = false;
   // sliding-window kernels (opt_kernels == 6)
   bool win_bwd = false;
@@ -436,17 +440,36 @@ void derive_shapes(mmf_ctx* c) {
     }
   }
   if (c->opt_bwd == 3) c->win_bwd = false;
-  // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width)
+  // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width), NG
+  // consumer groups of GW warps per pipeline (a warp owns 32 CPT = SW / GW commodities)
   c->pipe_fwd = false;
-  if (c->pipe_bwd && c->pb.ns == 1 && c->ell_din > 0 && c->ell_din <= 32) {
-    const size_t budget = 220 * 1024 / FWD_NP;
+  // (auto: for one 256-commodity slice the wide-lane forward is as fast; measured on [3])
+  if (c->pipe_bwd && c->pb.ns == 1 && c->ell_din > 0 && c->ell_din <= 32 && (c->pb.SW >= 512 || c->opt_fgw)) {
+    const int SW = c->pb.SW;
+    int gw = 8, ng = 1, np = 2;  // (the first compiled combination of this SW, unless options choose)
+    bool first = true;
+#define MMF_FWD_FIRST(sw, cpt, g, n, q)                                                         \
+  if (SW == sw && first && (!c->opt_fgw || c->opt_fgw == g) && (!c->opt_fng || c->opt_fng == n) && \
+      (!c->opt_fnp || c->opt_fnp == q)) {                                                       \
+    gw = g;                                                                                     \
+    ng = n;                                                                                     \
+    np = q;                                                                                     \
+    first = false;                                                                              \
+  }
+    MMF_FWD_COMBOS(MMF_FWD_FIRST)
+#undef MMF_FWD_FIRST
+    const size_t budget = 226 * 1024 / np;
     int R = 0;
-    while (pfwd_smem(R + 1, c->ell_din, c->pb.SW).total <= budget) ++R;
-    if (R >= c->ell_din + 1) {  // (an item's rows may wrap around its pipeline's ring)
+    while (pfwd_smem(R + 1, c->ell_din, SW, ng).total <= budget) ++R;
+    const int rmin = c->ell_din + (MMF_FWD_OWNG ? 0 : 1);  // rows of the largest item
+    if (!first && R >= rmin) {  // (an item's rows may wrap around its pipeline's ring)
       c->pipe_fwd = true;
       c->pf = c->pb;
       c->pf.D = c->ell_din;
       c->pf.R = R;
+      c->pf_gw = gw;
+      c->pf_ng = ng;
+      c->pf_np = np;
     }
   }
   c->nch = c->Lp / c->LC;
@@ -1126,10 +1149,18 @@ template <class T_> struct Eng {
     else if (c->CPT == 2) tiled_fwd_cpt<2>(c, s, t, fmode);
     else tiled_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
   }
-  template <int CPT, int MODE> static void pipe_fwd_launch(mmf_ctx* c, cudaStream_t s, int t) {
+  template <int CPT, int GW, int NG, int NP, int MODE> static void pipe_fwd_launch(mmf_ctx* c, cudaStream_t s, int t) {
     const PipeCfg5& pc = c->pf;
-    const unsigned grid = (unsigned)std::min((c->N + FWD_NP - 1) / FWD_NP, c->sms);
-    k_fwd_pipe<CPT, MODE><<<grid, FWD_THREADS, FWD_NP * pfwd_smem(pc.R, pc.D, pc.SW).total, s>>>(c->dp, pc, t);
+    const unsigned grid = (unsigned)std::min((c->N + NP - 1) / NP, c->sms);
+    k_fwd_pipe<CPT, GW, NG, NP, MODE>
+        <<<grid, fwd_threads<GW, NG, NP>(), NP * pfwd_smem(pc.R, pc.D, pc.SW, NG).total, s>>>(c->dp, pc, t);
+  }
+  template <int MODE> static void pipe_fwd_mode(mmf_ctx* c, cudaStream_t s, int t) {
+    const int SW = c->pf.SW, gw = c->pf_gw, ng = c->pf_ng, np = c->pf_np;
+#define MMF_FWD_COMBO(sw, cpt, g, n, q) \
+  if (SW == sw && gw == g && ng == n && np == q) return pipe_fwd_launch<cpt, g, n, q, MODE>(c, s, t);
+    MMF_FWD_COMBOS(MMF_FWD_COMBO)
+#undef MMF_FWD_COMBO
   }
   static void pipe_fwd(mmf_ctx* c, cudaStream_t s, int t) {
     if constexpr (sizeof(M) == 4) {
@@ -1138,11 +1169,8 @@ template <class T_> struct Eng {
         return;
       }
       LaunchScope ls(c, K_FUSED, s);
-      const int cp = c->pf.SW / 256;
-      const bool last = t == c->T;
-      if (cp == 4) last ? pipe_fwd_launch<4, 2>(c, s, t) : pipe_fwd_launch<4, 1>(c, s, t);
-      else if (cp == 2) last ? pipe_fwd_launch<2, 2>(c, s, t) : pipe_fwd_launch<2, 1>(c, s, t);
-      else last ? pipe_fwd_launch<1, 2>(c, s, t) : pipe_fwd_launch<1, 1>(c, s, t);
+      if (t == c->T) pipe_fwd_mode<2>(c, s, t);
+      else pipe_fwd_mode<1>(c, s, t);
     }
   }
   template <int CPT> static void pipe2_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
@@ -1291,13 +1319,17 @@ template <class T_> struct Eng {
         CU(cudaFuncSetAttribute(k_bwd_pipe2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
       }
       if (c->pipe_fwd) {
-        const int sm = FWD_NP * (int)pfwd_smem(c->pf.R, c->pf.D, c->pf.SW).total;
-        CU(cudaFuncSetAttribute(k_fwd_pipe<4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CU(cudaFuncSetAttribute(k_fwd_pipe<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CU(cudaFuncSetAttribute(k_fwd_pipe<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CU(cudaFuncSetAttribute(k_fwd_pipe<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CU(cudaFuncSetAttribute(k_fwd_pipe<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CU(cudaFuncSetAttribute(k_fwd_pipe<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        const int sm = c->pf_np * (int)pfwd_smem(c->pf.R, c->pf.D, c->pf.SW, c->pf_ng).total;
+        const int SW = c->pf.SW, gw = c->pf_gw, ng = c->pf_ng, np = c->pf_np;
+#define MMF_FWD_COMBO(sw, cpt, g, n, q)                                                                    \
+  if (SW == sw && gw == g && ng == n && np == q) {                                                         \
+    CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+    CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+  }
+        MMF_FWD_COMBOS(MMF_FWD_COMBO)
+#undef MMF_FWD_COMBO
+        if (getenv("MMF_VERBOSE"))
+          fprintf(stderr, "[mmf] pipe fwd: SW %d GW %d NG %d NP %d R %d D %d smem %d\n", SW, gw, ng, np, c->pf.R, c->pf.D, sm);
       }
     }
     {
@@ -1642,13 +1674,25 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
     if (k == "copy") ctx->opt_copy = (int)value;
     if (k == "wintma") ctx->opt_wintma = (int)value;
     if (k == "bwd") ctx->opt_bwd = (int)value;
+    if (k == "fgw") {
+      if (value != 0 && value != 2 && value != 4 && value != 8) return fail(ctx, MMF_EINVAL, "fgw must be 0, 2, 4 or 8");
+      ctx->opt_fgw = (int)value;
+    }
+    if (k == "fng") {
+      if (value < 0 || value > 6) return fail(ctx, MMF_EINVAL, "fng must be in [0, 6]");
+      ctx->opt_fng = (int)value;
+    }
+    if (k == "fnp") {
+      if (value < 0 || value > 2) return fail(ctx, MMF_EINVAL, "fnp must be 0, 1 or 2");
+      ctx->opt_fnp = (int)value;
+    }
     if (k == "kernels") {
       if (value < 1 || value > 6) return fail(ctx, MMF_EINVAL, "kernels must be 1 .. 6");
       ctx->opt_kernels = (int)value;

@@ -30,11 +30,31 @@ namespace mmf {
 // serial latency (~0.9 us, mostly issuing the item's ~12 TMA copies; measured with idle consumers) is what
 // limits a single pipeline.  An item's rows may wrap around its ring (consumers resolve the wrap per row),
 // so a ring needs only D + 1 slots.
-constexpr int FWD_NG = 1;
-constexpr int FWD_NP = 2;
-constexpr int FWD_PW = PIPE_NWC * FWD_NG + 1;  // warps per pipeline
-constexpr int FWD_THREADS = FWD_NP * FWD_PW * 32;
-constexpr int FWD_SD = 8;  // item descriptors per pipeline (power of two)
+constexpr int FWD_NP = 2;  // (pipelines per CTA of the backward's structure)
+constexpr int FWD_PW = PIPE_NWC + 1;  // warps per pipeline of the backward (8 consumers + producer)
+constexpr int FWD_SD = 8;             // item descriptors per pipeline of the backward (power of two)
+constexpr int FWD_SDF = 4;            // item descriptors per pipeline of the forward (power of two)
+constexpr int FWD_P = 8;              // record prefetch distance of the forward (items; PIPE_RP > FWD_P + FWD_SDF)
+static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the consumers until released");
+#ifndef MMF_FWD_OWNG
+#define MMF_FWD_OWNG 0  // 1: the node's own row beta_t[j] is loaded by the consumers from global memory (L2-
+                        // prefetched by the producer) instead of staged in the ring
+#endif
+// forward pipelines: NG consumer groups of GW warps (a group takes every NG-th item of its pipeline; a warp
+// owns 32 CPT commodities of the item, SW = 32 GW CPT) + one producer warp
+template <int GW, int NG, int NP> constexpr int fwd_threads() { return NP * (GW * NG + 1) * 32; }
+// compiled (SW, CPT, GW, NG, NP) combinations: NP pipelines per CTA, each NG groups of GW warps (a warp owns
+// CPT commodities per lane); the first of each SW is the default
+#define MMF_FWD_COMBOS(X)                                                                           \
+  X(1024, 4, 8, 1, 2) X(1024, 8, 4, 2, 2) X(1024, 8, 4, 3, 1) X(512, 2, 8, 1, 2) X(512, 4, 4, 2, 2) \
+  X(256, 4, 2, 4, 2)
+inline bool fwd_combo_ok(int SW, int gw, int ng, int np) {
+#define MMF_FWD_OK(sw, cpt, g, n, q) \
+  if (SW == sw && gw == g && ng == n && np == q) return true;
+  MMF_FWD_COMBOS(MMF_FWD_OK)
+#undef MMF_FWD_OK
+  return false;
+}
 
 struct __align__(16) FwdHdr {
   unsigned kb[32];  // rows (compacted, nonzero factor): K W significand bits
@@ -43,40 +63,47 @@ struct __align__(16) FwdHdr {
   int rowof[32];    // arcs (all in-arcs, q < na): row index or -1
   int aux[32];      //   ... arc id | bit 31 uncapacitated
   int rtail[32];    //   ... tail node
-  ArcOps ops[32];   //   ... dual-update operands (prefetched with the records)
-
   unsigned capmask; // bit q: row q's arc is capacitated
   int nr, na, start, end;
-  int pad[3];
+  int oslot;        // record-ring slot of the item (its dual-update operands, ArcOps, stay there until released)
+  int pad[2];
 };
 
 // per consumer group scratch: flow partials (row, warp), double-buffered by the group's item parity (a
 // warp may start the group's next item while another still reads this item's partials)
 struct FwdGrp {
   float fpart[2][32][PIPE_NWC];
+  // the update's results per arc (written by the group's warp 0 between the two barriers of an item)
+  float rq[2][32];
+  unsigned nkb[2][32], nk2[2][32];
+  int big[2];
+  int pad[2];
 };
+#ifndef MMF_FWD_DEDUP
+#define MMF_FWD_DEDUP 0  // 1: warp 0 alone evaluates the dual update (second barrier); 0: every warp does
+#endif
 
 struct PFwdSmem {
   size_t off_full, off_empty, off_ring, off_oring, off_hdr, off_grp, off_sig, off_exp, total;
 };
 
-__host__ __device__ inline PFwdSmem pfwd_smem(int R, int D, int SW) {
+__host__ __device__ inline PFwdSmem pfwd_smem(int R, int D, int SW, int NG) {
   PFwdSmem m;
   size_t o = 0;
   m.off_full = o;
-  o += 8 * (size_t)FWD_SD;
+  o += 8 * (size_t)FWD_SDF;
   m.off_empty = o;
-  o += 8 * (size_t)FWD_SD;
+  o += 8 * (size_t)FWD_SDF;
   o = (o + 15) / 16 * 16;
   m.off_ring = o;
   o += (size_t)PIPE_RP * D * 16;
   m.off_oring = o;
   o += (size_t)PIPE_RP * D * 32;
   m.off_hdr = o;
-  o += (size_t)FWD_SD * sizeof(FwdHdr);
+  o += (size_t)FWD_SDF * sizeof(FwdHdr);
   o = (o + 15) / 16 * 16;
   m.off_grp = o;
-  o += (size_t)FWD_NG * sizeof(FwdGrp);
+  o += (size_t)NG * sizeof(FwdGrp);
   o = (o + 127) / 128 * 128;
   m.off_sig = o;
   o += (size_t)R * SW * 4;
@@ -86,6 +113,9 @@ __host__ __device__ inline PFwdSmem pfwd_smem(int R, int D, int SW) {
   return m;
 }
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void* g, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
 }
@@ -115,6 +145,25 @@ __device__ __forceinline__ float bfly8(const float* v, int lane) {
     w[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
   }
   float r = (b2 ? w[1] : w[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w[0] : w[1], 4);
+  r += __shfl_xor_sync(0xffffffffu, r, 2);
+  r += __shfl_xor_sync(0xffffffffu, r, 1);
+  return r;
+}
+
+// the same for up to 4 values (2 + 1 + 1 + 1 + 1 shuffles); total of value q in the lanes with (lane & 7) == 0
+// and bfly_row4(lane) == q
+__device__ __forceinline__ int bfly_row4(int lane) { return ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1); }
+__device__ __forceinline__ float bfly4(const float* v, int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8;
+  float u[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b4 ? v[i] : v[i + 2];
+    const float keep = b4 ? v[i + 2] : v[i];
+    u[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float r = (b3 ? u[1] : u[0]) + __shfl_xor_sync(0xffffffffu, b3 ? u[0] : u[1], 8);
+  r += __shfl_xor_sync(0xffffffffu, r, 4);
   r += __shfl_xor_sync(0xffffffffu, r, 2);
   r += __shfl_xor_sync(0xffffffffu, r, 1);
   return r;
@@ -174,10 +223,10 @@ struct FwdOps {
   float d, wm, Km;
   int we, Ke, eopos, copos;
 };
-__device__ __forceinline__ FwdOps fwd_ops(const DevPtrs& p, const FwdHdr& h, int t, int lane) {
+__device__ __forceinline__ FwdOps fwd_ops(const ArcOps* hops, const FwdHdr& h, int lane) {
   FwdOps o{0.f, 1.f, 0.f, 0, 0, 0, 0};
   if (lane < h.na) {
-    const ArcOps a = h.ops[lane];
+    const ArcOps a = hops[lane];
     o.d = a.d;
     o.wm = a.wm;
     o.we = a.we;
@@ -188,6 +237,7 @@ __device__ __forceinline__ FwdOps fwd_ops(const DevPtrs& p, const FwdHdr& h, int
   }
   return o;
 }
+template <int GW>
 __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, const FwdOps& o,
                                              const float (*fp)[PIPE_NWC], int t, int j, int D, int lane, bool writer,
                                              bool* big_out) {
@@ -207,7 +257,7 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
       float s = 0.f;
       if (row >= 0)
 #pragma unroll
-        for (int w = 0; w < PIPE_NWC; ++w) s += fp[row][w];
+        for (int w = 0; w < GW; ++w) s += fp[row][w];
       const float d = o.d, w0 = o.wm;
       const int e0 = o.we;
       float wm;
@@ -275,16 +325,68 @@ struct RingRows {
     return (r >= R ? r - R : r) * SW + col;
   }
 };
+// the same with the item's base offset and wrap point precomputed (rows q < qw do not wrap)
+struct RingRowsF {
+  const float* sig;
+  const int16_t* sex;
+  int base, qw, RSW, SW;
+  __device__ __forceinline__ RingRowsF(const RingRows& r)
+      : sig(r.sig), sex(r.sex), base(r.start * r.SW + r.col), qw(r.R - r.start), RSW(r.R * r.SW), SW(r.SW) {}
+  __device__ __forceinline__ int off(int q) const { return base + q * SW - (q >= qw ? RSW : 0); }
+};
 
-// alpha from the new factors (gathered from the arcs' lanes), two passes over shared memory
-template <int CPT>
-__device__ __forceinline__ void fwd_alpha_new(const RingRows& rw, const FwdHdr& h, const FwdUpd& u, int nr, int lane,
-                                              float* s, int* Ex) {
+// the dual update's per-arc results as every warp of the group sees them: from the group's shared scratch
+// (MMF_FWD_DEDUP: written by warp 0) or from the arcs' lanes (every warp evaluated the update)
+struct UpdView {
+  const float* rq_;
+  const unsigned *kb_, *k2_;
+  FwdUpd u;
+  __device__ __forceinline__ float rq(int src) const {
+    return MMF_FWD_DEDUP ? rq_[src] : __shfl_sync(0xffffffffu, u.rq, src);
+  }
+  __device__ __forceinline__ unsigned kb(int src) const {
+    return MMF_FWD_DEDUP ? kb_[src] : __shfl_sync(0xffffffffu, u.nkb, src);
+  }
+  __device__ __forceinline__ unsigned k2(int src) const {
+    return MMF_FWD_DEDUP ? k2_[src] : __shfl_sync(0xffffffffu, u.nk2, src);
+  }
+};
+// the update phase of an item (after the flow partials are in fp and the group's barrier has passed)
+template <int GW>
+__device__ __forceinline__ UpdView fwd_update_phase(const DevPtrs& p, const FwdHdr& h, const FwdOps& o0,
+                                                    const ArcOps* hops, FwdGrp& G, int par, int t, int j, int D,
+                                                    int lane, int wg, int bar_id, bool* big) {
+  UpdView v;
+#if MMF_FWD_DEDUP
+  if (wg == 0) {
+    const FwdOps o = fwd_ops(hops, h, lane);
+    bool b;
+    const FwdUpd u = fwd_update<GW>(p, h, o, G.fpart[par], t, j, D, lane, true, &b);
+    G.rq[par][lane] = u.rq;
+    G.nkb[par][lane] = u.nkb;
+    G.nk2[par][lane] = u.nk2;
+    if (lane == 0) G.big[par] = b;
+  }
+  named_bar(bar_id, GW * 32);
+  v.rq_ = G.rq[par];
+  v.kb_ = G.nkb[par];
+  v.k2_ = G.nk2[par];
+  *big = G.big[par] != 0;
+#else
+  v.u = fwd_update<GW>(p, h, o0, G.fpart[par], t, j, D, lane, wg == 0, big);
+#endif
+  return v;
+}
+
+// alpha from the new factors, two passes over shared memory
+template <int CPT, class RW>
+__device__ __forceinline__ void fwd_alpha_new(const RW& rw, const FwdHdr& h, const UpdView& u, int nr, float* s,
+                                              int* Ex) {
   unsigned E2[CPT];
   xmax_init<CPT>(E2);
   for (int q = 0; q < nr; ++q) {
     const int src = h.rarc[q];
-    const unsigned kb = __shfl_sync(0xffffffffu, u.nkb, src), k2 = __shfl_sync(0xffffffffu, u.nk2, src);
+    const unsigned kb = u.kb(src), k2 = u.k2(src);
     if (!(__uint_as_float(kb) > 0.f)) continue;
     Row<TrF32, CPT> x;
     x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
@@ -299,7 +401,7 @@ __device__ __forceinline__ void fwd_alpha_new(const RingRows& rw, const FwdHdr& 
   }
   for (int q = 0; q < nr; ++q) {
     const int src = h.rarc[q];
-    const unsigned kb = __shfl_sync(0xffffffffu, u.nkb, src), k2 = __shfl_sync(0xffffffffu, u.nk2, src);
+    const unsigned kb = u.kb(src), k2 = u.k2(src);
     if (!(__uint_as_float(kb) > 0.f)) continue;
     Row<TrF32, CPT> x;
     x.load(rw.sig + rw.off(q), rw.sex + rw.off(q));
@@ -307,47 +409,98 @@ __device__ __forceinline__ void fwd_alpha_new(const RingRows& rw, const FwdHdr& 
   }
 }
 
-template <int CPT, int N>
-__device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw, const FwdHdr& h,
-                                         float (*fp)[PIPE_NWC], int t, int j, int D, int lane, int wg, int bar_id,
-                                         float* s, int* Ex) {
+// a lane's CPT significands / packed exponent words of a shared-memory row
+template <int CPT> __device__ __forceinline__ void load_sig(const float* pm, float* m) {
+  typedef typename VecM<float, CPT>::T VM;
+  const VM vm = *reinterpret_cast<const VM*>(pm);
+  const float* sm = reinterpret_cast<const float*>(&vm);
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) m[c] = sm[c];
+}
+template <int CPT> __device__ __forceinline__ void load_exps(const int16_t* pe, int* w) {
+  typedef typename VecE<int16_t, CPT>::T VE;
+  const VE ve = *reinterpret_cast<const VE*>(pe);
+  const int* sw = reinterpret_cast<const int*>(&ve);
+#pragma unroll
+  for (int k = 0; k < CPT / 2; ++k) w[k] = sw[k];
+}
+// in place: m[c] <- m[c] K W 2^(e[c] + ke - E[c]) (xterms on separately loaded words)
+template <int CPT>
+__device__ __forceinline__ void xterms_w(const int* w, float* m, unsigned kb, unsigned k2, const XPre<CPT>& P) {
+#pragma unroll
+  for (int k = 0; k < CPT / 2; ++k) {
+    const unsigned u = __viaddmax_s16x2((unsigned)w[k], k2, P.Lo2[k]);
+    const unsigned d2 = __viaddmax_s16x2(u, P.nE2[k], 0xff82ff82u);
+    m[2 * k] *= __uint_as_float(kb + (d2 << 23));
+    m[2 * k + 1] *= __uint_as_float(kb + ((d2 & 0xffff0000u) << 7));
+  }
+}
+
+// register path, N (compile-time) rows held in registers: the maximum exponent, the terms in place
+template <int CPT, int GW, int N>
+__device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, const FwdHdr& h, const ArcOps* hops,
+                                         const Row<TrF32, CPT>& bown, FwdGrp& G, int par, int t, int j, int D,
+                                         int lane, int wg, int bar_id, float* s, int* Ex) {
   typedef Row<TrF32, CPT> R_;
-  const FwdOps o = fwd_ops(p, h, t, lane);
-  R_ b;
-  b.load(rw.sig + rw.off(N), rw.sex + rw.off(N));  // own row beta_t[j]
-  float tq[N > 0 ? N : 1][CPT];
+  constexpr int NQ = N > 0 ? N : 1;
+  const RingRowsF rw(rw0);
+  const FwdOps o0 = MMF_FWD_DEDUP ? FwdOps{} : fwd_ops(hops, h, lane);
+  float tq[NQ][CPT];
   XPre<CPT> P;
   {
-    R_ x[N > 0 ? N : 1];
+    int xw[NQ][CPT / 2];
 #pragma unroll
-    for (int q = 0; q < N; ++q) x[q].load(rw.sig + rw.off(q), rw.sex + rw.off(q));
-    unsigned E2[CPT];
+    for (int q = 0; q < N; ++q) {
+      const int o = rw.off(q);
+      load_exps<CPT>(rw.sex + o, xw[q]);
+      load_sig<CPT>(rw.sig + o, tq[q]);
+    }
+    unsigned E2[CPT / 2];
     xmax_init<CPT>(E2);
 #pragma unroll
-    for (int q = 0; q < N; ++q) xmax_add<CPT>(E2, x[q], h.k2[q], k2_to_ke(h.k2[q]));
+    for (int q = 0; q < N; ++q) {
+      const unsigned k2 = h.k2[q];
+#pragma unroll
+      for (int k = 0; k < CPT / 2; ++k) E2[k] = __viaddmax_s16x2((unsigned)xw[q][k], k2, E2[k]);
+    }
     P.set(E2);
 #pragma unroll
-    for (int q = 0; q < N; ++q) xterms<CPT>(x[q], h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, tq[q]);
+    for (int q = 0; q < N; ++q) xterms_w<CPT>(xw[q], tq[q], h.kb[q], h.k2[q], P);
   }
   float bl[CPT];
-  beta_lin<CPT>(b, P, bl);
+  if constexpr (MMF_FWD_OWNG) {
+    beta_lin<CPT>(bown, P, bl);
+  } else {
+    R_ b;
+    const int o = rw.off(N);
+    b.load(rw.sig + o, rw.sex + o);  // own row beta_t[j]
+    beta_lin<CPT>(b, P, bl);
+  }
   const unsigned cap = h.capmask;
+  float (*fp)[PIPE_NWC] = G.fpart[par];
   if (N > 0 && cap != 0u) {
-    float f[8];
+    constexpr int NF = N <= 4 ? 4 : 8;
+    float f[NF];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < NF; ++q) {
       f[q] = 0.f;
       if (q < N)
 #pragma unroll
         for (int c = 0; c < CPT; ++c) f[q] = fmaf(tq[q < N ? q : 0][c], bl[c], f[q]);
     }
-    const float r = bfly8(f, lane);
-    const int row = bfly_row(lane);
-    if ((lane & 3) == 0 && row < N && ((cap >> row) & 1u)) fp[row][wg] = r;
+    if constexpr (NF == 4) {
+      const float r = bfly4(f, lane);
+      const int row = bfly_row4(lane);
+      if ((lane & 7) == 0 && row < N && ((cap >> row) & 1u)) fp[row][wg] = r;
+    } else {
+      const float r = bfly8(f, lane);
+      const int row = bfly_row(lane);
+      if ((lane & 3) == 0 && row < N && ((cap >> row) & 1u)) fp[row][wg] = r;
+    }
   }
-  named_bar(bar_id, PIPE_NWC * 32);
+  named_bar(bar_id, GW * 32);
   bool big;
-  const FwdUpd u = fwd_update(p, h, o, fp, t, j, D, lane, wg == 0, &big);
+  const UpdView u = fwd_update_phase<GW>(p, h, o0, hops, G, par, t, j, D, lane, wg, bar_id, &big);
   if (!big) {
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -356,24 +509,23 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw, c
     }
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      const float r = __shfl_sync(0xffffffffu, u.rq, h.rarc[q]);
+      const float r = u.rq(h.rarc[q]);
 #pragma unroll
       for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
     }
   } else {  // large ratios: recompute from shared memory with the new factors
-    fwd_alpha_new<CPT>(rw, h, u, N, lane, s, Ex);
+    fwd_alpha_new<CPT>(rw, h, u, N, s, Ex);
   }
 }
 
-// any row count (more than 8 rows): streaming flows, then the update, then alpha from shared memory
-template <int CPT>
-__device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& rw, const FwdHdr& h,
-                                             float (*fp)[PIPE_NWC], int t, int j, int D, int lane, int wg, int bar_id,
-                                             int nr, float* s, int* Ex) {
+// any row count (more than the register path's): streaming flows, then the update, then alpha from shared
+// memory
+template <int CPT, int GW>
+__device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& rw, const FwdHdr& h, const ArcOps* hops,
+                                             const Row<TrF32, CPT>& bown, FwdGrp& G, int par, int t, int j, int D,
+                                             int lane, int wg, int bar_id, int nr, float* s, int* Ex) {
   typedef Row<TrF32, CPT> R_;
-  const FwdOps o = fwd_ops(p, h, t, lane);
-  R_ b;
-  b.load(rw.sig + rw.off(nr), rw.sex + rw.off(nr));
+  const FwdOps o0 = MMF_FWD_DEDUP ? FwdOps{} : fwd_ops(hops, h, lane);
   unsigned E2[CPT];
   xmax_init<CPT>(E2);
   for (int q = 0; q < nr; ++q) {
@@ -384,7 +536,14 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& r
   XPre<CPT> P;
   P.set(E2);
   float bl[CPT];
-  beta_lin<CPT>(b, P, bl);
+  if constexpr (MMF_FWD_OWNG) {
+    beta_lin<CPT>(bown, P, bl);
+  } else {
+    R_ b;
+    b.load(rw.sig + rw.off(nr), rw.sex + rw.off(nr));
+    beta_lin<CPT>(b, P, bl);
+  }
+  float (*fp)[PIPE_NWC] = G.fpart[par];
   for (int q = 0; q < nr; ++q) {
     if (!((h.capmask >> q) & 1u)) continue;
     R_ x;
@@ -397,22 +556,24 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& r
     f = warp_sum<float>(f);
     if (lane == 0) fp[q][wg] = f;
   }
-  named_bar(bar_id, PIPE_NWC * 32);
+  named_bar(bar_id, GW * 32);
   bool big;
-  const FwdUpd u = fwd_update(p, h, o, fp, t, j, D, lane, wg == 0, &big);
-  fwd_alpha_new<CPT>(rw, h, u, nr, lane, s, Ex);
+  const UpdView u = fwd_update_phase<GW>(p, h, o0, hops, G, par, t, j, D, lane, wg, bar_id, &big);
+  fwd_alpha_new<CPT>(rw, h, u, nr, s, Ex);
 }
 
-template <int CPT, int MODE>
-__global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5 pc, int t) {
+template <int CPT, int GW, int NG, int NP, int MODE>
+__global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPtrs p, PipeCfg5 pc, int t) {
   typedef float M;
   typedef int16_t E;
-  constexpr int SW = pipe_sw<CPT>();
+  constexpr int SW = 32 * GW * CPT;
+  constexpr int PW = GW * NG + 1;                             // warps per pipeline
+  constexpr int NMAX = CPT >= 8 && fwd_threads<GW, NG, NP>() > 448 ? 6 : 8;  // register path up to NMAX rows
   extern __shared__ __align__(16) unsigned char smem_all[];
-  const PFwdSmem L = pfwd_smem(pc.R, pc.D, SW);
-  const int pl = (threadIdx.x >> 5) / FWD_PW;                 // pipeline of this warp
+  const PFwdSmem L = pfwd_smem(pc.R, pc.D, SW, NG);
+  const int pl = (threadIdx.x >> 5) / PW;                     // pipeline of this warp
   unsigned char* smem = smem_all + (size_t)pl * L.total;      // its share of the shared memory
-  const int jstep = FWD_NP * gridDim.x, j0 = blockIdx.x + pl * gridDim.x;
+  const int jstep = NP * gridDim.x, j0 = blockIdx.x + pl * gridDim.x;
   unsigned long long* full = (unsigned long long*)(smem + L.off_full);
   unsigned long long* empty = (unsigned long long*)(smem + L.off_empty);
   ArcKW<M>* ring = (ArcKW<M>*)(smem + L.off_ring);
@@ -421,19 +582,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
   FwdGrp* grps = (FwdGrp*)(smem + L.off_grp);
   M* sig = (M*)(smem + L.off_sig);
   E* sex = (E*)(smem + L.off_exp);
-  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) % FWD_PW;  // (warp within the pipeline)
+  const int lane = threadIdx.x & 31, warp = (threadIdx.x >> 5) % PW;  // (warp within the pipeline)
   const int D = pc.D, R = pc.R;
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < FWD_SD; ++s) {
+    for (int s = 0; s < FWD_SDF; ++s) {
       mbar_init(&full[s], 1);          // expect_tx arrive (all rows land by TMA)
-      mbar_init(&empty[s], PIPE_NWC);  // one consumer group per item
+      mbar_init(&empty[s], GW);        // one consumer group per item
     }
     mbar_fence_init();
   }
   __syncthreads();
   View<TrF32> v(p);
 
-  if (warp == PIPE_NWC * FWD_NG) {  // ---------------- producer
+  if (warp == GW * NG) {  // ---------------- producer
     const ArcKW<M>* ell = (const ArcKW<M>*)p.ell_in + (size_t)(t - 1) * p.N * D;
     const M* gm = v.am(t - 1);
     const E* ge = v.ae(t - 1);
@@ -452,33 +613,35 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
         cp_async16(&oring[pslot * D + lane], go);
         cp_async16((char*)&oring[pslot * D + lane] + 16, (const char*)go + 16);
       }
+      if (MMF_FWD_OWNG && pnode < p.N && lane >= 30) {  // the item's own row beta_t[j] -> L2 (read at its start)
+        const size_t g = (size_t)pnode * p.Lp;
+        if (lane == 30) bulk_prefetch_l2(bm + g, SW * 4);
+        else bulk_prefetch_l2(be + g, SW * 2);
+      }
       cp_async_commit();
       pnode += jstep;
       pslot = pslot + 1 == PIPE_RP ? 0 : pslot + 1;
     };
 #pragma unroll 1
-    for (int k = 0; k < PIPE_P; ++k) prefetch();
+    for (int k = 0; k < FWD_P; ++k) prefetch();
     RowRing rr;
     auto release = [&]() {
-      const int ds = rr.kold & (FWD_SD - 1);
-      mbar_wait(&empty[ds], (rr.kold / FWD_SD) & 1);
+      const int ds = rr.kold & (FWD_SDF - 1);
+      mbar_wait(&empty[ds], (rr.kold / FWD_SDF) & 1);
       rr.tail = (unsigned)hdr[ds].end;
       ++rr.kold;
     };
     int k = 0, cslot = 0;
     for (int j = j0; j < p.N; j += jstep, ++k) {
-      cp_async_wait<PIPE_P - 1>();
+      cp_async_wait<FWD_P - 1>();
       __syncwarp();
       ArcKW<M> r;
       r.node = -1;
       r.km = M(0);
       r.ke = 0;
       r.aux = 0;
-      ArcOps ro;
-      if (lane < D) {
-        r = ring[cslot * D + lane];
-        ro = oring[cslot * D + lane];
-      }
+      if (lane < D) r = ring[cslot * D + lane];
+      const int oslot = cslot;
       cslot = cslot + 1 == PIPE_RP ? 0 : cslot + 1;
       __syncwarp();
       const bool valid = lane < D && r.node >= 0;
@@ -487,9 +650,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
       const unsigned obal = __ballot_sync(0xffffffffu, ok);
       const unsigned cbal = __ballot_sync(0xffffffffu, ok && r.aux >= 0);
       const int na = __popc(vbal), nr = __popc(obal);
-      while (rr.kold <= k - FWD_SD) release();
-      while (rr.head + (unsigned)(nr + 1) - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D + 1)
-      const int ds = k & (FWD_SD - 1);
+      while (rr.kold <= k - FWD_SDF) release();
+      constexpr int OWN = MMF_FWD_OWNG ? 0 : 1;  // ring rows per item: nr (+ the own row)
+      while (rr.head + (unsigned)(nr + OWN) - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D + OWN)
+      const int ds = k & (FWD_SDF - 1);
       FwdHdr& h = hdr[ds];
       const int rs = __popc(obal & ((1u << lane) - 1u));
       if (ok) {
@@ -501,7 +665,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
         h.rowof[lane] = ok ? rs : -1;
         h.aux[lane] = r.aux;
         h.rtail[lane] = r.node;
-        h.ops[lane] = ro;
       }
       if (lane == 0) {
         // capmask over rows (row order = lane order of the nonzero-factor arcs)
@@ -515,10 +678,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
         h.nr = nr;
         h.na = na;
         h.start = rr.rpos;
-        h.end = (int)(rr.head + (unsigned)(nr + 1));
+        h.end = (int)(rr.head + (unsigned)(nr + OWN));
+        h.oslot = oslot;
       }
       __syncwarp();  // (the header writes of every lane precede lane 0's releasing arrive)
-      if (lane == 0) mbar_arrive_expect_tx(&full[ds], (unsigned)(nr + 1) * (unsigned)SW * 6u);
+      if (lane == 0) mbar_arrive_expect_tx(&full[ds], (unsigned)(nr + OWN) * (unsigned)SW * 6u);
       __syncwarp();
       prefetch();
       if (ok) {
@@ -528,15 +692,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
         bulk_g2s(sig + q * SW, gm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, ge + g, SW * 2, &full[ds]);
       }
-      if (lane == 31) {  // the node's own beta_t row -> slot nr
+      if (!MMF_FWD_OWNG && lane == 31) {  // the node's own beta_t row -> slot nr
         const size_t g = (size_t)j * p.Lp;
         int q = rr.rpos + nr;
         if (q >= R) q -= R;
         bulk_g2s(sig + q * SW, bm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, be + g, SW * 2, &full[ds]);
       }
-      rr.head += (unsigned)(nr + 1);
-      rr.rpos += nr + 1;
+      rr.head += (unsigned)(nr + OWN);
+      rr.rpos += nr + OWN;
       if (rr.rpos >= R) rr.rpos -= R;
     }
     cp_async_wait<0>();
@@ -544,15 +708,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
   }
 
   // ---------------- consumers
-  const int grp = warp / PIPE_NWC, wg = warp % PIPE_NWC;
+  const int grp = warp / GW, wg = warp % GW;
   FwdGrp& G = grps[grp];
   const int col = wg * 32 * CPT + lane * CPT;
-  const int bar_id = 1 + pl;
+  const int bar_id = 1 + pl * NG + grp;
   int k = grp;
-  for (int j = j0; j < p.N; j += jstep, k += FWD_NG) {
-    const int ds = k & (FWD_SD - 1);
-    mbar_wait(&full[ds], (k / FWD_SD) & 1);
+  for (int j = j0 + grp * jstep; j < p.N; j += NG * jstep, k += NG) {
+    const int ds = k & (FWD_SDF - 1);
+    Row<TrF32, CPT> bown;  // own row beta_t[j] (global; its latency overlaps the wait and the row math)
+    if constexpr (MMF_FWD_OWNG) {
+      const size_t g = (size_t)j * p.Lp + col;
+      bown.load(v.bm(t) + g, v.be(t) + g);
+    }
+    mbar_wait(&full[ds], (k / FWD_SDF) & 1);
     const FwdHdr& h = hdr[ds];
+    const ArcOps* hops = oring + h.oslot * D;
     if (pc.dry) {  // diagnostics: delivery rate of the producer / TMA alone
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[ds]);
@@ -560,20 +730,26 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_fwd_pipe(DevPtrs p, PipeCfg5
     }
     const int nr = h.nr;
     const RingRows rw{sig, sex, h.start, R, col, SW};
-    float (*fp)[PIPE_NWC] = G.fpart[(k / FWD_NG) & 1];
+    const int par = (k / NG) & 1;
     M s[CPT];
     int Ex[CPT];
     switch (nr) {
-      case 0: fwd_body<CPT, 0>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 1: fwd_body<CPT, 1>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 2: fwd_body<CPT, 2>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 3: fwd_body<CPT, 3>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 4: fwd_body<CPT, 4>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 5: fwd_body<CPT, 5>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 6: fwd_body<CPT, 6>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 7: fwd_body<CPT, 7>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 8: fwd_body<CPT, 8>(p, rw, h, fp, t, j, D, lane, wg, bar_id, s, Ex); break;
-      default: fwd_body_any<CPT>(p, rw, h, fp, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
+      case 0: fwd_body<CPT, GW, 0>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 1: fwd_body<CPT, GW, 1>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 2: fwd_body<CPT, GW, 2>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 3: fwd_body<CPT, GW, 3>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 4: fwd_body<CPT, GW, 4>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 5: fwd_body<CPT, GW, 5>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 6: fwd_body<CPT, GW, 6>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 7:
+        if constexpr (NMAX >= 7) fwd_body<CPT, GW, 7>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex);
+        else fwd_body_any<CPT, GW>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex);
+        break;
+      case 8:
+        if constexpr (NMAX >= 8) fwd_body<CPT, GW, 8>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex);
+        else fwd_body_any<CPT, GW>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex);
+        break;
+      default: fwd_body_any<CPT, GW>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);

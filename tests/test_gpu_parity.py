@@ -204,6 +204,16 @@ def test_pipelined_kernels_L1024_grid(bwd):
     assert_parity(p, 3, "fp32", options=dict(bwd=bwd))
 
 
+@pytest.mark.parametrize("L,fgw,fng,fnp", [(1024, 8, 1, 2), (1024, 4, 2, 2), (1024, 4, 3, 1), (512, 8, 1, 2),
+                                           (512, 4, 2, 2), (256, 2, 4, 2)])
+def test_pipelined_forward_groups(L, fgw, fng, fnp):
+    """Every compiled consumer-group layout of the pipelined forward (fgw warps per group, fng groups per
+    pipeline, fnp pipelines per CTA; 32 * fgw * CPT = the slice width) against the live oracle, on a grid
+    whose in-degrees (2..5 plus the loop) exercise the register paths and a ragged commodity tail."""
+    p = grid_problem(12, 12, 8, L - 5 if L > 256 else L, 0.1, seed=31, cap=(0.5, 3.0))
+    assert_parity(p, 2, "fp32", options=dict(fgw=fgw, fng=fng, fnp=fnp))
+
+
 def _invariants(p, F, W, rtol):
     """Properties of the end-of-sweep readout that hold at any size: F >= 0, W in [0, 1],
     per-step mass = total commodity mass (the sink marginal is exact after a4, and point-mass sources carry
