@@ -116,7 +116,10 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "kernels"  kernel family 1..6 (default 6 = TMA-pipelined forward (2 pipelines / CTA) and
  *              backward (3 pipelines / CTA); 5 single-pipeline; 4 register head-flow; 3 wide-lane;
  *              2 smem node tiles; 1 per-node reference kernels)
- *   "bwd"      backward kernel with kernels >= 5: 0 auto, 1 three-pipeline, 2 sliding window, 3 single
+ *   "bwd"      backward kernel with kernels >= 5: 0 auto, 1 three-pipeline, 2 sliding window, 3 single,
+ *              4 row-reuse rings (contiguous node blocks, resident rows referenced instead of reloaded)
+ *   "fgw", "fng", "fnp"  pipelined forward: warps per consumer group (8, 4, 2), groups per pipeline,
+ *              pipelines per CTA (0 = default; the compiled combinations are listed in pipefwd.cuh)
  *   "wintma"   window backward row blocks by 2-D tensor TMA (1) or cp.async (0)
  *   "order"    node order (kernels >= 2): 0 input, 1 reverse Cuthill-McKee, 2 BFS tiles (default)
  *   "cpt"      commodities per thread 0 (auto), 1, 2, 4, 8

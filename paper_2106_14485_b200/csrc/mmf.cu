@@ -9,6 +9,7 @@
 #include "kernels.cuh"
 #include "tiled.cuh"
 #include "win.cuh"
+#include "reuse.cuh"
 
 #include <dlfcn.h>
 #include <cstdlib>
@@ -111,6 +112,8 @@ struct mmf_ctx {
                         // kernel), 1 = two-pipeline TMA kernel, 2 = window kernel, 3 = pipe (1 pipeline)
   PipeCfg5 pb2{};       // two-pipeline backward configuration
   bool pipe2_bwd = false;
+  bool ru_bwd = false;  // row-reuse backward (reuse.cuh)
+  PipeCfg5 pr{};
 
   // ---- derived
   int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
@@ -440,6 +443,22 @@ void derive_shapes(mmf_ctx* c) {
     }
   }
   if (c->opt_bwd == 3) c->win_bwd = false;
+  // row-reuse backward: contiguous node blocks per pipeline, resident rows referenced instead of reloaded
+  c->ru_bwd = false;
+  // (option only: measured slower than the three-pipeline kernel on [4] and [5])
+  if (c->pipe_bwd && c->pb.SW >= 512 && c->opt_bwd == 4 && c->pb.D < 32) {
+    const size_t budget = 226 * 1024 / RU_NP;
+    int R = 0;
+    while (ru_smem(R + 1, c->pb.D, c->pb.SW).total <= budget) ++R;
+    if (R >= c->pb.D) {
+      c->ru_bwd = true;
+      c->pr = c->pb;
+      c->pr.R = R;
+      c->pr.ns = c->Lp / c->pb.SW;
+      c->pr.nitems = c->N * c->pr.ns;
+      c->win_bwd = false;
+    }
+  }
   // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width), NG
   // consumer groups of GW warps per pipeline (a warp owns 32 CPT = SW / GW commodities)
   c->pipe_fwd = false;
@@ -539,6 +558,65 @@ std::vector<int> strip_newid(const std::vector<int>& rank, int b, int w) {
   std::vector<int> nid(N);
   for (int k = 0; k < N; ++k) nid[ord[k]] = k;
   return nid;
+}
+
+// ---- row-reuse node order (the pipelined kernels' default) ------------------------------------------
+// A pipeline walks consecutive nodes; a row gathered for one of the last few items is still resident in its
+// ring.  Score of an order = the fraction of gathered rows (in-lists: forward; out-lists: backward) whose
+// node was gathered within the previous RU_WIN items.  Candidates: input, reverse Cuthill-McKee, and strip
+// versions of both (strip_newid) of widths 2 .. 32.
+constexpr int RU_WIN = 3;
+double reuse_frac(const mmf_ctx* c, const std::vector<int>& nid, bool in_lists) {
+  const int N = c->N;
+  const size_t A = c->tail.size();
+  std::vector<int> ptr(N + 1, 0), lst(A);
+  for (size_t a = 0; a < A; ++a) ptr[nid[in_lists ? c->head[a] : c->tail[a]] + 1]++;
+  for (int v = 0; v < N; ++v) ptr[v + 1] += ptr[v];
+  std::vector<int> fill(ptr.begin(), ptr.end() - 1);
+  for (size_t a = 0; a < A; ++a) {
+    const int item = nid[in_lists ? c->head[a] : c->tail[a]];
+    lst[fill[item]++] = nid[in_lists ? c->tail[a] : c->head[a]];
+  }
+  std::vector<int> last(N, -(1 << 30));
+  size_t hit = 0;
+  for (int j = 0; j < N; ++j)
+    for (int q = ptr[j]; q < ptr[j + 1]; ++q) {
+      const int r = lst[q];
+      hit += j - last[r] <= RU_WIN;
+      last[r] = j;
+    }
+  return A ? (double)hit / (double)A : 0.0;
+}
+void choose_reuse_order(mmf_ctx* c) {
+  const int N = c->N;
+  const size_t A = c->tail.size();
+  std::vector<std::vector<int>> cands;
+  cands.emplace_back(N);
+  std::iota(cands[0].begin(), cands[0].end(), 0);
+  cands.push_back(rcm_newid(N, c->tail, c->head));
+  for (int base = 0; base < 2; ++base) {
+    std::vector<int> d;
+    for (size_t a = 0; a < A; ++a)
+      if (c->tail[a] != c->head[a]) d.push_back(std::abs(cands[base][c->tail[a]] - cands[base][c->head[a]]));
+    if (d.empty()) continue;
+    std::nth_element(d.begin(), d.begin() + (size_t)(0.90 * (d.size() - 1)), d.end());
+    const int b90 = d[(size_t)(0.90 * (d.size() - 1))];
+    for (int w : {2, 4, 8, 16, 32})
+      if (b90 > 2 * w) cands.push_back(strip_newid(cands[base], b90, w));
+  }
+  double best = -1.0;
+  size_t bi = 0;
+  for (size_t ci = 0; ci < cands.size(); ++ci) {
+    const double f = reuse_frac(c, cands[ci], true) + reuse_frac(c, cands[ci], false);
+    if (getenv("MMF_VERBOSE")) fprintf(stderr, "[mmf] reuse order cand %zu: %.3f\n", ci, 0.5 * f);
+    if (f > best + 1e-9) {
+      best = f;
+      bi = ci;
+    }
+  }
+  c->newid = cands[bi];
+  c->win_Wb = 0;
+  c->win_cpt = 4;
 }
 
 size_t win_bwd_smem(int cpt, int Wb, int farmax, int maxrec, int segB) {
@@ -706,7 +784,8 @@ void prepare(mmf_ctx* c) {
   std::vector<int> order;
   const int B = c->opt_kernels >= 2 ? c->opt_tile : std::max(N, 1);
   if (c->opt_kernels == 6 && c->opt_reorder) {
-    choose_window_order(c);
+    if (c->opt_bwd == 4) choose_reuse_order(c);  // (row-reuse backward: neighbour overlap of consecutive nodes)
+    else choose_window_order(c);
     c->h_tile_ptr.assign(1, 0);
     for (int v = B; v < N; v += B) c->h_tile_ptr.push_back(v);
     c->h_tile_ptr.push_back(N);
@@ -1199,6 +1278,14 @@ template <class T_> struct Eng {
           k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
         return;
       }
+      if (c->ru_bwd) {
+        const PipeCfg5& pc = c->pr;
+        const unsigned grid = (unsigned)std::min((c->N + RU_NP - 1) / RU_NP, c->sms);
+        const size_t sm = RU_NP * ru_smem(pc.R, pc.D, pc.SW).total;
+        if (pc.SW == 1024) k_bwd_reuse<4><<<grid, RU_THREADS, sm, s>>>(c->dp, pc, t);
+        else k_bwd_reuse<2><<<grid, RU_THREADS, sm, s>>>(c->dp, pc, t);
+        return;
+      }
       if (c->pipe2_bwd) {
         const int cp = c->pb2.SW / 256;
         if (cp == 4) pipe2_bwd_cpt<4>(c, s, t);
@@ -1311,6 +1398,12 @@ template <class T_> struct Eng {
           fprintf(stderr, "[mmf] window bwd: cpt %d Wb %d RBa %d ns %d nseg %d segB %d farmax %d maxrec %d smem %zu\n",
                   c->win_cpt, c->wcb.Wb, c->wcb.RBa, c->wcb.ns, c->wcb.nseg, c->wcb.segB, c->wcb.farmax,
                   c->wcb.maxrec, c->win_cpt == 4 ? win_smem<4>(c->wcb).total : c->win_cpt == 2 ? win_smem<2>(c->wcb).total : win_smem<1>(c->wcb).total);
+      }
+      if (c->ru_bwd) {
+        const int sm = RU_NP * (int)ru_smem(c->pr.R, c->pr.D, c->pr.SW).total;
+        CU(cudaFuncSetAttribute(k_bwd_reuse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_bwd_reuse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        if (getenv("MMF_VERBOSE")) fprintf(stderr, "[mmf] reuse bwd: SW %d R %d D %d smem %d\n", c->pr.SW, c->pr.R, c->pr.D, sm);
       }
       if (c->pipe2_bwd) {
         const int sm = BWD_NP * (int)((pipe_smem(c->pb2.R, FWD_SD, c->pb2.D, c->pb2.SW).total + 127) / 128 * 128);

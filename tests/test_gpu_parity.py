@@ -195,11 +195,11 @@ def test_config_parity_against_stored_oracle(name, k, prec):
     assert abs(sg["mass"] - float(z[f"mass_{k}"])) <= 10 * TOL[prec] * abs(float(z[f"mass_{k}"]))
 
 
-@pytest.mark.parametrize("bwd", [0, 1, 2, 3])
+@pytest.mark.parametrize("bwd", [0, 1, 2, 3, 4])
 def test_pipelined_kernels_L1024_grid(bwd):
     """L = 1024 (the bench's commodity count on [4]: one 1024-commodity slice per node, 4 commodities per
     lane in the pipelined forward and backward kernels) on a 20 x 20 grid, live oracle; every backward
-    variant (auto, two-pipeline TMA, sliding window, single-pipeline TMA)."""
+    variant (auto, three-pipeline TMA, sliding window, single-pipeline TMA, row-reuse rings)."""
     p = grid_problem(20, 20, 12, 1024, 0.1, seed=29, cap=(0.5, 3.0))
     assert_parity(p, 3, "fp32", options=dict(bwd=bwd))
 
