@@ -105,6 +105,7 @@ struct mmf_ctx {
   int opt_dry = 0;      // diagnostics: pipelined backward consumers skip the arithmetic
   int opt_copy = 0;     // pipelined kernels' row staging: 0 = TMA bulk copies, 1 = per-lane cp.async
   int opt_wintma = 1;   // window kernels: 1 = 2-D TMA row-block loads, 0 = per-thread cp.async
+  int opt_wrap = -1;    // k_bwd_pipe2 ring wrap: -1 auto, 0 items never wrap, 1 items may wrap
   int opt_fgw = 0;      // pipelined forward: warps per consumer group (0 auto, 8, 4, 2)
   int opt_fng = 0;      // pipelined forward: consumer groups per pipeline (0 auto, 1 .. 6)
   int opt_fnp = 0;      // pipelined forward: pipelines per CTA (0 auto, 1, 2)
@@ -440,6 +441,10 @@ void derive_shapes(mmf_ctx* c) {
       c->pb2.ns = c->Lp / c->pb.SW;
       c->pb2.nitems = c->N * c->pb2.ns;
       c->win_bwd = c->win_bwd && c->opt_bwd == 2;
+      // items that never wrap save per-row offset arithmetic but waste ring slots: worth it when items are
+      // long or the ring holds many of them (measured: [5], [3] gain; [4] loses)
+      const double avg = (double)c->A / std::max(c->N, 1);
+      c->pb2.wrap = c->opt_wrap >= 0 ? c->opt_wrap : !(avg >= 8.0 || R >= 3.0 * avg);
     }
   }
   if (c->opt_bwd == 3) c->win_bwd = false;
@@ -1767,7 +1772,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -1781,6 +1786,10 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     if (k == "fng") {
       if (value < 0 || value > 6) return fail(ctx, MMF_EINVAL, "fng must be in [0, 6]");
       ctx->opt_fng = (int)value;
+    }
+    if (k == "wrap") {
+      if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "wrap must be -1, 0 or 1");
+      ctx->opt_wrap = (int)value;
     }
     if (k == "fnp") {
       if (value < 0 || value > 2) return fail(ctx, MMF_EINVAL, "fnp must be 0, 1 or 2");

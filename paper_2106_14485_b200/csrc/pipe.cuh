@@ -41,6 +41,8 @@ struct PipeCfg5 {
   int nitems;  // N * ns
   int dry;     // diagnostics: consumers only wait and release (measures the producer / TMA delivery rate)
   int copy;    // row staging: 0 = cp.async.bulk (TMA, one per row plane), 1 = cp.async 16 B per lane (LDGSTS)
+  int wrap;    // k_bwd_pipe2: 1 = an item's rows may wrap around the ring (offsets computed per row), 0 = items
+               // never wrap (the producer skips to slot 0; compile-time row offsets, fewer ring slots usable)
 };
 
 // item descriptor: the n present rows (compacted, nonzero factor; ring slots start .. start + n - 1, never
@@ -128,10 +130,18 @@ struct ItemIt {
 // Exponents are handled two per 32-bit word (CPT even): the max of (row exponent + arc exponent) by one
 // VIADDMNMX.S16x2 per pair (exact: |e| <= 16384, |ke| <= 16000); the scale 2^d, d = max(max(e + ke,
 // E - 32512) - E, -126) (no 16-bit wrap) by two more; then K W 2^d by an integer add into the float's
-// exponent field — mod 2^32 the low / high half of d << 23 equals d2 << 23 / (d2 & 0xffff0000) << 7.
+// exponent field — mod 2^32 the low / high half of d << 23 equals d2 << 23 / (d2 >> 16) << 23 (SHF + LEA).
 
+#ifndef MMF_HI_SHF
+#define MMF_HI_SHF 1
+#endif
+#if MMF_HI_SHF
+#define MMF_HI23(d2) (((d2) >> 16) << 23)
+#else
+#define MMF_HI23(d2) (((d2)&0xffff0000u) << 7)
+#endif
 template <int CPT> struct XPre {  // per-item constants of a lane: -E and the low clamp E - 32512, packed
-  unsigned nE2[CPT / 2 > 0 ? CPT / 2 : 1], Lo2[CPT / 2 > 0 ? CPT / 2 : 1];
+  unsigned nE2[CPT / 2 > 0 ? CPT / 2 : 1], Lo2[CPT / 2 > 0 ? CPT / 2 : 1], Ep2[CPT / 2 > 0 ? CPT / 2 : 1];
   int nE[CPT];
   int E[CPT];
   __device__ __forceinline__ void set(const unsigned* E2) {
@@ -140,6 +150,7 @@ template <int CPT> struct XPre {  // per-item constants of a lane: -E and the lo
       for (int w = 0; w < CPT / 2; ++w) {
         nE2[w] = __vneg2(E2[w]);
         Lo2[w] = __vsubss2(E2[w], 0x7f007f00u);
+        Ep2[w] = __vaddss2(E2[w], 0x007f007fu);  // E + 127 (float exponent bias), saturated
         E[2 * w] = (int)(short)(E2[w] & 0xffffu);
         E[2 * w + 1] = (int)E2[w] >> 16;
       }
@@ -181,7 +192,7 @@ __device__ __forceinline__ void xterms(const Row<TrF32, CPT>& x, unsigned kb, un
       const unsigned u = __viaddmax_s16x2((unsigned)x.w[w], k2, P.Lo2[w]);
       const unsigned d2 = __viaddmax_s16x2(u, P.nE2[w], 0xff82ff82u);
       tq[2 * w] = x.m[2 * w] * __uint_as_float(kb + (d2 << 23));
-      tq[2 * w + 1] = x.m[2 * w + 1] * __uint_as_float(kb + ((d2 & 0xffff0000u) << 7));
+      tq[2 * w + 1] = x.m[2 * w + 1] * __uint_as_float(kb + MMF_HI23(d2));
     }
   } else {
 #pragma unroll
@@ -200,7 +211,7 @@ __device__ __forceinline__ void xacc(const Row<TrF32, CPT>& x, unsigned kb, unsi
       const unsigned u = __viaddmax_s16x2((unsigned)x.w[w], k2, P.Lo2[w]);
       const unsigned d2 = __viaddmax_s16x2(u, P.nE2[w], 0xff82ff82u);
       acc[2 * w] = fmaf(x.m[2 * w], __uint_as_float(kb + (d2 << 23)), acc[2 * w]);
-      acc[2 * w + 1] = fmaf(x.m[2 * w + 1], __uint_as_float(kb + ((d2 & 0xffff0000u) << 7)), acc[2 * w + 1]);
+      acc[2 * w + 1] = fmaf(x.m[2 * w + 1], __uint_as_float(kb + MMF_HI23(d2)), acc[2 * w + 1]);
     }
   } else {
 #pragma unroll
@@ -211,6 +222,51 @@ __device__ __forceinline__ void xacc(const Row<TrF32, CPT>& x, unsigned kb, unsi
   }
 }
 __device__ __forceinline__ int k2_to_ke(unsigned k2) { return (int)(short)(k2 & 0xffffu); }
+
+// normalise a lane's sums (s[c] * 2^Ex[c], s[c] = 0 or a normal float) into [1, 2) significands and int16
+// exponents two at a time, and store them (norm_lane's semantics: zero -> (0, EZERO); an exponent outside
+// [-ELIM, ELIM] is clamped and raises the sticky ERR_RANGE — checked once per lane)
+template <int CPT>
+__device__ __forceinline__ void norm_store_f32(const DevPtrs& p, const float* s, const int* Ex, float* pm,
+                                               int16_t* pe, int l0, int node) {
+  static_assert(CPT % 2 == 0, "packed exponents");
+  typedef typename VecM<float, CPT>::T VM;
+  typedef typename VecE<int16_t, CPT>::T VE;
+  VM vm;
+  VE ve;
+  float* m = reinterpret_cast<float*>(&vm);
+  unsigned* e2 = reinterpret_cast<unsigned*>(&ve);
+  unsigned hi = 0x80008000u, lo = 0x7fff7fffu;
+#pragma unroll
+  for (int w = 0; w < CPT / 2; ++w) {
+    const unsigned u0 = __float_as_uint(s[2 * w]), u1 = __float_as_uint(s[2 * w + 1]);
+    const unsigned E2 = __byte_perm((unsigned)Ex[2 * w], (unsigned)Ex[2 * w + 1], 0x5410);
+    const unsigned f2 = (u0 >> 23) | ((u1 >> 7) & 0x00ff0000u);  // float exponent fields (0: the sum is 0)
+    const unsigned z2 = __vcmpeq2(f2, 0u);
+    const unsigned er = __vsub2(__vadd2(E2, f2), 0x007f007fu);
+    e2[w] = (er & ~z2) | (0xc000c000u & z2);  // (EZERO = -16384)
+    const unsigned enz = er & ~z2;
+    hi = __vmaxs2(hi, enz);
+    lo = __vmins2(lo, enz);
+    m[2 * w] = u0 ? __uint_as_float((u0 & 0x007fffffu) | 0x3f800000u) : 0.f;
+    m[2 * w + 1] = u1 ? __uint_as_float((u1 & 0x007fffffu) | 0x3f800000u) : 0.f;
+  }
+  const int emax = max((int)(short)(hi & 0xffffu), (int)hi >> 16);
+  const int emin = min((int)(short)(lo & 0xffffu), (int)lo >> 16);
+  if (emax > ELIM || emin < -ELIM) {  // (rare) clamp and report, element by element
+    int16_t* es = reinterpret_cast<int16_t*>(&ve);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int e = es[c];
+      if (m[c] != 0.f && (e > ELIM || e < -ELIM)) {
+        set_error(p, ERR_RANGE, l0 + c, node);
+        es[c] = (int16_t)(e > 0 ? ELIM : -ELIM);
+      }
+    }
+  }
+  *reinterpret_cast<VM*>(pm) = vm;
+  *reinterpret_cast<VE*>(pe) = ve;
+}
 
 // sum over N (compile-time) contiguous rows sg + q * SW of an item: (s, E) per commodity
 template <int CPT, int N>

@@ -36,6 +36,12 @@ constexpr int FWD_SD = 8;             // item descriptors per pipeline of the ba
 constexpr int FWD_SDF = 4;            // item descriptors per pipeline of the forward (power of two)
 constexpr int FWD_P = 8;              // record prefetch distance of the forward (items; PIPE_RP > FWD_P + FWD_SDF)
 static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the consumers until released");
+#ifndef MMF_NORM_PACKED
+#define MMF_NORM_PACKED 0  // packed normalise-and-store of the pipelined kernels' output rows (measured: no gain)
+#endif
+#ifndef MMF_BWD_NOWRAP_PATH
+#define MMF_BWD_NOWRAP_PATH 1  // compile the backward's never-wrapping item path
+#endif
 #ifndef MMF_FWD_OWNG
 #define MMF_FWD_OWNG 0  // 1: the node's own row beta_t[j] is loaded by the consumers from global memory (L2-
                         // prefetched by the producer) instead of staged in the ring
@@ -307,10 +313,19 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
 // by the mass: the exponent is clamped to the normal range)
 template <int CPT>
 __device__ __forceinline__ void beta_lin(const Row<TrF32, CPT>& b, const XPre<CPT>& P, float* bl) {
+  if constexpr (CPT % 2 == 0) {  // two at a time: biased exponent e + E + 127 clamped to [0, 254] (0: flushed)
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const int es = b.e(c) + P.E[c];
-    bl[c] = (es < -126 || !(b.m[c] > 0.f)) ? 0.f : b.m[c] * __uint_as_float((unsigned)(min(es, 127) + 127) << 23);
+    for (int w = 0; w < CPT / 2; ++w) {
+      const unsigned es = __vmins2(__vmaxs2(__vaddss2((unsigned)b.w[w], P.Ep2[w]), 0u), 0x00fe00feu);
+      bl[2 * w] = b.m[2 * w] * __uint_as_float(es << 23);
+      bl[2 * w + 1] = b.m[2 * w + 1] * __uint_as_float((es >> 16) << 23);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const int es = b.e(c) + P.E[c];
+      bl[c] = (es < -126 || !(b.m[c] > 0.f)) ? 0.f : b.m[c] * __uint_as_float((unsigned)(min(es, 127) + 127) << 23);
+    }
   }
 }
 
@@ -325,14 +340,14 @@ struct RingRows {
     return (r >= R ? r - R : r) * SW + col;
   }
 };
-// the same with the item's base offset and wrap point precomputed (rows q < qw do not wrap)
-struct RingRowsF {
+// an item's rows are contiguous ring slots start .. start + n - 1 (the producers never wrap an item: they
+// skip to slot 0 instead), so row q is at a compile-time offset from the item's base
+template <int SW> struct RingRowsF {
   const float* sig;
   const int16_t* sex;
-  int base, qw, RSW, SW;
   __device__ __forceinline__ RingRowsF(const RingRows& r)
-      : sig(r.sig), sex(r.sex), base(r.start * r.SW + r.col), qw(r.R - r.start), RSW(r.R * r.SW), SW(r.SW) {}
-  __device__ __forceinline__ int off(int q) const { return base + q * SW - (q >= qw ? RSW : 0); }
+      : sig(r.sig + r.start * SW + r.col), sex(r.sex + r.start * SW + r.col) {}
+  __device__ __forceinline__ int off(int q) const { return q * SW; }
 };
 
 // the dual update's per-arc results as every warp of the group sees them: from the group's shared scratch
@@ -432,7 +447,7 @@ __device__ __forceinline__ void xterms_w(const int* w, float* m, unsigned kb, un
     const unsigned u = __viaddmax_s16x2((unsigned)w[k], k2, P.Lo2[k]);
     const unsigned d2 = __viaddmax_s16x2(u, P.nE2[k], 0xff82ff82u);
     m[2 * k] *= __uint_as_float(kb + (d2 << 23));
-    m[2 * k + 1] *= __uint_as_float(kb + ((d2 & 0xffff0000u) << 7));
+    m[2 * k + 1] *= __uint_as_float(kb + MMF_HI23(d2));
   }
 }
 
@@ -443,7 +458,7 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
                                          int lane, int wg, int bar_id, float* s, int* Ex) {
   typedef Row<TrF32, CPT> R_;
   constexpr int NQ = N > 0 ? N : 1;
-  const RingRowsF rw(rw0);
+  const RingRowsF<32 * GW * CPT> rw(rw0);
   const FwdOps o0 = MMF_FWD_DEDUP ? FwdOps{} : fwd_ops(hops, h, lane);
   float tq[NQ][CPT];
   XPre<CPT> P;
@@ -521,9 +536,10 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
 // any row count (more than the register path's): streaming flows, then the update, then alpha from shared
 // memory
 template <int CPT, int GW>
-__device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& rw, const FwdHdr& h, const ArcOps* hops,
+__device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& rw0, const FwdHdr& h, const ArcOps* hops,
                                              const Row<TrF32, CPT>& bown, FwdGrp& G, int par, int t, int j, int D,
                                              int lane, int wg, int bar_id, int nr, float* s, int* Ex) {
+  const RingRowsF<32 * GW * CPT> rw(rw0);
   typedef Row<TrF32, CPT> R_;
   const FwdOps o0 = MMF_FWD_DEDUP ? FwdOps{} : fwd_ops(hops, h, lane);
   unsigned E2[CPT];
@@ -652,7 +668,14 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
       const int na = __popc(vbal), nr = __popc(obal);
       while (rr.kold <= k - FWD_SDF) release();
       constexpr int OWN = MMF_FWD_OWNG ? 0 : 1;  // ring rows per item: nr (+ the own row)
-      while (rr.head + (unsigned)(nr + OWN) - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D + OWN)
+      const int nrow = nr + OWN;
+      {  // items never wrap: skip the ring's last rpos..R-1 slots (counted with this item) if it does not fit
+        unsigned pad = rr.rpos + nrow > R ? (unsigned)(R - rr.rpos) : 0u;
+        while (rr.head + pad + (unsigned)nrow - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D + OWN)
+        if (rr.head + pad + (unsigned)nrow - rr.tail > (unsigned)R) pad = 0u;  // (all released: start over at 0)
+        if (rr.rpos + nrow > R) rr.rpos = 0;
+        rr.head += pad;
+      }
       const int ds = k & (FWD_SDF - 1);
       FwdHdr& h = hdr[ds];
       const int rs = __popc(obal & ((1u << lane) - 1u));
@@ -678,7 +701,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
         h.nr = nr;
         h.na = na;
         h.start = rr.rpos;
-        h.end = (int)(rr.head + (unsigned)(nr + OWN));
+        h.end = (int)(rr.head + (unsigned)nrow);
         h.oslot = oslot;
       }
       __syncwarp();  // (the header writes of every lane precede lane 0's releasing arrive)
@@ -687,21 +710,19 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
       prefetch();
       if (ok) {
         const size_t g = (size_t)r.node * p.Lp;
-        int q = rr.rpos + rs;
-        if (q >= R) q -= R;
+        const int q = rr.rpos + rs;
         bulk_g2s(sig + q * SW, gm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, ge + g, SW * 2, &full[ds]);
       }
       if (!MMF_FWD_OWNG && lane == 31) {  // the node's own beta_t row -> slot nr
         const size_t g = (size_t)j * p.Lp;
-        int q = rr.rpos + nr;
-        if (q >= R) q -= R;
+        const int q = rr.rpos + nr;
         bulk_g2s(sig + q * SW, bm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, be + g, SW * 2, &full[ds]);
       }
-      rr.head += (unsigned)(nr + OWN);
-      rr.rpos += nr + OWN;
-      if (rr.rpos >= R) rr.rpos -= R;
+      rr.head += (unsigned)nrow;
+      rr.rpos += nrow;
+      if (rr.rpos >= R) rr.rpos = 0;
     }
     cp_async_wait<0>();
     return;
@@ -754,14 +775,20 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
     // s is 0 or a normal float (ratios are within 2^+-40 of the previous terms): bit-level normalisation
-    Lane<M, E, CPT> a;
-    norm_lane<TrF32, CPT>(p, s, Ex, a, col, j);
     const size_t g = (size_t)j * p.Lp + col;
-    a.store(v.am(t) + g, v.ae(t) + g);
-    if (MODE == 2) {  // a4: UT = muT ./ alpha_T -> beta_T
+    if constexpr (MODE == 2) {  // a4: UT = muT ./ alpha_T -> beta_T
+      Lane<M, E, CPT> a;
+      norm_lane<TrF32, CPT>(p, s, Ex, a, col, j);
+      a.store(v.am(t) + g, v.ae(t) + g);
       Lane<M, E, CPT> ut;
       boundary_lane<TrF32, CPT>(p, 1, j, col, g, a, ut);
       ut.store(v.bm(p.T) + g, v.be(p.T) + g);
+    } else if constexpr (MMF_NORM_PACKED) {
+      norm_store_f32<CPT>(p, s, Ex, v.am(t) + g, v.ae(t) + g, col, j);
+    } else {
+      Lane<M, E, CPT> a;
+      norm_lane<TrF32, CPT>(p, s, Ex, a, col, j);
+      a.store(v.am(t) + g, v.ae(t) + g);
     }
   }
 }
@@ -775,8 +802,8 @@ namespace mmf {
 //   beta_t[i, slice] = sum_{a: i_a = i} K_t W_t[a] beta_{t+1}[j_a, slice]   (eq:psi P:1038-1043)
 // items = (node, slice) pairs in grid-stride order, rows staged by TMA bulk copies into each pipeline's
 // ring (items may wrap), arc records prefetched with cp.async.
-template <int CPT, int N>
-__device__ __forceinline__ void ring_sum_n(const RingRows& rw, const PipeHdr& h, float* s, int* Ex) {
+template <int CPT, int N, class RW>
+__device__ __forceinline__ void ring_sum_n(const RW& rw, const PipeHdr& h, float* s, int* Ex) {
   Row<TrF32, CPT> x[N > 0 ? N : 1];
 #pragma unroll
   for (int q = 0; q < N; ++q) x[q].load(rw.sig + rw.off(q), rw.sex + rw.off(q));
@@ -794,8 +821,8 @@ __device__ __forceinline__ void ring_sum_n(const RingRows& rw, const PipeHdr& h,
 #pragma unroll
   for (int q = 0; q < N; ++q) xacc<CPT>(x[q], h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, s);
 }
-template <int CPT>
-__device__ __forceinline__ void ring_sum_any(const RingRows& rw, const PipeHdr& h, int n, float* s, int* Ex) {
+template <int CPT, class RW>
+__device__ __forceinline__ void ring_sum_any(const RW& rw, const PipeHdr& h, int n, float* s, int* Ex) {
   unsigned E2[CPT];
   xmax_init<CPT>(E2);
   for (int q = 0; q < n; ++q) {
@@ -816,8 +843,8 @@ __device__ __forceinline__ void ring_sum_any(const RingRows& rw, const PipeHdr& 
     xacc<CPT>(x, h.kb[q], h.k2[q], k2_to_ke(h.k2[q]), P, s);
   }
 }
-template <int CPT>
-__device__ __forceinline__ void ring_sum(const RingRows& rw, const PipeHdr& h, int n, float* s, int* Ex) {
+template <int CPT, class RW>
+__device__ __forceinline__ void ring_sum(const RW& rw, const PipeHdr& h, int n, float* s, int* Ex) {
   switch (n) {
     case 0: ring_sum_n<CPT, 0>(rw, h, s, Ex); break;
     case 1: ring_sum_n<CPT, 1>(rw, h, s, Ex); break;
@@ -903,7 +930,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
       const unsigned bal = __ballot_sync(0xffffffffu, ok);
       const int n = __popc(bal);
       while (rr.kold <= k - FWD_SD) release();
-      while (rr.head + (unsigned)n - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D)
+      {  // items never wrap (as in the forward) unless pc.wrap
+        unsigned pad = !pc.wrap && rr.rpos + n > R ? (unsigned)(R - rr.rpos) : 0u;
+        while (rr.head + pad + (unsigned)n - rr.tail > (unsigned)R && rr.kold < k) release();  // (R >= D)
+        if (rr.head + pad + (unsigned)n - rr.tail > (unsigned)R) pad = 0u;
+        if (!pc.wrap && rr.rpos + n > R) rr.rpos = 0;
+        rr.head += pad;
+      }
       const int ds = k & (FWD_SD - 1);
       const int slot = __popc(bal & ((1u << lane) - 1u));
       if (ok) {
@@ -943,16 +976,21 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
     const int ds = k & (FWD_SD - 1);
     mbar_wait(&full[ds], (k / FWD_SD) & 1);
     const PipeHdr& h = hdr[ds];
-    const RingRows rw{sig, sex, h.start, R, col, SW};
+    const RingRows rw0{sig, sex, h.start, R, col, SW};
     M s[CPT];
     int Ex[CPT];
-    ring_sum<CPT>(rw, h, h.n, s, Ex);
+    if (MMF_BWD_NOWRAP_PATH == 0 || pc.wrap) ring_sum<CPT>(rw0, h, h.n, s, Ex);
+    else ring_sum<CPT>(RingRowsF<SW>(rw0), h, h.n, s, Ex);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
-    Lane<M, E, CPT> out;
-    norm_lane<TrF32, CPT>(p, s, Ex, out, it.sl * SW + col, it.node);
     const size_t g = (size_t)it.node * p.Lp + (size_t)(it.sl * SW + col);
-    out.store(bmt + g, bet + g);
+    if constexpr (CPT % 2 == 0 && MMF_NORM_PACKED) {
+      norm_store_f32<CPT>(p, s, Ex, bmt + g, bet + g, it.sl * SW + col, it.node);
+    } else {
+      Lane<M, E, CPT> out;
+      norm_lane<TrF32, CPT>(p, s, Ex, out, it.sl * SW + col, it.node);
+      out.store(bmt + g, bet + g);
+    }
   }
 }
 

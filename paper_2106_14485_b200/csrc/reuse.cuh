@@ -215,7 +215,7 @@ __device__ __forceinline__ void ru_sum_n(const RuRows& rw, const RuHdr& h, float
       const unsigned u = __viaddmax_s16x2((unsigned)xw[q][k], k2, P.Lo2[k]);
       const unsigned d2 = __viaddmax_s16x2(u, P.nE2[k], 0xff82ff82u);
       s[2 * k] = fmaf(xm[q][2 * k], __uint_as_float(kb + (d2 << 23)), s[2 * k]);
-      s[2 * k + 1] = fmaf(xm[q][2 * k + 1], __uint_as_float(kb + ((d2 & 0xffff0000u) << 7)), s[2 * k + 1]);
+      s[2 * k + 1] = fmaf(xm[q][2 * k + 1], __uint_as_float(kb + MMF_HI23(d2)), s[2 * k + 1]);
     }
   }
 }
@@ -381,10 +381,8 @@ __global__ void __launch_bounds__(RU_THREADS, 1) k_bwd_reuse(DevPtrs p, PipeCfg5
     ru_sum<CPT>(rw, h, h.n, s, Ex);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
-    Lane<M, E, CPT> out;
-    norm_lane<TrF32, CPT>(p, s, Ex, out, it.s * SW + col, it.j);
     const size_t go = (size_t)it.j * p.Lp + (size_t)(it.s * SW + col);
-    out.store(bmt + go, bet + go);
+    norm_store_f32<CPT>(p, s, Ex, bmt + go, bet + go, it.s * SW + col, it.j);
   }
 }
 

@@ -204,6 +204,15 @@ def test_pipelined_kernels_L1024_grid(bwd):
     assert_parity(p, 3, "fp32", options=dict(bwd=bwd))
 
 
+@pytest.mark.parametrize("wrap", [0, 1])
+@pytest.mark.parametrize("L", [1024, 512])
+def test_pipelined_backward_ring_wrap(L, wrap):
+    """The three-pipeline backward with items that may wrap around the ring (per-row offsets) and with
+    items that never wrap (the producer skips to slot 0), on a grid with a ragged commodity tail."""
+    p = grid_problem(14, 14, 8, L - 3, 0.1, seed=33, cap=(0.5, 3.0))
+    assert_parity(p, 2, "fp32", options=dict(bwd=1, wrap=wrap))
+
+
 @pytest.mark.parametrize("L,fgw,fng,fnp", [(1024, 8, 1, 2), (1024, 4, 2, 2), (1024, 4, 3, 1), (512, 8, 1, 2),
                                            (512, 4, 2, 2), (256, 2, 4, 2)])
 def test_pipelined_forward_groups(L, fgw, fng, fnp):
