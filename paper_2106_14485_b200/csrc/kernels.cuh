@@ -58,6 +58,7 @@ struct DevPtrs {
   const int* ell_ipos;  // [A] internal arc -> slot in ell_in (head * Din + k)
   const int* ell_opos;  // [A] internal arc -> slot in ell_out (tail * Dout + k)
   int Din, Dout;
+  int diag;  // diagnostics of the pipelined forward (option "dry" >= 2; results invalid), else 0
 };
 
 // per-step arc record: gathered node, arc factor K_t W_t as XF (km = 0: zero factor), aux word

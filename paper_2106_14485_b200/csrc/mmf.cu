@@ -972,6 +972,7 @@ size_t layout(mmf_ctx* c, char* base) {
     c->wdo.fnode = c->win_bwd ? (const int*)at(L.take(c->h_wfnode_out.size() * 4 + 4)) : nullptr;
     const bool ell = c->pipe_bwd;
     p.Din = ell ? c->ell_din : 0;
+    p.diag = c->opt_dry >= 2 ? c->opt_dry : 0;
     p.Dout = ell ? c->pb.D : 0;
     p.ell_in = ell ? at(L.take(T * N * (size_t)p.Din * 16)) : nullptr;
     p.ell_ops = ell && c->prec == MMF_FP32 ? at(L.take(T * N * (size_t)p.Din * 32)) : nullptr;
@@ -1792,7 +1793,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_wrap = (int)value;
     }
     if (k == "fnp") {
-      if (value < 0 || value > 2) return fail(ctx, MMF_EINVAL, "fnp must be 0, 1 or 2");
+      if (value < 0 || value > 3) return fail(ctx, MMF_EINVAL, "fnp must be in [0, 3]");
       ctx->opt_fnp = (int)value;
     }
     if (k == "kernels") {

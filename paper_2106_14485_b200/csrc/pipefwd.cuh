@@ -42,8 +42,11 @@ static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the cons
 #ifndef MMF_BWD_NOWRAP_PATH
 #define MMF_BWD_NOWRAP_PATH 1  // compile the backward's never-wrapping item path
 #endif
+#ifndef MMF_FWD_LEAN_UPDATE
+#define MMF_FWD_LEAN_UPDATE 1  // branch-light dual update in the pipelined forward
+#endif
 #ifndef MMF_FWD_OWNG
-#define MMF_FWD_OWNG 0  // 1: the node's own row beta_t[j] is loaded by the consumers from global memory (L2-
+#define MMF_FWD_OWNG 1  // 1: the node's own row beta_t[j] is loaded by the consumers from global memory (L2-
                         // prefetched by the producer) instead of staged in the ring
 #endif
 // forward pipelines: NG consumer groups of GW warps (a group takes every NG-th item of its pipeline; a warp
@@ -52,7 +55,9 @@ template <int GW, int NG, int NP> constexpr int fwd_threads() { return NP * (GW 
 // compiled (SW, CPT, GW, NG, NP) combinations: NP pipelines per CTA, each NG groups of GW warps (a warp owns
 // CPT commodities per lane); the first of each SW is the default
 #define MMF_FWD_COMBOS(X)                                                                           \
-  X(1024, 4, 8, 1, 2) X(1024, 8, 4, 2, 2) X(1024, 8, 4, 3, 1) X(512, 2, 8, 1, 2) X(512, 4, 4, 2, 2) \
+  X(1024, 4, 8, 1, 2) X(1024, 4, 8, 1, 3) X(1024, 4, 8, 2, 1) X(1024, 8, 4, 2, 2) X(1024, 8, 4, 3, 1)  \
+  X(512, 2, 8, 1, 2)                                                                                \
+  X(512, 4, 4, 2, 2)                                                                                \
   X(256, 4, 2, 4, 2)
 inline bool fwd_combo_ok(int SW, int gw, int ng, int np) {
 #define MMF_FWD_OK(sw, cpt, g, n, q) \
@@ -228,9 +233,10 @@ struct FwdUpd {
 struct FwdOps {
   float d, wm, Km;
   int we, Ke, eopos, copos;
+  float wd, rw;  // W_old d and 1 / W_old (approximate), formed before the item's barrier
 };
 __device__ __forceinline__ FwdOps fwd_ops(const ArcOps* hops, const FwdHdr& h, int lane) {
-  FwdOps o{0.f, 1.f, 0.f, 0, 0, 0, 0};
+  FwdOps o{0.f, 1.f, 0.f, 0, 0, 0, 0, 0.f, 1.f};
   if (lane < h.na) {
     const ArcOps a = hops[lane];
     o.d = a.d;
@@ -241,12 +247,93 @@ __device__ __forceinline__ FwdOps fwd_ops(const ArcOps* hops, const FwdHdr& h, i
     o.eopos = a.eopos;
     o.copos = a.copos;
   }
+  o.wd = o.wm * o.d;
+  o.rw = __fdividef(1.f, o.wm);
   return o;
 }
 template <int GW>
 __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, const FwdOps& o,
                                              const float (*fp)[PIPE_NWC], int t, int j, int D, int lane, bool writer,
                                              bool* big_out) {
+#if MMF_FWD_LEAN_UPDATE
+  // branch-light form (same arithmetic as below up to the rounding of d / F, computed as an approximate
+  // quotient (2 ulp) instead of an IEEE one): every arc lane evaluates, selects pick the case
+  FwdUpd u{1.f, 0x3f800000u, 0u};
+  const bool act = lane < h.na;
+  const int aux = act ? h.aux[lane] : -1;
+  const int row = act ? h.rowof[lane] : -1;
+  const bool cap = aux >= 0;
+  if (row >= 0) {
+    u.nkb = h.kb[row];
+    u.nk2 = h.k2[row];
+  }
+  float F = 0.f;
+  if (cap && row >= 0) {
+    if constexpr (GW == 8) {
+      const float4 a = *reinterpret_cast<const float4*>(&fp[row][0]);
+      const float4 b = *reinterpret_cast<const float4*>(&fp[row][4]);
+      F = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
+    } else {
+#pragma unroll
+      for (int w = 0; w < GW; ++w) F += fp[row][w];
+    }
+  }
+  const float d = o.d, w0 = o.wm;
+  const int e0 = o.we;
+  // x = W_old d / F; W_new = min(x, 1) with W = wm 2^we, wm in [1, 2)
+  float x = __fdividef(o.wd, F);
+  const bool sub = x < 1.17549435e-38f;  // (subnormal or 0: rescale by 2^64)
+  x = sub ? x * 18446744073709551616.f : x;
+  const unsigned ux = __float_as_uint(x);
+  const int ex = e0 + (int)(ux >> 23) - 127 - (sub ? 64 : 0);
+  const float mx = __uint_as_float((ux & 0x007fffffu) | 0x3f800000u);
+  const bool one = !(F > 0.f) || !(x < 3.0e38f) || ex >= 0;  // (F = 0 or W d / F >= 1)
+  const bool zero = d == 0.f;
+  float wm = zero ? 0.f : one ? 1.f : mx;
+  int we = zero ? EZERO : one ? 0 : ex;
+  if (!cap) {
+    wm = w0;
+    we = e0;
+  }
+  float km = o.Km * wm;
+  int ke = o.Ke + we;
+  const bool kz = !(km > 0.f) || ke < -ELIM;
+  km = kz ? 0.f : km;
+  ke = kz ? -ELIM : min(ke, ELIM);
+  bool big = false;
+  if (cap) {
+    if (writer) {
+      View<TrF32> v(p);
+      if (!(F == F) || isinf(F)) set_error(p, ERR_NAN, -1, aux);
+      v.Wm(t - 1)[aux] = wm;
+      v.We(t - 1)[aux] = we;
+      ArcKW<float> rr;
+      rr.km = km;
+      rr.ke = ke;
+      rr.aux = aux;
+      rr.node = h.rtail[lane];
+      ((ArcKW<float>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
+      ArcOps* op = (ArcOps*)p.ell_ops + (size_t)(t - 1) * p.N * D + (size_t)j * D + lane;
+      op->wm = wm;
+      op->we = we;
+      ((ArcKW<float>*)p.inrec)[(size_t)(t - 1) * p.A + aux] = rr;
+      rr.node = j;
+      ((ArcKW<float>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + o.eopos] = rr;
+      ((ArcKW<float>*)p.outrec)[(size_t)(t - 1) * p.A + o.copos] = rr;
+    }
+    if (row >= 0) {
+      const int de = we - e0;
+      const bool ok = w0 > 0.f && wm > 0.f && de <= 40 && de >= -40;
+      big = !ok;
+      u.rq = ok ? wm * o.rw * __uint_as_float((unsigned)(de + 127) << 23) : 0.f;
+      u.nkb = __float_as_uint(km);
+      u.nk2 = pack2(ke);
+    }
+  }
+  *big_out = __any_sync(0xffffffffu, big);
+  return u;
+#else
+
   typedef float M;
   View<TrF32> v(p);
   bool big = false;
@@ -306,6 +393,7 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
   }
   *big_out = __any_sync(0xffffffffu, big);
   return u;
+#endif
 }
 
 // alpha from the new factors (gathered from the arcs' lanes), two passes over shared memory
@@ -493,6 +581,18 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
   }
   const unsigned cap = h.capmask;
   float (*fp)[PIPE_NWC] = G.fpart[par];
+  if (p.diag == 2) {  // diagnostics (results invalid): alpha with the old factors only
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      s[c] = 0.f;
+      Ex[c] = P.E[c];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) s[c] += tq[q][c] * bl[c];
+    return;
+  }
   if (N > 0 && cap != 0u) {
     constexpr int NF = N <= 4 ? 4 : 8;
     float f[NF];
@@ -514,6 +614,18 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
     }
   }
   named_bar(bar_id, GW * 32);
+  if (p.diag == 3) {  // diagnostics (results invalid): flows and their reduction, no dual update
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      s[c] = fp[0][c];
+      Ex[c] = P.E[c];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) s[c] = fmaf(tq[q][c], bl[c], s[c]);
+    return;
+  }
   bool big;
   const UpdView u = fwd_update_phase<GW>(p, h, o0, hops, G, par, t, j, D, lane, wg, bar_id, &big);
   if (!big) {
@@ -584,7 +696,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
   typedef int16_t E;
   constexpr int SW = 32 * GW * CPT;
   constexpr int PW = GW * NG + 1;                             // warps per pipeline
-  constexpr int NMAX = CPT >= 8 && fwd_threads<GW, NG, NP>() > 448 ? 6 : 8;  // register path up to NMAX rows
+  constexpr int NMAX = fwd_threads<GW, NG, NP>() > 640 ? 5 : CPT >= 8 && fwd_threads<GW, NG, NP>() > 448 ? 6 : 8;
   extern __shared__ __align__(16) unsigned char smem_all[];
   const PFwdSmem L = pfwd_smem(pc.R, pc.D, SW, NG);
   const int pl = (threadIdx.x >> 5) / PW;                     // pipeline of this warp
@@ -744,7 +856,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     mbar_wait(&full[ds], (k / FWD_SDF) & 1);
     const FwdHdr& h = hdr[ds];
     const ArcOps* hops = oring + h.oslot * D;
-    if (pc.dry) {  // diagnostics: delivery rate of the producer / TMA alone
+    if (pc.dry == 1) {  // diagnostics: delivery rate of the producer / TMA alone
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[ds]);
       continue;
