@@ -253,8 +253,9 @@ __device__ __forceinline__ FwdOps fwd_ops(const ArcOps* hops, const FwdHdr& h, i
 }
 template <int GW>
 __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, const FwdOps& o,
-                                             const float (*fp)[PIPE_NWC], int t, int j, int D, int lane, bool writer,
+                                             const float (*fp)[PIPE_NWC], int t, int j, int D, int lane, int writer_wg,
                                              bool* big_out) {
+  const bool writer = writer_wg == 0;
 #if MMF_FWD_LEAN_UPDATE
   // branch-light form (same arithmetic as below up to the rounding of d / F, computed as an approximate
   // quotient (2 ulp) instead of an IEEE one): every arc lane evaluates, selects pick the case
@@ -302,25 +303,33 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
   ke = kz ? -ELIM : min(ke, ELIM);
   bool big = false;
   if (cap) {
-    if (writer) {
+    // the new W and the refreshed records are stored by one warp of the group (SP = 1; spreading the stores
+    // over the warps measured slower)
+    const int wg = writer_wg == 0 ? 0 : 1 + writer_wg;
+    ArcKW<float> rr;
+    rr.km = km;
+    rr.ke = ke;
+    rr.aux = aux;
+    rr.node = j;
+    const size_t ell = (size_t)(t - 1) * p.N * D + (size_t)j * D + lane;
+    if (wg == 0) {
       View<TrF32> v(p);
-      if (!(F == F) || isinf(F)) set_error(p, ERR_NAN, -1, aux);
       v.Wm(t - 1)[aux] = wm;
       v.We(t - 1)[aux] = we;
-      ArcKW<float> rr;
-      rr.km = km;
-      rr.ke = ke;
-      rr.aux = aux;
-      rr.node = h.rtail[lane];
-      ((ArcKW<float>*)p.ell_in)[(size_t)(t - 1) * p.N * D + (size_t)j * D + lane] = rr;
-      ArcOps* op = (ArcOps*)p.ell_ops + (size_t)(t - 1) * p.N * D + (size_t)j * D + lane;
+    }
+    if (wg == 0) {
+      ArcOps* op = (ArcOps*)p.ell_ops + ell;
       op->wm = wm;
       op->we = we;
-      ((ArcKW<float>*)p.inrec)[(size_t)(t - 1) * p.A + aux] = rr;
-      rr.node = j;
-      ((ArcKW<float>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + o.eopos] = rr;
-      ((ArcKW<float>*)p.outrec)[(size_t)(t - 1) * p.A + o.copos] = rr;
     }
+    if (wg == 0) ((ArcKW<float>*)p.ell_out)[(size_t)(t - 1) * p.N * p.Dout + o.eopos] = rr;
+    if (wg == 0) ((ArcKW<float>*)p.outrec)[(size_t)(t - 1) * p.A + o.copos] = rr;
+    if (wg == 0) {
+      if (!(F == F) || isinf(F)) set_error(p, ERR_NAN, -1, aux);
+    }
+    rr.node = h.rtail[lane];
+    if (wg == 0) ((ArcKW<float>*)p.ell_in)[ell] = rr;
+    if (wg == 0) ((ArcKW<float>*)p.inrec)[(size_t)(t - 1) * p.A + aux] = rr;
     if (row >= 0) {
       const int de = we - e0;
       const bool ok = w0 > 0.f && wm > 0.f && de <= 40 && de >= -40;
@@ -464,7 +473,7 @@ __device__ __forceinline__ UpdView fwd_update_phase(const DevPtrs& p, const FwdH
   if (wg == 0) {
     const FwdOps o = fwd_ops(hops, h, lane);
     bool b;
-    const FwdUpd u = fwd_update<GW>(p, h, o, G.fpart[par], t, j, D, lane, true, &b);
+    const FwdUpd u = fwd_update<GW>(p, h, o, G.fpart[par], t, j, D, lane, 0, &b);
     G.rq[par][lane] = u.rq;
     G.nkb[par][lane] = u.nkb;
     G.nk2[par][lane] = u.nk2;
@@ -476,7 +485,7 @@ __device__ __forceinline__ UpdView fwd_update_phase(const DevPtrs& p, const FwdH
   v.k2_ = G.nk2[par];
   *big = G.big[par] != 0;
 #else
-  v.u = fwd_update<GW>(p, h, o0, G.fpart[par], t, j, D, lane, wg == 0, big);
+  v.u = fwd_update<GW>(p, h, o0, G.fpart[par], t, j, D, lane, wg, big);
 #endif
   return v;
 }
