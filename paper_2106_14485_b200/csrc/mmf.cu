@@ -172,6 +172,7 @@ struct mmf_ctx {
   std::vector<cudaEvent_t> ev_pool;
 
   size_t sm() const { return prec == MMF_FP32 ? sizeof(float) : sizeof(double); }
+  int* d_int_of_arc = nullptr;  // (readouts: user arc -> internal arc, uploaded on first use)
   size_t se() const { return prec == MMF_FP32 ? sizeof(int16_t) : sizeof(int32_t); }
 };
 
@@ -1714,6 +1715,61 @@ mmf_status finalize(mmf_ctx* ctx) {
 // ================================================================================================
 // C ABI
 
+namespace mmf {
+// readouts in user arc order, converted to fp64 on the device ([T][A]: t * A + user arc <- t * A + internal arc)
+template <class M>
+__global__ void k_export_flows(const M* __restrict__ src, const int* __restrict__ ioa, double* __restrict__ out,
+                               int64_t A, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = k / A, a = k - t * A;
+    out[k] = (double)src[t * A + ioa[a]];
+  }
+}
+template <class M>
+__global__ void k_export_duals(const M* __restrict__ wm, const int* __restrict__ we, const int* __restrict__ ioa,
+                               double* __restrict__ out, int64_t A, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = k / A, a = k - t * A;
+    const int64_t i = t * A + ioa[a];
+    const double m = (double)wm[i];
+    out[k] = m == 0.0 ? 0.0 : ldexp(m, we[i]);  // (values below 2^-1074 read 0)
+  }
+}
+// what: 0 edge flows (one readout pass first), 1 capacity duals
+static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
+  if (!ctx || !out) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  CU(cudaSetDevice(ctx->device));
+  if (what == 0) {
+    mmf_status st = dispatch(ctx, [&](auto eng) { return decltype(eng)::readout(ctx, ctx->stream); });
+    if (st != MMF_OK) return st;
+  }
+  mmf_status st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  const int64_t A = ctx->A, n = (int64_t)ctx->T * A;
+  if (!ctx->d_int_of_arc) {
+    CU(cudaMalloc(&ctx->d_int_of_arc, (size_t)A * sizeof(int)));
+    CU(cudaMemcpy(ctx->d_int_of_arc, ctx->int_of_arc.data(), (size_t)A * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  double* d = nullptr;
+  CU(cudaMallocAsync(&d, (size_t)n * sizeof(double), ctx->stream));
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 8 * 148);
+  if (ctx->prec == MMF_FP32) {
+    if (what == 0) k_export_flows<float><<<grid, 256, 0, ctx->stream>>>((const float*)ctx->dp.Fout, ctx->d_int_of_arc, d, A, n);
+    else k_export_duals<float><<<grid, 256, 0, ctx->stream>>>((const float*)ctx->dp.Wm, ctx->dp.We, ctx->d_int_of_arc, d, A, n);
+  } else {
+    if (what == 0) k_export_flows<double><<<grid, 256, 0, ctx->stream>>>((const double*)ctx->dp.Fout, ctx->d_int_of_arc, d, A, n);
+    else k_export_duals<double><<<grid, 256, 0, ctx->stream>>>((const double*)ctx->dp.Wm, ctx->dp.We, ctx->d_int_of_arc, d, A, n);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  cudaFreeAsync(d, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return fail(ctx, MMF_ECUDA, std::string("readout: ") + cudaGetErrorString(e));
+  return MMF_OK;
+}
+}  // namespace mmf
+
 extern "C" {
 
 const char* mmf_version(void) { return "mmf 0.1 (sm_100a, XF f32/i16 + f64/i32)"; }
@@ -2077,43 +2133,11 @@ mmf_status mmf_sync(mmf_ctx* ctx) {
 }
 
 mmf_status mmf_read_edge_flows(mmf_ctx* ctx, double* out) {
-  if (!ctx || !out) return MMF_EINVAL;
-  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
-  CU(cudaSetDevice(ctx->device));
-  mmf_status st = dispatch(ctx, [&](auto eng) { return decltype(eng)::readout(ctx, ctx->stream); });
-  if (st != MMF_OK) return st;
-  st = mmf_sync(ctx);
-  if (st != MMF_OK) return st;
-  const size_t TA = (size_t)ctx->T * ctx->A;
-  std::vector<char> h(TA * ctx->sm());
-  CU(cudaMemcpy(h.data(), ctx->dp.Fout, h.size(), cudaMemcpyDeviceToHost));
-  const int64_t A = ctx->A;
-  for (int t = 0; t < ctx->T; ++t)
-    for (int64_t a = 0; a < A; ++a) {
-      size_t k = (size_t)t * A + ctx->int_of_arc[a];
-      out[(size_t)t * A + a] = ctx->prec == MMF_FP32 ? (double)((float*)h.data())[k] : ((double*)h.data())[k];
-    }
-  return MMF_OK;
+  return mmf::read_export(ctx, out, 0);
 }
 
 mmf_status mmf_read_cap_duals(mmf_ctx* ctx, double* out) {
-  if (!ctx || !out) return MMF_EINVAL;
-  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
-  mmf_status st = mmf_sync(ctx);
-  if (st != MMF_OK) return st;
-  const size_t TA = (size_t)ctx->T * ctx->A;
-  std::vector<char> hm(TA * ctx->sm());
-  std::vector<int> he(TA);
-  CU(cudaMemcpy(hm.data(), ctx->dp.Wm, hm.size(), cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(he.data(), ctx->dp.We, TA * 4, cudaMemcpyDeviceToHost));
-  const int64_t A = ctx->A;
-  for (int t = 0; t < ctx->T; ++t)
-    for (int64_t a = 0; a < A; ++a) {
-      size_t k = (size_t)t * A + ctx->int_of_arc[a];
-      double m = ctx->prec == MMF_FP32 ? (double)((float*)hm.data())[k] : ((double*)hm.data())[k];
-      out[(size_t)t * A + a] = m == 0 ? 0.0 : std::ldexp(m, he[k]);
-    }
-  return MMF_OK;
+  return mmf::read_export(ctx, out, 1);
 }
 
 mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {
@@ -2214,6 +2238,7 @@ mmf_status mmf_destroy(mmf_ctx* ctx) {
   if (ctx->ev_priv) cudaEventDestroy(ctx->ev_priv);
   if (ctx->comm) nccl_api().CommDestroy(ctx->comm);
   if (ctx->ws_owned) cudaFree(ctx->ws);
+  if (ctx->d_int_of_arc) cudaFree(ctx->d_int_of_arc);
   if (ctx->priv) cudaStreamDestroy(ctx->priv);
   delete ctx;
   return MMF_OK;
