@@ -42,6 +42,9 @@ static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the cons
 #ifndef MMF_BWD_NOWRAP_PATH
 #define MMF_BWD_NOWRAP_PATH 1  // compile the backward's never-wrapping item path
 #endif
+#ifndef MMF_FWD_ILP
+#define MMF_FWD_ILP 0  // (measured 1% slower) split dependency chains (maximum, alpha accumulation) of the forward's register path
+#endif
 #ifndef MMF_FWD_LEAN_UPDATE
 #define MMF_FWD_LEAN_UPDATE 1  // branch-light dual update in the pipelined forward
 #endif
@@ -568,6 +571,24 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
       load_sig<CPT>(rw.sig + o, tq[q]);
     }
     unsigned E2[CPT / 2];
+#if MMF_FWD_ILP
+    {  // two interleaved maximum chains (halves the dependency depth)
+      unsigned Eb[CPT / 2];
+      xmax_init<CPT>(E2);
+      xmax_init<CPT>(Eb);
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        const unsigned k2 = h.k2[q];
+#pragma unroll
+        for (int k = 0; k < CPT / 2; ++k) {
+          if (q & 1) Eb[k] = __viaddmax_s16x2((unsigned)xw[q][k], k2, Eb[k]);
+          else E2[k] = __viaddmax_s16x2((unsigned)xw[q][k], k2, E2[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < CPT / 2; ++k) E2[k] = __vmaxs2(E2[k], Eb[k]);
+    }
+#else
     xmax_init<CPT>(E2);
 #pragma unroll
     for (int q = 0; q < N; ++q) {
@@ -575,6 +596,7 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
 #pragma unroll
       for (int k = 0; k < CPT / 2; ++k) E2[k] = __viaddmax_s16x2((unsigned)xw[q][k], k2, E2[k]);
     }
+#endif
     P.set(E2);
 #pragma unroll
     for (int q = 0; q < N; ++q) xterms_w<CPT>(xw[q], tq[q], h.kb[q], h.k2[q], P);
@@ -643,12 +665,29 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
       s[c] = 0.f;
       Ex[c] = P.E[c];
     }
+#if MMF_FWD_ILP
+    float s2[CPT];  // (two interleaved accumulation chains)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) s2[c] = 0.f;
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      const float r = u.rq(h.rarc[q]);
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        if (q & 1) s2[c] = fmaf(r, tq[q][c], s2[c]);
+        else s[c] = fmaf(r, tq[q][c], s[c]);
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) s[c] += s2[c];
+#else
 #pragma unroll
     for (int q = 0; q < N; ++q) {
       const float r = u.rq(h.rarc[q]);
 #pragma unroll
       for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
     }
+#endif
   } else {  // large ratios: recompute from shared memory with the new factors
     fwd_alpha_new<CPT>(rw, h, u, N, s, Ex);
   }

@@ -204,6 +204,34 @@ def test_pipelined_kernels_L1024_grid(bwd):
     assert_parity(p, 3, "fp32", options=dict(bwd=bwd))
 
 
+def _hub_problem(L, nhub=22):
+    """A 10 x 10 grid plus a hub (node 0 linked both ways to nhub other nodes: degree nhub + 3, above the
+    pipelined kernels' register paths) and a node whose in-arcs and self-loop are all closed (no rows once its
+    factors reach 0: the empty-item path).  nhub = 8 keeps the widest item small enough for 1024-commodity
+    pipelined slices; nhub = 22 selects 512-commodity slices."""
+    import dataclasses
+    p = grid_problem(10, 10, 6, L, 0.1, seed=35, cap=(0.5, 3.0))
+    hub = np.arange(30, 30 + nhub, dtype=np.int32)
+    tail = np.r_[p.tail, hub, np.zeros_like(hub)].astype(np.int32)
+    head = np.r_[p.head, np.zeros_like(hub), hub].astype(np.int32)
+    cost = np.r_[p.cost, np.full(2 * hub.size, 0.7)]
+    cap = np.r_[p.cap, np.full(2 * hub.size, 2.0)]
+    cap[head == 55] = 0.0  # (node 55: closed in-arcs and loop)
+    src, dst = p.src.copy(), p.dst.copy()
+    dst[dst == 55] = 56
+    src[src == dst] = 57
+    # (OD pairs were drawn within 6 hops; 8 steps leave room for the detours around node 55)
+    return dataclasses.replace(p, tail=tail, head=head, cost=cost, cap=cap, src=src, dst=dst, T=8, name=f"hub-L{L}")
+
+
+@pytest.mark.parametrize("L,nhub,opts", [(1019, 22, {}), (1019, 22, dict(bwd=1, wrap=0)), (509, 22, {}),
+                                         (1019, 8, {}), (1019, 8, dict(fgw=4, fng=2, fnp=2)),
+                                         (1019, 8, dict(bwd=4))])
+def test_pipelined_hub_and_empty_items(L, nhub, opts):
+    """High-degree items (streaming paths of the pipelined forward and backward) and empty items, live oracle."""
+    assert_parity(_hub_problem(L, nhub), 3, "fp32", options=opts)
+
+
 @pytest.mark.parametrize("wrap", [0, 1])
 @pytest.mark.parametrize("L", [1024, 512])
 def test_pipelined_backward_ring_wrap(L, wrap):
