@@ -173,6 +173,7 @@ struct mmf_ctx {
 
   size_t sm() const { return prec == MMF_FP32 ? sizeof(float) : sizeof(double); }
   int* d_int_of_arc = nullptr;  // (readouts: user arc -> internal arc, uploaded on first use)
+  double* d_export = nullptr;    // (readouts: [T][A] fp64 staging, allocated on first use)
   size_t se() const { return prec == MMF_FP32 ? sizeof(int16_t) : sizeof(int32_t); }
 };
 
@@ -1751,8 +1752,8 @@ static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
     CU(cudaMalloc(&ctx->d_int_of_arc, (size_t)A * sizeof(int)));
     CU(cudaMemcpy(ctx->d_int_of_arc, ctx->int_of_arc.data(), (size_t)A * sizeof(int), cudaMemcpyHostToDevice));
   }
-  double* d = nullptr;
-  CU(cudaMallocAsync(&d, (size_t)n * sizeof(double), ctx->stream));
+  if (!ctx->d_export) CU(cudaMalloc(&ctx->d_export, (size_t)n * sizeof(double)));
+  double* d = ctx->d_export;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 8 * 148);
   if (ctx->prec == MMF_FP32) {
     if (what == 0) k_export_flows<float><<<grid, 256, 0, ctx->stream>>>((const float*)ctx->dp.Fout, ctx->d_int_of_arc, d, A, n);
@@ -1763,7 +1764,6 @@ static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
   }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-  cudaFreeAsync(d, ctx->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return fail(ctx, MMF_ECUDA, std::string("readout: ") + cudaGetErrorString(e));
   return MMF_OK;
@@ -2239,6 +2239,7 @@ mmf_status mmf_destroy(mmf_ctx* ctx) {
   if (ctx->comm) nccl_api().CommDestroy(ctx->comm);
   if (ctx->ws_owned) cudaFree(ctx->ws);
   if (ctx->d_int_of_arc) cudaFree(ctx->d_int_of_arc);
+  if (ctx->d_export) cudaFree(ctx->d_export);
   if (ctx->priv) cudaStreamDestroy(ctx->priv);
   delete ctx;
   return MMF_OK;

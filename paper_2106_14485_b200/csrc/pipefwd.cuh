@@ -42,6 +42,9 @@ static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the cons
 #ifndef MMF_BWD_NOWRAP_PATH
 #define MMF_BWD_NOWRAP_PATH 1  // compile the backward's never-wrapping item path
 #endif
+#ifndef MMF_FWD_PREACC
+#define MMF_FWD_PREACC 0  // (measured no gain) alpha with the old factors before the barrier, corrected for changed factors after
+#endif
 #ifndef MMF_FWD_ILP
 #define MMF_FWD_ILP 0  // (measured 1% slower) split dependency chains (maximum, alpha accumulation) of the forward's register path
 #endif
@@ -644,6 +647,17 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
       if ((lane & 3) == 0 && row < N && ((cap >> row) & 1u)) fp[row][wg] = r;
     }
   }
+#if MMF_FWD_PREACC && !MMF_FWD_DEDUP
+  // alpha with the old factors, accumulated before the barrier (off the update's critical path); after the
+  // update only the rows whose factor changed (ratio r != 1: saturated arcs) are corrected by (r - 1) t_q
+  float sp[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) sp[c] = 0.f;
+#pragma unroll
+  for (int q = 0; q < N; ++q)
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) sp[c] += tq[q][c];
+#endif
   named_bar(bar_id, GW * 32);
   if (p.diag == 3) {  // diagnostics (results invalid): flows and their reduction, no dual update
 #pragma unroll
@@ -665,7 +679,21 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
       s[c] = 0.f;
       Ex[c] = P.E[c];
     }
-#if MMF_FWD_ILP
+#if MMF_FWD_PREACC && !MMF_FWD_DEDUP
+    const unsigned chg = __ballot_sync(0xffffffffu, lane < h.na && u.u.rq != 1.f);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) s[c] = sp[c];
+    if (chg) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        const int src = h.rarc[q];
+        const float r = __shfl_sync(0xffffffffu, u.u.rq, src) - 1.f;
+        if ((chg >> src) & 1u)
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
+      }
+    }
+#elif MMF_FWD_ILP
     float s2[CPT];  // (two interleaved accumulation chains)
 #pragma unroll
     for (int c = 0; c < CPT; ++c) s2[c] = 0.f;
