@@ -197,10 +197,47 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
     st.sweeps += 1
 
 
-def oracle_run(problem, sweeps: int) -> OracleState:
+def damped_update(omega_old: np.ndarray, omega_full: np.ndarray, theta: float) -> np.ndarray:
+    """W <- W^(1 - theta) * min(W d / F, 1)^theta, in logs; an exact zero stays zero
+    (0^x = 0 for x > 0), theta = 1 is the undamped update."""
+    if theta == 1.0:
+        return omega_full.copy()
+    with np.errstate(invalid="ignore"):
+        om = (1.0 - theta) * omega_old + theta * omega_full
+    return np.where(np.isneginf(omega_old) | np.isneginf(omega_full), NEG_INF, om)
+
+
+def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
+    """One sweep of the bulk-coupled (Jacobi) schedule of SURVEY §8(f) NEXT-1: every W_t is updated from the
+    same alpha/beta pair — the forward pass computes alpha_{t+1} with the W_t of the previous sweep and the
+    flows F_t from (alpha_t, beta_{t+1}) — then damped, W <- W^(1 - theta) min(W d / F, 1)^theta; then the
+    sink scaling and the backward pass as in Algorithm 2."""
+    p = st.problem
+    oi = st.in_seg[0]
+    tail_i = p.tail[oi]
+    st.lam0 = _boundary(st.log_mu0, st.b[0], "source")
+    st.a[0] = st.lam0
+    new_omega = np.empty_like(st.omega)
+    for t in range(p.T):
+        X = st.a[t][:, p.tail] + st.lK[t][None, :] + st.b[t + 1][:, p.head]
+        full = capacity_update(st.logd[t], _lse_rows(X))
+        new_omega[t] = damped_update(st.omega[t], full, theta)
+        Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]   # (the previous W_t)
+        st.a[t + 1] = seg_lse(Y, st.in_seg)
+    st.omega = new_omega
+    st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
+    backward(st)
+    st.sweeps += 1
+
+
+def oracle_run(problem, sweeps: int, schedule: str = "gs", theta: float = 1.0) -> OracleState:
+    """sweeps of Algorithm 2 (schedule "gs") or of the damped Jacobi schedule ("jacobi")."""
     st = oracle_init(problem)
     for _ in range(sweeps):
-        oracle_sweep(st)
+        if schedule == "gs":
+            oracle_sweep(st)
+        else:
+            oracle_sweep_jacobi(st, theta)
     return st
 
 

@@ -356,3 +356,79 @@ def test_tiny_runs_200_sweeps_and_satisfies_capacities_approximately():
     assert abs(s["mass"] - 3.0) < 1e-9
     assert s["src_mismatch"] < 1e-6
     assert s["cap_violation"] < 1e-3
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-1: the damped Jacobi schedule, W <- W^(1-theta) min(W d / F, 1)^theta from one
+# alpha/beta pair
+
+from oracle import oracle_sweep_jacobi  # noqa: E402
+
+
+@pytest.mark.parametrize("kw", [MICROS[0], MICROS[1], MICROS[6]])
+@pytest.mark.parametrize("theta", [1.0, 0.5])
+def test_jacobi_update_equals_full_tensor_projection(kw, theta):
+    """Every W_t of a Jacobi sweep is the damped update evaluated on the SAME tensor: the flows are the
+    bimarginals of M(U0 new, W old, UT old) summed literally over the full tensor (brute force), and the
+    sink scaling then matches P_T = muT of M(U0 new, W new, UT new)."""
+    from oracle.brute import bimarginal
+    p = _micro(kw)
+    st = oracle_init(p)
+    for _ in range(2):
+        oracle_sweep(st)
+    for _ in range(3):
+        W_old, lamT_old = np.exp(st.omega), st.lamT.copy()
+        oracle_sweep_jacobi(st, theta)
+        M = full_tensor(p, np.exp(st.lam0), W_old, np.exp(lamT_old))
+        F = arc_flows(p, M)
+        cap = np.broadcast_to(p.cap, F.shape)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            full = np.where(np.isinf(cap), 1.0, np.where(cap == 0, 0.0,
+                            np.where(F > 0, np.minimum(W_old * cap / np.where(F > 0, F, 1.0), 1.0), 1.0)))
+        W_ref = W_old ** (1.0 - theta) * full ** theta
+        assert max_rel_err(np.exp(st.omega), W_ref, 1e-300) < 1e-12
+        M_new = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT))
+        # the end-of-sweep sink marginal is exact only for the alpha that a4 used: alpha_T of the pass with
+        # W old, i.e. the tensor M(U0 new, W old, UT new)
+        M_a4 = full_tensor(p, np.exp(st.lam0), W_old, np.exp(st.lamT))
+        assert max_rel_err(commodity_marginal(M_a4, p.T), p.muT, 1e-300) < 1e-12
+        assert np.all(np.isfinite(commodity_marginal(M_new, 0)))
+
+
+@pytest.mark.parametrize("theta", [0.3, 1.0])
+def test_jacobi_equals_gs_without_capacities(theta):
+    """d = inf: W stays 1, so the Jacobi schedule reduces to the plain Sinkhorn of Algorithm 2 iterate by
+    iterate (the schedules differ only in when W is updated)."""
+    p = grid_problem(3, 3, 5, 3, 0.3, seed=12, cap=None)
+    a = oracle_init(p)
+    b = oracle_init(p)
+    for _ in range(4):
+        oracle_sweep(a)
+        oracle_sweep_jacobi(b, theta)
+        assert max_rel_err(np.exp(b.lam0), np.exp(a.lam0), 1e-300) < 1e-13
+        assert max_rel_err(np.exp(b.lamT), np.exp(a.lamT), 1e-300) < 1e-13
+
+
+def test_jacobi_fixed_point_is_the_gs_optimum():
+    """Damped Jacobi converges to the same optimum as Gauss-Seidel (the unique minimiser of the strictly convex
+    problem, pinned independently by the LP bracket P6): capacity duals and flows agree after convergence."""
+    p = grid_problem(3, 3, 4, 2, 0.5, seed=13, cap=(0.15, 0.4))
+    gs = oracle_run(p, 400)
+    jb = oracle_run(p, 400, schedule="jacobi", theta=0.5)
+    Fg, Wg = readout_flows(gs)
+    Fj, Wj = readout_flows(jb)
+    assert max_rel_err(Wj, Wg, 1e-12) < 1e-7
+    assert max_rel_err(Fj, Fg, 1e-12) < 1e-7
+    assert np.any(Wg < 0.99)  # (capacities bind: the schedules differ along the way)
+
+
+def test_jacobi_theta_zero_keeps_w():
+    """theta = 0 never moves W: after any number of sweeps the state is Algorithm 2's on the uncapacitated
+    copy of the instance."""
+    import dataclasses
+    p = grid_problem(3, 3, 4, 2, 0.5, seed=14, cap=(0.15, 0.4))
+    q = dataclasses.replace(p, cap=np.full_like(p.cap, np.inf))
+    a = oracle_run(q, 3)
+    b = oracle_run(p, 3, schedule="jacobi", theta=0.0)
+    assert np.all(b.omega == 0.0)
+    assert max_rel_err(np.exp(b.lam0), np.exp(a.lam0), 1e-300) < 1e-13
