@@ -227,6 +227,12 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     st.omega = new_omega
     st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
     backward(st)
+    # readouts (edge flows, mass) are projections of the end-of-sweep tensor M(U0, W, UT): keep the forward
+    # messages of that tensor, i.e. recomputed with the new W (under Gauss-Seidel the pass's own messages
+    # already are; DESIGN.md §2 reading R-J)
+    for t in range(p.T):
+        Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
+        st.a[t + 1] = seg_lse(Y, st.in_seg)
     st.sweeps += 1
 
 

@@ -59,6 +59,8 @@ struct DevPtrs {
   const int* ell_opos;  // [A] internal arc -> slot in ell_out (tail * Dout + k)
   int Din, Dout;
   int diag;  // diagnostics of the pipelined forward (option "dry" >= 2; results invalid), else 0
+  int jac;      // schedule: 0 Gauss-Seidel (Algorithm 2), 1 damped Jacobi
+  float theta;  // Jacobi damping: W <- W^(1 - theta) min(W d / F, 1)^theta
 };
 
 // per-step arc record: gathered node, arc factor K_t W_t as XF (km = 0: zero factor), aux word

@@ -105,6 +105,8 @@ struct mmf_ctx {
   int opt_dry = 0;      // diagnostics: pipelined backward consumers skip the arithmetic
   int opt_copy = 0;     // pipelined kernels' row staging: 0 = TMA bulk copies, 1 = per-lane cp.async
   int opt_wintma = 1;   // window kernels: 1 = 2-D TMA row-block loads, 0 = per-thread cp.async
+  int opt_schedule = 0;      // 0 Gauss-Seidel (Algorithm 2), 1 damped Jacobi
+  int opt_theta_milli = 500;  // Jacobi damping theta in 1/1000
   int opt_wrap = -1;    // k_bwd_pipe2 ring wrap: -1 auto, 0 items never wrap, 1 items may wrap
   int opt_fgw = 0;      // pipelined forward: warps per consumer group (0 auto, 8, 4, 2)
   int opt_fng = 0;      // pipelined forward: consumer groups per pipeline (0 auto, 1 .. 6)
@@ -975,6 +977,8 @@ size_t layout(mmf_ctx* c, char* base) {
     const bool ell = c->pipe_bwd;
     p.Din = ell ? c->ell_din : 0;
     p.diag = c->opt_dry >= 2 ? c->opt_dry : 0;
+    p.jac = c->opt_schedule;
+    p.theta = (float)c->opt_theta_milli / 1000.f;
     p.Dout = ell ? c->pb.D : 0;
     p.ell_in = ell ? at(L.take(T * N * (size_t)p.Din * 16)) : nullptr;
     p.ell_ops = ell && c->prec == MMF_FP32 ? at(L.take(T * N * (size_t)p.Din * 32)) : nullptr;
@@ -1829,7 +1833,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -1843,6 +1847,14 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     if (k == "fng") {
       if (value < 0 || value > 6) return fail(ctx, MMF_EINVAL, "fng must be in [0, 6]");
       ctx->opt_fng = (int)value;
+    }
+    if (k == "schedule") {
+      if (value < 0 || value > 1) return fail(ctx, MMF_EINVAL, "schedule must be 0 (Gauss-Seidel) or 1 (Jacobi)");
+      ctx->opt_schedule = (int)value;
+    }
+    if (k == "theta_milli") {
+      if (value < 0 || value > 1000) return fail(ctx, MMF_EINVAL, "theta_milli must be in [0, 1000]");
+      ctx->opt_theta_milli = (int)value;
     }
     if (k == "wrap") {
       if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "wrap must be -1, 0 or 1");
@@ -2068,6 +2080,10 @@ mmf_status mmf_init(mmf_ctx* ctx) {
   CU(cudaSetDevice(ctx->device));
   mmf_status st = finalize(ctx);
   if (st != MMF_OK) return st;
+  if (ctx->opt_schedule == 1 && !(ctx->prec == MMF_FP32 && ctx->pipe_fwd && ctx->opt_kernels >= 5 && !ctx->comm))
+    return fail(ctx, MMF_EINVAL,
+                "schedule 1 (Jacobi) runs on the pipelined fp32 forward: one slice of >= 512 commodities per node, "
+                "single GPU");
   st = dispatch(ctx, [&](auto eng) { return decltype(eng)::init_device(ctx, ctx->stream); });
   if (st != MMF_OK) return st;
   CU(cudaGetLastError());

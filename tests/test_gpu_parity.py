@@ -34,14 +34,14 @@ def run_gpu(p, sweeps, prec, **kw):
     return F, W, st
 
 
-def run_oracle(p, sweeps):
-    st = oracle_run(p, sweeps)
+def run_oracle(p, sweeps, **kw):
+    st = oracle_run(p, sweeps, **kw)
     F, W = readout_flows(st)
     return F, W, oracle_stats(st)
 
 
-def assert_parity(p, sweeps, prec, **kw):
-    Fo, Wo, so = run_oracle(p, sweeps)
+def assert_parity(p, sweeps, prec, oracle_kw=None, **kw):
+    Fo, Wo, so = run_oracle(p, sweeps, **(oracle_kw or {}))
     Fg, Wg, sg = run_gpu(p, sweeps, prec, **kw)
     ef = max_rel_err(Fg, Fo, flow_floor(p))
     ew = max_rel_err(Wg, Wo, W_FLOOR)
@@ -230,6 +230,24 @@ def _hub_problem(L, nhub=22):
 def test_pipelined_hub_and_empty_items(L, nhub, opts):
     """High-degree items (streaming paths of the pipelined forward and backward) and empty items, live oracle."""
     assert_parity(_hub_problem(L, nhub), 3, "fp32", options=opts)
+
+
+@pytest.mark.parametrize("theta", [500, 1000, 200])
+@pytest.mark.parametrize("which", ["grid", "hub"])
+def test_jacobi_schedule(which, theta):
+    """the damped Jacobi schedule (option schedule=1, theta_milli) in the pipelined
+    forward against the oracle's Jacobi sweep (tests/test_oracle_pins.py pins it), 1024-commodity slices."""
+    p = grid_problem(12, 12, 8, 1019, 0.1, seed=31, cap=(0.3, 1.5)) if which == "grid" else _hub_problem(1019, 8)
+    assert_parity(p, 4, "fp32", oracle_kw=dict(schedule="jacobi", theta=theta / 1000.0),
+                  options=dict(schedule=1, theta_milli=theta))
+
+
+def test_jacobi_schedule_unsupported_paths_rejected():
+    from paper_2106_14485_b200 import MMFError
+    p = grid_problem(4, 4, 4, 8, 0.5, seed=36)
+    with pytest.raises(MMFError) as e:
+        run_gpu(p, 1, "fp64", options=dict(schedule=1))
+    assert e.value.name == "MMF_EINVAL"
 
 
 @pytest.mark.parametrize("wrap", [0, 1])

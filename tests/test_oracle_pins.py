@@ -392,7 +392,9 @@ def test_jacobi_update_equals_full_tensor_projection(kw, theta):
         # W old, i.e. the tensor M(U0 new, W old, UT new)
         M_a4 = full_tensor(p, np.exp(st.lam0), W_old, np.exp(st.lamT))
         assert max_rel_err(commodity_marginal(M_a4, p.T), p.muT, 1e-300) < 1e-12
-        assert np.all(np.isfinite(commodity_marginal(M_new, 0)))
+        # readout = projections of the end-of-sweep tensor
+        F_end, _ = readout_flows(st)
+        assert max_rel_err(F_end, arc_flows(p, M_new), 1e-300) < 1e-12
 
 
 @pytest.mark.parametrize("theta", [0.3, 1.0])
