@@ -141,6 +141,16 @@ mmf_status mmf_sweep(mmf_ctx* ctx, int32_t n);
  * (commodity, node) in mmf_last_error) and NCCL async errors. */
 mmf_status mmf_sync(mmf_ctx* ctx);
 
+/* Solve to tolerance (SPEC solve): run sweeps until the error of the end-of-sweep state
+ *   err = ( sum_{l,i} |U0 beta_0 - mu0| + sum_{l,j} |alpha_T UT - muT| + sum_{t,a} (F_t[a] - d_t[a])_+ ) / mass
+ * (marginal L1 mismatches plus the total capacity excess, relative to the tensor mass; reduced on the device,
+ * all ranks) is below tol, evaluated every check_every sweeps, at most max_sweeps sweeps.  err_hist
+ * (nullable) receives the error of every check (ceil(max_sweeps / check_every) entries at most).
+ * Returns MMF_OK when converged, MMF_ENOTCONV when the sweep cap was reached first (the state is valid;
+ * max_sweeps = 0 returns the initial state, err = +inf).  Synchronises. */
+mmf_status mmf_solve(mmf_ctx* ctx, double tol, int32_t max_sweeps, int32_t check_every, int32_t* sweeps_done,
+                     double* err_out, double* err_hist);
+
 /* End-of-sweep edge flows F_t[a] = sum over ALL commodities (all ranks), fp64, [T][n_arcs] in user
  * arc order: one extra forward pass without updates (cor:proj P:1078-1079).  Synchronises. */
 mmf_status mmf_read_edge_flows(mmf_ctx* ctx, double* out_TxA);

@@ -291,5 +291,36 @@ def stats(st: OracleState) -> dict:
         "src_mismatch": float(np.abs(P0 - p.mu0).sum()),
         "sink_mismatch": float(np.abs(PT - p.muT).sum()),
         "cap_violation": float(np.maximum(F - cap, 0.0)[np.isfinite(cap)].max(initial=0.0)),
+        "cap_excess": float(np.maximum(F - cap, 0.0)[np.isfinite(cap)].sum()),
         "sweeps": st.sweeps,
     }
+
+
+def solve_error(st: OracleState) -> float:
+    """Convergence error of the end-of-sweep state (SPEC solve, as defined in
+    include/mmf.h mmf_solve): (source + sink marginal L1 mismatch + total capacity excess) / tensor mass."""
+    s = stats(st)
+    return (s["src_mismatch"] + s["sink_mismatch"] + s["cap_excess"]) / s["mass"]
+
+
+def oracle_solve(problem, tol: float, max_sweeps: int, check_every: int = 1, schedule: str = "gs",
+                 theta: float = 1.0) -> tuple:
+    """Sweeps until solve_error < tol, checked every check_every sweeps (at most max_sweeps).
+    Returns (state, converged, sweeps, err, history)."""
+    st = oracle_init(problem)
+    done, err, hist = 0, float("inf"), []
+    while True:
+        if done > 0:
+            err = solve_error(st)
+            hist.append(err)
+            if err < tol:
+                break
+        if done >= max_sweeps:
+            break
+        for _ in range(min(check_every, max_sweeps - done)):
+            if schedule == "gs":
+                oracle_sweep(st)
+            else:
+                oracle_sweep_jacobi(st, theta)
+        done = st.sweeps
+    return st, err < tol, done, err, hist

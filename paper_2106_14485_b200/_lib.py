@@ -22,7 +22,7 @@ EXPORTS = ["mmf_create", "mmf_set_graph", "mmf_set_costs", "mmf_set_capacity", "
            "mmf_set_point_marginals", "mmf_workspace_bytes", "mmf_set_workspace", "mmf_attach_nccl", "mmf_nccl_unique_id",
            "mmf_set_option", "mmf_init", "mmf_sweep", "mmf_sync", "mmf_read_edge_flows", "mmf_read_cap_duals",
            "mmf_read_stats", "mmf_read_kernel_stats", "mmf_sweep_bytes", "mmf_destroy", "mmf_last_error",
-           "mmf_version"]
+           "mmf_version", "mmf_solve"]
 
 
 class MMFError(RuntimeError):
@@ -70,6 +70,7 @@ def load(path: str = None):
         "mmf_read_edge_flows": ([vp, dp], C.c_int),
         "mmf_read_cap_duals": ([vp, dp], C.c_int),
         "mmf_read_stats": ([vp, C.POINTER(mmf_stats)], C.c_int),
+        "mmf_solve": ([vp, C.c_double, i32, i32, C.POINTER(C.c_int32), dp, dp], C.c_int),
         "mmf_read_kernel_stats": ([vp, C.POINTER(C.c_int64), dp, C.c_int], C.c_int),
         "mmf_sweep_bytes": ([vp, dp, dp, C.c_int], C.c_int),
         "mmf_destroy": ([vp], C.c_int),
@@ -192,6 +193,19 @@ def mmf_read_cap_duals(ctx, T: int, A: int, out=None) -> np.ndarray:
     out = np.empty((T, A), np.float64) if out is None else out
     _check(ctx, load().mmf_read_cap_duals(ctx, _p(out, C.c_double)))
     return out
+
+
+def mmf_solve(ctx, tol: float, max_sweeps: int, check_every: int = 1) -> dict:
+    """Sweeps until the end-of-sweep error is below tol (MMF_ENOTCONV is reported as converged=False)."""
+    done = C.c_int32(0)
+    err = C.c_double(0.0)
+    hist = np.zeros(max(1, -(-max_sweeps // max(check_every, 1))), np.float64)
+    st = load().mmf_solve(ctx, float(tol), int(max_sweeps), int(check_every), C.byref(done), C.byref(err),
+                          hist.ctypes.data_as(C.POINTER(C.c_double)))
+    if st not in (0, 3):
+        _check(ctx, st)
+    n = -(-done.value // max(check_every, 1))
+    return {"converged": st == 0, "sweeps": done.value, "err": err.value, "history": hist[:n].copy()}
 
 
 def mmf_read_stats(ctx) -> dict:

@@ -68,6 +68,11 @@ class Solver:
     def sync(self):
         L.mmf_sync(self.ctx)
 
+    def solve(self, tol: float, max_sweeps: int, check_every: int = 1) -> dict:
+        """Sweeps until the end-of-sweep error (marginal mismatches + capacity excess, relative to the mass)
+        is below tol; returns {converged, sweeps, err, history}."""
+        return L.mmf_solve(self.ctx, tol, max_sweeps, check_every)
+
     def edge_flows(self) -> np.ndarray:
         return L.mmf_read_edge_flows(self.ctx, self.p.T, self.p.A)
 

@@ -536,4 +536,22 @@ template <class T_> __global__ void k_stats_arcs(DevPtrs p) {
   if ((threadIdx.x & 31) == 0) atomicAdd(&p.stats[5], acc);
 }
 
+// capacity excess of the readout flows: sum over capacitated (t, a) of (F_t[a] - d_t[a])_+ -> stats[6]
+// (solve-to-tolerance; the flows are already summed over all commodities / ranks)
+template <class T_> __global__ void k_stats_excess(DevPtrs p) {
+  typedef typename T_::M M;
+  View<T_> v(p);
+  const size_t n = (size_t)p.T * p.A;
+  double acc = 0;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(idx / p.A), a = (int)(idx % p.A);
+    const double d = (double)v.dcap(t)[a];
+    const double F = (double)((const M*)p.Fout)[idx];
+    if (!isinf(d) && F > d) acc += F - d;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&p.stats[6], acc);
+}
+
 }  // namespace mmf

@@ -1488,6 +1488,12 @@ template <class T_> struct Eng {
     return MMF_OK;
   }
 
+  static mmf_status excess(mmf_ctx* ctx, cudaStream_t s) {
+    LaunchScope ls(ctx, K_OTHER, s);
+    size_t n = (size_t)ctx->T * ctx->A;
+    k_stats_excess<T_><<<grid1d(n, 256), 256, 0, s>>>(ctx->dp);
+    return MMF_OK;
+  }
   static mmf_status stats(mmf_ctx* ctx, cudaStream_t s) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
@@ -2154,6 +2160,46 @@ mmf_status mmf_read_edge_flows(mmf_ctx* ctx, double* out) {
 
 mmf_status mmf_read_cap_duals(mmf_ctx* ctx, double* out) {
   return mmf::read_export(ctx, out, 1);
+}
+
+mmf_status mmf_solve(mmf_ctx* ctx, double tol, int32_t max_sweeps, int32_t check_every, int32_t* sweeps_done,
+                     double* err_out, double* err_hist) {
+  if (!ctx || !sweeps_done || !err_out) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  if (max_sweeps < 0 || check_every < 1 || !(tol >= 0)) return fail(ctx, MMF_EINVAL, "max_sweeps >= 0, check_every >= 1, tol >= 0");
+  CU(cudaSetDevice(ctx->device));
+  int done = 0, h = 0;
+  double err = INFINITY;
+  for (;;) {
+    if (done > 0) {  // error of the end-of-sweep state, reduced on the device
+      mmf_status st = dispatch(ctx, [&](auto eng) { return decltype(eng)::readout(ctx, ctx->stream); });
+      if (st != MMF_OK) return st;
+      st = dispatch(ctx, [&](auto eng) { return decltype(eng)::stats(ctx, ctx->stream); });
+      if (st != MMF_OK) return st;
+      st = dispatch(ctx, [&](auto eng) { return decltype(eng)::excess(ctx, ctx->stream); });
+      if (st != MMF_OK) return st;
+      if (ctx->comm) {  // (mass and marginal mismatches are per-rank partial sums; the flows are already global)
+        int r = nccl_api().AllReduce(ctx->dp.stats, ctx->dp.stats, 5, NCCL_FLOAT64, NCCL_SUM, ctx->comm, ctx->stream);
+        if (r != 0) return fail(ctx, MMF_ENCCL, "ncclAllReduce(stats) failed");
+      }
+      st = mmf_sync(ctx);
+      if (st != MMF_OK) return st;
+      double s[8];
+      CU(cudaMemcpy(s, ctx->dp.stats, sizeof s, cudaMemcpyDeviceToHost));
+      err = s[0] > 0 ? (s[1] + s[2] + s[6]) / s[0] : INFINITY;
+      if (err_hist) err_hist[h] = err;
+      ++h;
+      if (err < tol) break;
+    }
+    if (done >= max_sweeps) break;
+    const int n = std::min(check_every, max_sweeps - done);
+    mmf_status st = mmf_sweep(ctx, n);
+    if (st != MMF_OK) return st;
+    done += n;
+  }
+  *sweeps_done = done;
+  *err_out = err;
+  return err < tol ? MMF_OK : MMF_ENOTCONV;
 }
 
 mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {

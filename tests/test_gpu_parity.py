@@ -242,6 +242,33 @@ def test_jacobi_schedule(which, theta):
                   options=dict(schedule=1, theta_milli=theta))
 
 
+@pytest.mark.parametrize("prec,L,check", [("fp32", 1019, 1), ("fp64", 37, 1), ("fp32", 1019, 3)])
+def test_solve_to_tolerance(prec, L, check):
+    """mmf_solve (on-device marginal-mismatch and capacity-excess reductions) stops at the
+    same sweep as the oracle's solve loop (tol placed between the oracle's errors of two consecutive checks),
+    with the same state; the error history matches the oracle's."""
+    from oracle import oracle_solve
+    from paper_2106_14485_b200 import Solver
+    # (total masses chosen so that capacities bind and the error decays geometrically over the 12 sweeps)
+    p = grid_problem(8, 8, 6, L, 0.2, seed=37, cap=(0.1, 0.3), mass=np.full(L, (8.0 if L > 100 else 4.0) / L))
+    _, _, _, _, hist = oracle_solve(p, 0.0, 12, check)
+    floor = 1e-5 if prec == "fp32" else 1e-9  # (errors well above the arithmetic's own noise)
+    k = next(i for i in range(1, len(hist)) if hist[i] < 0.95 * hist[i - 1] and hist[i] > floor)
+    tol = (hist[k] * hist[k - 1]) ** 0.5
+    st, conv, sweeps, err, hist_o = oracle_solve(p, tol, 12, check)
+    assert conv
+    with Solver(p, prec=prec) as s:
+        r = s.solve(tol, 12, check)
+        F, W = s.edge_flows(), s.cap_duals()
+    assert r["converged"] and r["sweeps"] == sweeps
+    assert np.all(np.abs(r["history"] - np.array(hist_o)) <= 1e-2 * np.array(hist_o) + 0.1 * floor), (r, hist_o)
+    Fo, Wo = readout_flows(st)
+    assert max_rel_err(F, Fo, flow_floor(p)) < TOL[prec] and max_rel_err(W, Wo, W_FLOOR) < TOL[prec]
+    with Solver(p, prec=prec) as s:
+        r0 = s.solve(tol, 0, check)
+    assert not r0["converged"] and r0["sweeps"] == 0
+
+
 def test_jacobi_schedule_unsupported_paths_rejected():
     from paper_2106_14485_b200 import MMFError
     p = grid_problem(4, 4, 4, 8, 0.5, seed=36)

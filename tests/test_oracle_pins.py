@@ -434,3 +434,39 @@ def test_jacobi_theta_zero_keeps_w():
     b = oracle_run(p, 3, schedule="jacobi", theta=0.0)
     assert np.all(b.omega == 0.0)
     assert max_rel_err(np.exp(b.lam0), np.exp(a.lam0), 1e-300) < 1e-13
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-4: solve to tolerance
+
+from oracle import oracle_solve, solve_error  # noqa: E402
+
+
+def test_solve_error_equals_full_tensor_marginals_and_excess():
+    """The solve error is the literal marginal L1 mismatch + capacity excess of the full tensor."""
+    p = _micro(MICROS[4])  # (dense marginals, capacities bind)
+    st = oracle_run(p, 3)
+    M = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT))
+    F = arc_flows(p, M)
+    cap = np.broadcast_to(p.cap, F.shape)
+    ex = np.maximum(F - cap, 0.0)[np.isfinite(cap)].sum()
+    ref = (np.abs(commodity_marginal(M, 0) - p.mu0).sum() + np.abs(commodity_marginal(M, p.T) - p.muT).sum()
+           + ex) / M.sum()
+    assert abs(solve_error(st) - ref) <= 1e-12 * max(ref, 1e-300) + 1e-15
+
+
+def test_solve_converges_and_satisfies_constraints():
+    """tol = 1e-8 on a tiny capacitated instance: converged, and the brute-force tensor of the returned state
+    meets the marginals and capacities to the tolerance; max_sweeps = 0 returns the initial state, not
+    converged (SPEC solve examples)."""
+    p = grid_problem(3, 3, 4, 2, 0.5, seed=13, cap=(0.15, 0.4))
+    st, conv, k, err, hist = oracle_solve(p, 1e-8, 2000)
+    assert conv and err < 1e-8 and len(hist) == k
+    M = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT))
+    mass = M.sum()
+    assert np.abs(commodity_marginal(M, 0) - p.mu0).sum() / mass < 1e-8
+    F = arc_flows(p, M)
+    cap = np.broadcast_to(p.cap, F.shape)
+    assert np.maximum(F - cap, 0.0)[np.isfinite(cap)].sum() / mass < 1e-8
+    st0, conv0, k0, err0, hist0 = oracle_solve(p, 1e-8, 0)
+    assert not conv0 and k0 == 0 and hist0 == [] and st0.sweeps == 0
