@@ -151,6 +151,21 @@ mmf_status mmf_sync(mmf_ctx* ctx);
 mmf_status mmf_solve(mmf_ctx* ctx, double tol, int32_t max_sweeps, int32_t check_every, int32_t* sweeps_done,
                      double* err_out, double* err_hist);
 
+/* Per-commodity arc flows of step t (0 <= t < T) of the end-of-sweep state, F^l_t[a] = alpha_t[i_a,l] K_t[a]
+ * W_t[a] beta_{t+1}[j_a,l] (cor:proj P:1078 in node form), fp64, [n_arcs][l_count] in user
+ * arc order, this rank's commodities.  Recomputes the forward messages up to t.  Synchronises. */
+mmf_status mmf_read_commodity_flows(mmf_ctx* ctx, int32_t t, double* out_AxL);
+
+/* Checkpoint / resume.  The iteration state is the capacity duals W [T][n_arcs] and
+ * the sink scaling UT (this rank's commodities) of the end-of-sweep state, plus the sweep count; records,
+ * beta_t, U0 and alpha are recomputed from them on load, so a restored context continues exactly like the
+ * saved one (bitwise, with the same options).  The buffer is opaque and versioned: W in user arc order, UT in
+ * user node order, a header with the problem shape and a hash of the graph, checked by mmf_load_state
+ * (MMF_EINVAL on mismatch).  mmf_save_state / mmf_load_state synchronise; call them after mmf_init. */
+mmf_status mmf_state_bytes(const mmf_ctx* ctx, size_t* bytes);
+mmf_status mmf_save_state(mmf_ctx* ctx, void* host_buf, size_t bytes);
+mmf_status mmf_load_state(mmf_ctx* ctx, const void* host_buf, size_t bytes);
+
 /* End-of-sweep edge flows F_t[a] = sum over ALL commodities (all ranks), fp64, [T][n_arcs] in user
  * arc order: one extra forward pass without updates (cor:proj P:1078-1079).  Synchronises. */
 mmf_status mmf_read_edge_flows(mmf_ctx* ctx, double* out_TxA);

@@ -22,7 +22,8 @@ EXPORTS = ["mmf_create", "mmf_set_graph", "mmf_set_costs", "mmf_set_capacity", "
            "mmf_set_point_marginals", "mmf_workspace_bytes", "mmf_set_workspace", "mmf_attach_nccl", "mmf_nccl_unique_id",
            "mmf_set_option", "mmf_init", "mmf_sweep", "mmf_sync", "mmf_read_edge_flows", "mmf_read_cap_duals",
            "mmf_read_stats", "mmf_read_kernel_stats", "mmf_sweep_bytes", "mmf_destroy", "mmf_last_error",
-           "mmf_version", "mmf_solve"]
+           "mmf_version", "mmf_solve", "mmf_state_bytes", "mmf_save_state", "mmf_load_state",
+           "mmf_read_commodity_flows"]
 
 
 class MMFError(RuntimeError):
@@ -71,6 +72,10 @@ def load(path: str = None):
         "mmf_read_cap_duals": ([vp, dp], C.c_int),
         "mmf_read_stats": ([vp, C.POINTER(mmf_stats)], C.c_int),
         "mmf_solve": ([vp, C.c_double, i32, i32, C.POINTER(C.c_int32), dp, dp], C.c_int),
+        "mmf_state_bytes": ([vp, C.POINTER(C.c_size_t)], C.c_int),
+        "mmf_read_commodity_flows": ([vp, i32, dp], C.c_int),
+        "mmf_save_state": ([vp, vp, C.c_size_t], C.c_int),
+        "mmf_load_state": ([vp, vp, C.c_size_t], C.c_int),
         "mmf_read_kernel_stats": ([vp, C.POINTER(C.c_int64), dp, C.c_int], C.c_int),
         "mmf_sweep_bytes": ([vp, dp, dp, C.c_int], C.c_int),
         "mmf_destroy": ([vp], C.c_int),
@@ -206,6 +211,24 @@ def mmf_solve(ctx, tol: float, max_sweeps: int, check_every: int = 1) -> dict:
         _check(ctx, st)
     n = -(-done.value // max(check_every, 1))
     return {"converged": st == 0, "sweeps": done.value, "err": err.value, "history": hist[:n].copy()}
+
+
+def mmf_read_commodity_flows(ctx, t: int, A: int, L: int) -> np.ndarray:
+    out = np.empty((A, L), np.float64)
+    _check(ctx, load().mmf_read_commodity_flows(ctx, int(t), _p(out, C.c_double)))
+    return out
+
+
+def mmf_save_state(ctx) -> bytes:
+    n = C.c_size_t(0)
+    _check(ctx, load().mmf_state_bytes(ctx, C.byref(n)))
+    buf = C.create_string_buffer(n.value)
+    _check(ctx, load().mmf_save_state(ctx, buf, n))
+    return buf.raw
+
+
+def mmf_load_state(ctx, state: bytes):
+    _check(ctx, load().mmf_load_state(ctx, C.c_char_p(state), len(state)))
 
 
 def mmf_read_stats(ctx) -> dict:

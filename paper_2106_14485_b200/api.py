@@ -68,6 +68,18 @@ class Solver:
     def sync(self):
         L.mmf_sync(self.ctx)
 
+    def commodity_flows(self, t: int) -> np.ndarray:
+        """Per-commodity arc flows of step t, [A, l_count] fp64 in user arc order (this solver's commodities)."""
+        return L.mmf_read_commodity_flows(self.ctx, t, self.p.A, self.l_count)
+
+    def save_state(self) -> bytes:
+        """Checkpoint (W and UT of the end-of-sweep state; include/mmf.h mmf_save_state)."""
+        return L.mmf_save_state(self.ctx)
+
+    def load_state(self, state: bytes):
+        """Resume from a checkpoint of the same problem (any kernel options)."""
+        L.mmf_load_state(self.ctx, state)
+
     def solve(self, tol: float, max_sweeps: int, check_every: int = 1) -> dict:
         """Sweeps until the end-of-sweep error (marginal mismatches + capacity excess, relative to the mass)
         is below tol; returns {converged, sweeps, err, history}."""

@@ -536,6 +536,25 @@ template <class T_> __global__ void k_stats_arcs(DevPtrs p) {
   if ((threadIdx.x & 31) == 0) atomicAdd(&p.stats[5], acc);
 }
 
+// per-commodity arc flows of step t (cor:proj P:1078 in node form): out[a_user][l] = alpha_t[i_a, l] K_t W_t[a]
+// beta_{t+1}[j_a, l] in fp64 (alpha_t of the end-of-sweep tensor is in its slot)
+template <class T_>
+__global__ void k_commodity_flows(DevPtrs p, const int* __restrict__ ioa, int t, double* __restrict__ out) {
+  typedef typename T_::M M;
+  View<T_> v(p);
+  const int64_t n = (int64_t)p.A * p.L;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t au = k / p.L;
+    const int l = (int)(k - au * p.L);
+    const int a = ioa[au];
+    const int i = p.tail[a], j = p.out_head[p.opos[a]];
+    const size_t gi = (size_t)i * p.Lp + l, gj = (size_t)j * p.Lp + l;
+    const double m = (double)v.am(t)[gi] * (double)v.bm(t + 1)[gj] * (double)v.Km(t)[a] * (double)v.Wm(t)[a];
+    const int e = (int)v.ae(t)[gi] + (int)v.be(t + 1)[gj] + v.Ke(t)[a] + v.We(t)[a];
+    out[k] = m == 0.0 ? 0.0 : ldexp(m, e);
+  }
+}
+
 // capacity excess of the readout flows: sum over capacitated (t, a) of (F_t[a] - d_t[a])_+ -> stats[6]
 // (solve-to-tolerance; the flows are already summed over all commodities / ranks)
 template <class T_> __global__ void k_stats_excess(DevPtrs p) {

@@ -1463,6 +1463,22 @@ template <class T_> struct Eng {
     return MMF_OK;
   }
 
+  // after a state load (W and UT written): records from W, then the backward pass (as mmf_init does with W = 1)
+  static mmf_status restore(mmf_ctx* ctx, cudaStream_t s) {
+    mmf_ctx* c = ctx;
+    const DevPtrs& p = c->dp;
+    if (p.inrec) {
+      LaunchScope ls(c, K_OTHER, s);
+      size_t n = (size_t)c->T * c->A;
+      k_init_recs<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
+    }
+    if (c->opt_kernels >= 2)
+      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);
+    else
+      bwd_pass(c, s);
+    return MMF_OK;
+  }
+
   static mmf_status readout(mmf_ctx* ctx, cudaStream_t s) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
@@ -1488,6 +1504,27 @@ template <class T_> struct Eng {
     return MMF_OK;
   }
 
+  // forward messages of the end-of-sweep tensor up to step t (the readout pass's launches 0..t), then the
+  // per-commodity flows of step t into d_out ([n_arcs][L] user arc order)
+  static mmf_status commodity_flows(mmf_ctx* ctx, cudaStream_t s, int t, double* d_out) {
+    mmf_ctx* c = ctx;
+    if (c->opt_kernels >= 2) {
+      for (int k = 0; k <= t; ++k) tiled_fwd(c, s, k, 2);
+    } else {
+      const size_t n = (size_t)c->N * c->Lp;
+      CU(cudaMemcpyAsync(c->dp.am, c->dp.u0m, n * sizeof(M), cudaMemcpyDeviceToDevice, s));
+      CU(cudaMemcpyAsync(c->dp.ae, c->dp.u0e, n * sizeof(E), cudaMemcpyDeviceToDevice, s));
+      for (int k = 0; k < t; ++k) {
+        mmf_status st = fwd_step(c, s, k, 1);
+        if (st != MMF_OK) return st;
+      }
+    }
+    LaunchScope ls(c, K_OTHER, s);
+    const int64_t n = (int64_t)c->A * c->L;
+    const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 8 * 148);
+    k_commodity_flows<T_><<<grid, 256, 0, s>>>(c->dp, c->d_int_of_arc, t, d_out);
+    return MMF_OK;
+  }
   static mmf_status excess(mmf_ctx* ctx, cudaStream_t s) {
     LaunchScope ls(ctx, K_OTHER, s);
     size_t n = (size_t)ctx->T * ctx->A;
@@ -1777,6 +1814,32 @@ static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
   if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   if (e != cudaSuccess) return fail(ctx, MMF_ECUDA, std::string("readout: ") + cudaGetErrorString(e));
   return MMF_OK;
+}
+}  // namespace mmf
+
+namespace mmf {
+// ---- checkpoint / resume: W [T][A] (user arc order) and UT = beta_T [N][Lp] (user node
+// order) of the end-of-sweep state; everything else is recomputed from them on load
+struct StateHdr {
+  char magic[8];  // "MMFSTAT1"
+  int32_t prec, N, T, L, Lp, l_begin;
+  int64_t A, sweeps;
+  uint64_t graph_hash;
+};
+static uint64_t graph_hash(const mmf_ctx* c) {
+  uint64_t h = 1469598103934665603ull;
+  auto mix = [&](uint64_t x) {
+    h ^= x;
+    h *= 1099511628211ull;
+  };
+  mix((uint64_t)c->N);
+  mix((uint64_t)c->A);
+  for (int64_t a = 0; a < c->A; ++a) mix(((uint64_t)(uint32_t)c->tail[a] << 32) | (uint32_t)c->head[a]);
+  return h;
+}
+static size_t state_bytes(const mmf_ctx* c) {
+  const size_t se = c->prec == MMF_FP32 ? 2 : 4;
+  return sizeof(StateHdr) + (size_t)c->T * c->A * (c->sm() + 4) + (size_t)c->N * c->Lp * (c->sm() + se);
 }
 }  // namespace mmf
 
@@ -2200,6 +2263,126 @@ mmf_status mmf_solve(mmf_ctx* ctx, double tol, int32_t max_sweeps, int32_t check
   *sweeps_done = done;
   *err_out = err;
   return err < tol ? MMF_OK : MMF_ENOTCONV;
+}
+
+mmf_status mmf_read_commodity_flows(mmf_ctx* ctx, int32_t t, double* out) {
+  if (!ctx || !out) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  if (t < 0 || t >= ctx->T) return fail(ctx, MMF_EINVAL, "t must be in [0, T)");
+  CU(cudaSetDevice(ctx->device));
+  mmf_status st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  const int64_t A = ctx->A, n = A * ctx->L;
+  if (!ctx->d_int_of_arc) {
+    CU(cudaMalloc(&ctx->d_int_of_arc, (size_t)A * sizeof(int)));
+    CU(cudaMemcpy(ctx->d_int_of_arc, ctx->int_of_arc.data(), (size_t)A * sizeof(int), cudaMemcpyHostToDevice));
+  }
+  double* d = nullptr;
+  CU(cudaMalloc(&d, (size_t)n * sizeof(double)));
+  st = dispatch(ctx, [&](auto eng) { return decltype(eng)::commodity_flows(ctx, ctx->stream, t, d); });
+  cudaError_t e = st == MMF_OK ? cudaGetLastError() : cudaSuccess;
+  if (st == MMF_OK && e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (st == MMF_OK && e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cudaFree(d);
+  if (st != MMF_OK) return st;
+  if (e != cudaSuccess) return fail(ctx, MMF_ECUDA, std::string("commodity flows: ") + cudaGetErrorString(e));
+  return mmf_sync(ctx);
+}
+
+mmf_status mmf_state_bytes(const mmf_ctx* ctx, size_t* bytes) {
+  if (!ctx || !bytes) return MMF_EINVAL;
+  if (!ctx->inited) return MMF_ESTATE;
+  *bytes = mmf::state_bytes(ctx);
+  return MMF_OK;
+}
+
+mmf_status mmf_save_state(mmf_ctx* ctx, void* buf, size_t bytes) {
+  if (!ctx || !buf) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  if (bytes < mmf::state_bytes(ctx)) return fail(ctx, MMF_EINVAL, "state buffer too small (mmf_state_bytes)");
+  mmf_status st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  mmf::StateHdr h{};
+  memcpy(h.magic, "MMFSTAT1", 8);
+  h.prec = (int32_t)ctx->prec;
+  h.N = ctx->N;
+  h.T = ctx->T;
+  h.L = ctx->L;
+  h.Lp = ctx->Lp;
+  h.l_begin = ctx->l_begin;
+  h.A = ctx->A;
+  h.sweeps = ctx->sweeps;
+  h.graph_hash = mmf::graph_hash(ctx);
+  char* o = (char*)buf;
+  memcpy(o, &h, sizeof h);
+  o += sizeof h;
+  const size_t TA = (size_t)ctx->T * ctx->A, sm = ctx->sm(), se = ctx->prec == MMF_FP32 ? 2 : 4;
+  const size_t NL = (size_t)ctx->N * ctx->Lp;
+  std::vector<char> wm(TA * sm), bm(NL * sm), be(NL * se);
+  std::vector<int> we(TA);
+  CU(cudaMemcpy(wm.data(), ctx->dp.Wm, wm.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(we.data(), ctx->dp.We, TA * 4, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(bm.data(), (char*)ctx->dp.bm + (size_t)ctx->T * NL * sm, bm.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(be.data(), (char*)ctx->dp.be + (size_t)ctx->T * NL * se, be.size(), cudaMemcpyDeviceToHost));
+  char* owm = o;
+  char* owe = owm + TA * sm;
+  char* obm = owe + TA * 4;
+  char* obe = obm + NL * sm;
+  for (int t = 0; t < ctx->T; ++t)
+    for (int64_t a = 0; a < ctx->A; ++a) {
+      const size_t k = (size_t)t * ctx->A + ctx->int_of_arc[a], u = (size_t)t * ctx->A + a;
+      memcpy(owm + u * sm, wm.data() + k * sm, sm);
+      memcpy(owe + u * 4, &we[k], 4);
+    }
+  const size_t row_m = (size_t)ctx->Lp * sm, row_e = (size_t)ctx->Lp * se;
+  for (int v = 0; v < ctx->N; ++v) {
+    memcpy(obm + (size_t)v * row_m, bm.data() + (size_t)ctx->newid[v] * row_m, row_m);
+    memcpy(obe + (size_t)v * row_e, be.data() + (size_t)ctx->newid[v] * row_e, row_e);
+  }
+  return MMF_OK;
+}
+
+mmf_status mmf_load_state(mmf_ctx* ctx, const void* buf, size_t bytes) {
+  if (!ctx || !buf) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  if (bytes < sizeof(mmf::StateHdr)) return fail(ctx, MMF_EINVAL, "state buffer too small");
+  mmf::StateHdr h;
+  memcpy(&h, buf, sizeof h);
+  if (memcmp(h.magic, "MMFSTAT1", 8) != 0) return fail(ctx, MMF_EINVAL, "not an mmf state");
+  if (h.prec != (int32_t)ctx->prec || h.N != ctx->N || h.T != ctx->T || h.L != ctx->L || h.A != ctx->A ||
+      h.l_begin != ctx->l_begin || h.graph_hash != mmf::graph_hash(ctx))
+    return fail(ctx, MMF_EINVAL, "state was saved for another problem (graph, T, commodity slice or precision)");
+  const size_t TA = (size_t)ctx->T * ctx->A, sm = ctx->sm(), se = ctx->prec == MMF_FP32 ? 2 : 4;
+  const size_t NL = (size_t)ctx->N * ctx->Lp, NLs = (size_t)ctx->N * h.Lp;
+  if (bytes < sizeof h + TA * (sm + 4) + NLs * (sm + se)) return fail(ctx, MMF_EINVAL, "state buffer truncated");
+  mmf_status st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  const char* o = (const char*)buf + sizeof h;
+  const char* owm = o;
+  const char* owe = owm + TA * sm;
+  const char* obm = owe + TA * 4;
+  const char* obe = obm + NLs * sm;
+  std::vector<char> wm(TA * sm), bm(NL * sm, 0), be(NL * se, 0);
+  std::vector<int> we(TA);
+  for (int t = 0; t < ctx->T; ++t)
+    for (int64_t a = 0; a < ctx->A; ++a) {
+      const size_t k = (size_t)t * ctx->A + ctx->int_of_arc[a], u = (size_t)t * ctx->A + a;
+      memcpy(wm.data() + k * sm, owm + u * sm, sm);
+      memcpy(&we[k], owe + u * 4, 4);
+    }
+  const int Lc = std::min(ctx->Lp, (int)h.Lp);  // (padding may differ between kernel configurations)
+  for (int v = 0; v < ctx->N; ++v) {
+    memcpy(bm.data() + (size_t)ctx->newid[v] * ctx->Lp * sm, obm + (size_t)v * h.Lp * sm, (size_t)Lc * sm);
+    memcpy(be.data() + (size_t)ctx->newid[v] * ctx->Lp * se, obe + (size_t)v * h.Lp * se, (size_t)Lc * se);
+  }
+  CU(cudaMemcpy(ctx->dp.Wm, wm.data(), wm.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->dp.We, we.data(), TA * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy((char*)ctx->dp.bm + (size_t)ctx->T * NL * sm, bm.data(), bm.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy((char*)ctx->dp.be + (size_t)ctx->T * NL * se, be.data(), be.size(), cudaMemcpyHostToDevice));
+  st = dispatch(ctx, [&](auto eng) { return decltype(eng)::restore(ctx, ctx->stream); });
+  if (st != MMF_OK) return st;
+  ctx->sweeps = h.sweeps;
+  return mmf_sync(ctx);
 }
 
 mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {

@@ -269,6 +269,60 @@ def test_solve_to_tolerance(prec, L, check):
     assert not r0["converged"] and r0["sweeps"] == 0
 
 
+@pytest.mark.parametrize("prec,L,opts_b", [("fp32", 1019, None), ("fp64", 37, None), ("fp32", 1019, dict(kernels=3)),
+                                          ("fp32", 150, dict(cpt=1))])
+def test_checkpoint_resume(prec, L, opts_b):
+    """save after 3 sweeps, load into a fresh context, 2 more sweeps == 5 uninterrupted
+    sweeps — bitwise with the same options, within the parity tolerance across kernel configurations — and
+    equal to the oracle's 5 sweeps; a state of another problem is rejected."""
+    from paper_2106_14485_b200 import MMFError, Solver
+    p = grid_problem(9, 9, 7, L, 0.2, seed=38, cap=(0.3, 1.2))
+    with Solver(p, prec=prec) as a:
+        a.sweep(3)
+        state = a.save_state()
+        a.sweep(2)
+        Fa, Wa = a.edge_flows(), a.cap_duals()
+        sa = a.stats()
+    with Solver(p, prec=prec, options=opts_b) as b:
+        b.load_state(state)
+        b.sweep(2)
+        Fb, Wb = b.edge_flows(), b.cap_duals()
+        sb = b.stats()
+    assert sb["sweeps"] == sa["sweeps"] == 5
+    if opts_b is None:
+        assert np.array_equal(Fa, Fb) and np.array_equal(Wa, Wb)
+    else:
+        assert max_rel_err(Fb, Fa, flow_floor(p)) < TOL[prec] and max_rel_err(Wb, Wa, W_FLOOR) < TOL[prec]
+    Fo, Wo, _ = run_oracle(p, 5)
+    assert max_rel_err(Fb, Fo, flow_floor(p)) < TOL[prec] and max_rel_err(Wb, Wo, W_FLOOR) < TOL[prec]
+    q = grid_problem(9, 8, 7, L, 0.2, seed=38, cap=(0.3, 1.2))
+    with Solver(q, prec=prec) as c:
+        with pytest.raises(MMFError) as e:
+            c.load_state(state)
+        assert e.value.name == "MMF_EINVAL"
+
+
+@pytest.mark.parametrize("prec,L,opts", [("fp32", 1019, {}), ("fp64", 37, {}), ("fp32", 150, dict(kernels=1)),
+                                        ("fp32", 70, dict(kernels=6))])
+def test_commodity_flows_readout(prec, L, opts):
+    """per-commodity arc flows F^l_t of the end-of-sweep state against the oracle's
+    cor:proj readout, element by element, at the first, a middle and the last step; their commodity sum is the
+    edge-flow readout."""
+    from oracle import readout_commodity_flows
+    from paper_2106_14485_b200 import Solver
+    p = grid_problem(7, 7, 6, L, 0.2, seed=39, cap=(0.3, 1.2))
+    st = oracle_run(p, 3)
+    with Solver(p, prec=prec, options=opts) as s:
+        s.sweep(3)
+        F = s.edge_flows()
+        for t in (0, 3, p.T - 1):
+            Fl = s.commodity_flows(t)
+            ref = readout_commodity_flows(st, t)
+            assert Fl.shape == ref.shape == (p.A, p.L)
+            assert max_rel_err(Fl, ref, 1e-30 * float(p.mass.max())) < TOL[prec], t
+            assert max_rel_err(Fl.sum(axis=1), F[t], flow_floor(p)) < TOL[prec]
+
+
 def test_jacobi_schedule_unsupported_paths_rejected():
     from paper_2106_14485_b200 import MMFError
     p = grid_problem(4, 4, 4, 8, 0.5, seed=36)
