@@ -1430,6 +1430,7 @@ template <class T_> struct Eng {
   if (SW == sw && gw == g && ng == n && np == q) {                                                         \
     CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
     CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+    CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
   }
         MMF_FWD_COMBOS(MMF_FWD_COMBO)
 #undef MMF_FWD_COMBO
@@ -1483,8 +1484,15 @@ template <class T_> struct Eng {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
     if (c->opt_kernels >= 2) {
+      // (the pipelined forward in readout mode where the sweep uses it)
+      const bool pipe = sizeof(M) == 4 && c->opt_kernels >= 5 && c->pipe_fwd && !c->comm && !MMF_FWD_DEDUP;
       for (int t = 0; t <= c->T; ++t) {
-        tiled_fwd(c, s, t, 2);
+        if (pipe && t > 0) {
+          LaunchScope ls(c, K_FUSED, s);
+          pipe_fwd_mode<3>(c, s, t);  // (MODE 3: flows of every arc into Fout, no dual update)
+        } else {
+          tiled_fwd(c, s, t, 2);
+        }
         if (c->comm && t < c->T) {
           M* out = (M*)p.Fout + (size_t)t * c->A;
           int r = nccl_api().AllReduce(out, out, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,

@@ -512,6 +512,29 @@ __device__ __forceinline__ UpdView fwd_update_phase(const DevPtrs& p, const FwdH
   return v;
 }
 
+// readout mode (MODE 3): the flow of every in-arc of the item (0 for zero-factor arcs) -> Fout[t - 1][arc], by
+// warp 0; the dual update is skipped and alpha uses the current factors
+template <int GW>
+__device__ __forceinline__ void fwd_readout_store(const DevPtrs& p, const FwdHdr& h, const float (*fp)[PIPE_NWC],
+                                                  int t, int lane, int wg) {
+  if (wg != 0 || lane >= h.na) return;
+  const int row = h.rowof[lane];
+  float F = 0.f;
+  if (row >= 0)
+#pragma unroll
+    for (int w = 0; w < GW; ++w) F += fp[row][w];
+  ((float*)p.Fout)[(size_t)(t - 1) * p.A + (h.aux[lane] & 0x7fffffff)] = F;
+}
+__device__ __forceinline__ UpdView fwd_old_view(const FwdHdr& h, int lane) {
+  UpdView v;
+  v.u = FwdUpd{1.f, 0x3f800000u, 0u};
+  if (lane < h.na && h.rowof[lane] >= 0) {
+    v.u.nkb = h.kb[h.rowof[lane]];
+    v.u.nk2 = h.k2[h.rowof[lane]];
+  }
+  return v;
+}
+
 // alpha from the new factors, two passes over shared memory
 template <int CPT, class RW>
 __device__ __forceinline__ void fwd_alpha_new(const RW& rw, const FwdHdr& h, const UpdView& u, int nr, float* s,
@@ -571,7 +594,7 @@ __device__ __forceinline__ void xterms_w(const int* w, float* m, unsigned kb, un
 }
 
 // register path, N (compile-time) rows held in registers: the maximum exponent, the terms in place
-template <int CPT, int GW, int N>
+template <int CPT, int GW, int N, int MODE>
 __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, const FwdHdr& h, const ArcOps* hops,
                                          const Row<TrF32, CPT>& bown, FwdGrp& G, int par, int t, int j, int D,
                                          int lane, int wg, int bar_id, float* s, int* Ex) {
@@ -675,6 +698,19 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
     for (int c = 0; c < CPT; ++c) sp[c] += tq[q][c];
 #endif
   named_bar(bar_id, GW * 32);
+  if constexpr (MODE == 3) {  // readout: flows out, alpha with the current factors
+    fwd_readout_store<GW>(p, h, fp, t, lane, wg);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      s[c] = 0.f;
+      Ex[c] = P.E[c];
+    }
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) s[c] += tq[q][c];
+    return;
+  }
   if (p.diag == 3) {  // diagnostics (results invalid): flows and their reduction, no dual update
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
@@ -739,7 +775,7 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
 
 // any row count (more than the register path's): streaming flows, then the update, then alpha from shared
 // memory
-template <int CPT, int GW>
+template <int CPT, int GW, int MODE>
 __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& rw0, const FwdHdr& h, const ArcOps* hops,
                                              const Row<TrF32, CPT>& bown, FwdGrp& G, int par, int t, int j, int D,
                                              int lane, int wg, int bar_id, int nr, float* s, int* Ex) {
@@ -777,6 +813,11 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& r
     if (lane == 0) fp[q][wg] = f;
   }
   named_bar(bar_id, GW * 32);
+  if constexpr (MODE == 3) {
+    fwd_readout_store<GW>(p, h, fp, t, lane, wg);
+    fwd_alpha_new<CPT>(rw, h, fwd_old_view(h, lane), nr, s, Ex);
+    return;
+  }
   bool big;
   const UpdView u = fwd_update_phase<GW>(p, h, o0, hops, G, par, t, j, D, lane, wg, bar_id, &big);
   fwd_alpha_new<CPT>(rw, h, u, nr, s, Ex);
@@ -868,7 +909,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
       const bool ok = valid && r.km > M(0);
       const unsigned vbal = __ballot_sync(0xffffffffu, valid);
       const unsigned obal = __ballot_sync(0xffffffffu, ok);
-      const unsigned cbal = __ballot_sync(0xffffffffu, ok && r.aux >= 0);
+      const unsigned cbal = __ballot_sync(0xffffffffu, ok && (r.aux >= 0 || MODE == 3));  // (readout: every arc)
       const int na = __popc(vbal), nr = __popc(obal);
       while (rr.kold <= k - FWD_SDF) release();
       constexpr int OWN = MMF_FWD_OWNG ? 0 : 1;  // ring rows per item: nr (+ the own row)
@@ -959,22 +1000,22 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     M s[CPT];
     int Ex[CPT];
     switch (nr) {
-      case 0: fwd_body<CPT, GW, 0>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 1: fwd_body<CPT, GW, 1>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 2: fwd_body<CPT, GW, 2>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 3: fwd_body<CPT, GW, 3>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 4: fwd_body<CPT, GW, 4>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 5: fwd_body<CPT, GW, 5>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
-      case 6: fwd_body<CPT, GW, 6>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 0: fwd_body<CPT, GW, 0, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 1: fwd_body<CPT, GW, 1, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 2: fwd_body<CPT, GW, 2, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 3: fwd_body<CPT, GW, 3, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 4: fwd_body<CPT, GW, 4, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 5: fwd_body<CPT, GW, 5, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
+      case 6: fwd_body<CPT, GW, 6, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex); break;
       case 7:
-        if constexpr (NMAX >= 7) fwd_body<CPT, GW, 7>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex);
-        else fwd_body_any<CPT, GW>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex);
+        if constexpr (NMAX >= 7) fwd_body<CPT, GW, 7, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex);
+        else fwd_body_any<CPT, GW, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex);
         break;
       case 8:
-        if constexpr (NMAX >= 8) fwd_body<CPT, GW, 8>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex);
-        else fwd_body_any<CPT, GW>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex);
+        if constexpr (NMAX >= 8) fwd_body<CPT, GW, 8, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, s, Ex);
+        else fwd_body_any<CPT, GW, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex);
         break;
-      default: fwd_body_any<CPT, GW>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
+      default: fwd_body_any<CPT, GW, MODE>(p, rw, h, hops, bown, G, par, t, j, D, lane, wg, bar_id, nr, s, Ex); break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
