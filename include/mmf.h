@@ -119,8 +119,8 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "bwd"      backward kernel with kernels >= 5: 0 auto, 1 three-pipeline, 2 sliding window, 3 single,
  *              4 row-reuse rings (contiguous node blocks, resident rows referenced instead of reloaded)
  *   "schedule" 0 = Gauss-Seidel (Algorithm 2, default), 1 = damped Jacobi (every W_t from
- *              one alpha/beta pair, W <- W^(1-theta) min(W d / F, 1)^theta; pipelined fp32 forward only,
- *              else mmf_init returns MMF_EINVAL)
+ *              one alpha/beta pair, W <- W^(1-theta) min(W d / F, 1)^theta; one all-reduce of the T x n_arcs
+ *              flows per sweep on the multi-GPU path)
  *   "theta_milli"  Jacobi damping theta in 1/1000 (0 .. 1000, default 500)
  *   "fgw", "fng", "fnp"  pipelined forward: warps per consumer group (8, 4, 2), groups per pipeline,
  *              pipelines per CTA (0 = default; the compiled combinations are listed in pipefwd.cuh)

@@ -59,8 +59,7 @@ struct DevPtrs {
   const int* ell_opos;  // [A] internal arc -> slot in ell_out (tail * Dout + k)
   int Din, Dout;
   int diag;  // diagnostics of the pipelined forward (option "dry" >= 2; results invalid), else 0
-  int jac;      // schedule: 0 Gauss-Seidel (Algorithm 2), 1 damped Jacobi
-  float theta;  // Jacobi damping: W <- W^(1 - theta) min(W d / F, 1)^theta
+  float theta;  // Jacobi schedule damping: W <- W^(1 - theta) min(W d / F, 1)^theta
 };
 
 // per-step arc record: gathered node, arc factor K_t W_t as XF (km = 0: zero factor), aux word
@@ -534,6 +533,69 @@ template <class T_> __global__ void k_stats_arcs(DevPtrs p) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(&p.stats[5], acc);
+}
+
+// bulk-coupled (Jacobi) capacity-dual update of every step from the flows of one forward pass
+// (Fout, already summed over all commodities / ranks):  W <- W^(1 - theta) min(W d / F, 1)^theta  in fp64
+template <class T_> __global__ void k_jacobi_update(DevPtrs p) {
+  typedef typename T_::M M;
+  View<T_> v(p);
+  const size_t n = (size_t)p.T * p.A;
+  const double theta = (double)p.theta;
+  for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(idx / p.A), a = (int)(idx % p.A);
+    const M d = v.dcap(t)[a];
+    if (isinf(d)) continue;
+    M* Wm = v.Wm(t);
+    int* We = v.We(t);
+    const M wm0 = Wm[a];
+    const int we0 = We[a];
+    const double F = (double)((const M*)p.Fout)[idx];
+    M wm;
+    int we;
+    if (d == M(0)) {
+      wm = M(0);
+      we = EZERO;
+    } else if (!(F > 0.0)) {
+      wm = M(1);
+      we = 0;
+    } else {
+      double m;
+      int e;
+      const double x = (double)wm0 * ((double)d / F);
+      xf_norm<double>(x, we0, m, e);
+      if (isinf(x)) e = 0;
+      wm = (M)m;
+      if (wm >= M(2)) {
+        wm = M(1);
+        e += 1;
+      }
+      we = e;
+      if (e >= 0) {
+        wm = M(1);
+        we = 0;
+      }
+    }
+    if (theta != 1.0) {  // damping in logs: log W = (1 - theta) log W_old + theta log W_full; zero stays zero
+      if (wm0 > M(0) && wm > M(0)) {
+        const double L = (1.0 - theta) * ((double)we0 + log2((double)wm0)) + theta * ((double)we + log2((double)wm));
+        int ne = (int)floor(L);
+        M m = (M)exp2(L - (double)ne);
+        if (m >= M(2)) {
+          m *= M(0.5);
+          ++ne;
+        }
+        wm = m;
+        we = ne;
+      } else {
+        wm = M(0);
+        we = EZERO;
+      }
+    }
+    Wm[a] = wm;
+    We[a] = we;
+    if (p.inrec) write_recs<T_>(p, t, a, wm, we);
+  }
 }
 
 // per-commodity arc flows of step t (cor:proj P:1078 in node form): out[a_user][l] = alpha_t[i_a, l] K_t W_t[a]

@@ -977,7 +977,6 @@ size_t layout(mmf_ctx* c, char* base) {
     const bool ell = c->pipe_bwd;
     p.Din = ell ? c->ell_din : 0;
     p.diag = c->opt_dry >= 2 ? c->opt_dry : 0;
-    p.jac = c->opt_schedule;
     p.theta = (float)c->opt_theta_milli / 1000.f;
     p.Dout = ell ? c->pb.D : 0;
     p.ell_in = ell ? at(L.take(T * N * (size_t)p.Din * 16)) : nullptr;
@@ -1350,6 +1349,7 @@ template <class T_> struct Eng {
   }
 
   static mmf_status enqueue_sweep(mmf_ctx* c, cudaStream_t s) {
+    if (c->opt_schedule == 1) return jacobi_sweep(c, s);
     if (c->opt_kernels >= 5 && c->pipe_fwd && !c->comm) {
       for (int t = 0; t <= c->T; ++t) pipe_fwd(c, s, t);       // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
       for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
@@ -1480,7 +1480,35 @@ template <class T_> struct Eng {
     return MMF_OK;
   }
 
-  static mmf_status readout(mmf_ctx* ctx, cudaStream_t s) {
+  static mmf_status readout(mmf_ctx* ctx, cudaStream_t s) { return forward_flows(ctx, s, true); }
+
+  // Jacobi sweep: a2, one forward pass with the previous W (alpha_t and the flows F_t of
+  // every step, this rank's commodities), a4, ONE exchange of the T x |A| flows, all W_t, the backward pass
+  static mmf_status jacobi_sweep(mmf_ctx* c, cudaStream_t s) {
+    boundary(c, s, 0);  // a2
+    mmf_status st = forward_flows(c, s, false);
+    if (st != MMF_OK) return st;
+    boundary(c, s, 1);  // a4
+    if (c->comm) {
+      int r = nccl_api().AllReduce(c->dp.Fout, c->dp.Fout, (size_t)c->T * c->A,
+                                   c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64, NCCL_SUM, c->comm, s);
+      if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce(flows) failed");
+    }
+    {
+      LaunchScope ls(c, K_UPDATE, s);
+      size_t n = (size_t)c->T * c->A;
+      k_jacobi_update<T_><<<grid1d(n, 256), 256, 0, s>>>(c->dp);
+    }
+    if (c->opt_kernels >= 2)
+      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+    else
+      bwd_pass(c, s);
+    return MMF_OK;
+  }
+
+  // forward pass with the current factors (no dual update): alpha_t of the current state and the flows of every
+  // step into Fout (exchanged per step over the ranks if asked)
+  static mmf_status forward_flows(mmf_ctx* ctx, cudaStream_t s, bool exchange_each) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
     if (c->opt_kernels >= 2) {
@@ -1493,7 +1521,7 @@ template <class T_> struct Eng {
         } else {
           tiled_fwd(c, s, t, 2);
         }
-        if (c->comm && t < c->T) {
+        if (c->comm && exchange_each && t < c->T) {
           M* out = (M*)p.Fout + (size_t)t * c->A;
           int r = nccl_api().AllReduce(out, out, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
                                        NCCL_SUM, c->comm, s);
@@ -2157,10 +2185,6 @@ mmf_status mmf_init(mmf_ctx* ctx) {
   CU(cudaSetDevice(ctx->device));
   mmf_status st = finalize(ctx);
   if (st != MMF_OK) return st;
-  if (ctx->opt_schedule == 1 && !(ctx->prec == MMF_FP32 && ctx->pipe_fwd && ctx->opt_kernels >= 5 && !ctx->comm))
-    return fail(ctx, MMF_EINVAL,
-                "schedule 1 (Jacobi) runs on the pipelined fp32 forward: one slice of >= 512 commodities per node, "
-                "single GPU");
   st = dispatch(ctx, [&](auto eng) { return decltype(eng)::init_device(ctx, ctx->stream); });
   if (st != MMF_OK) return st;
   CU(cudaGetLastError());

@@ -301,22 +301,6 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
   if (!cap) {
     wm = w0;
     we = e0;
-  } else if (p.jac && p.theta != 1.f) {  // damped: log2 W = (1 - theta) log2 W_old + theta log2 W_full
-    if (w0 > 0.f && wm > 0.f) {
-      const double L = (1.0 - (double)p.theta) * ((double)e0 + (double)__log2f(w0)) +
-                       (double)p.theta * ((double)we + (double)__log2f(wm));
-      int ne = (int)floor(L);
-      float m = exp2f((float)(L - (double)ne));
-      if (m >= 2.f) {
-        m *= 0.5f;
-        ++ne;
-      }
-      wm = m;
-      we = ne;
-    } else {
-      wm = 0.f;
-      we = EZERO;
-    }
   }
   float km = o.Km * wm;
   int ke = o.Ke + we;
@@ -352,7 +336,7 @@ __device__ __forceinline__ FwdUpd fwd_update(const DevPtrs& p, const FwdHdr& h, 
     rr.node = h.rtail[lane];
     if (wg == 0) ((ArcKW<float>*)p.ell_in)[ell] = rr;
     if (wg == 0) ((ArcKW<float>*)p.inrec)[(size_t)(t - 1) * p.A + aux] = rr;
-    if (row >= 0 && !p.jac) {  // (Jacobi: alpha with the previous factors, u stays {1, old K W})
+    if (row >= 0) {
       const int de = we - e0;
       const bool ok = w0 > 0.f && wm > 0.f && de <= 40 && de >= -40;
       big = !ok;

@@ -323,12 +323,14 @@ def test_commodity_flows_readout(prec, L, opts):
             assert max_rel_err(Fl.sum(axis=1), F[t], flow_floor(p)) < TOL[prec]
 
 
-def test_jacobi_schedule_unsupported_paths_rejected():
-    from paper_2106_14485_b200 import MMFError
-    p = grid_problem(4, 4, 4, 8, 0.5, seed=36)
-    with pytest.raises(MMFError) as e:
-        run_gpu(p, 1, "fp64", options=dict(schedule=1))
-    assert e.value.name == "MMF_EINVAL"
+@pytest.mark.parametrize("prec,L,opts", [("fp64", 37, {}), ("fp32", 150, dict(kernels=3)), ("fp64", 20, dict(kernels=1)),
+                                        ("fp32", 300, dict(kernels=2)), ("fp32", 60, dict(kernels=4))])
+def test_jacobi_schedule_every_kernel_family(prec, L, opts):
+    """The Jacobi sweep (one forward pass in readout mode, one bulk update, the backward pass) on every kernel
+    family and both precisions, against the oracle."""
+    p = grid_problem(6, 7, 6, L, 0.2, seed=40, cap=(0.3, 1.2), marginals="dense" if L == 20 else "point")
+    assert_parity(p, 4, prec, oracle_kw=dict(schedule="jacobi", theta=0.5),
+                  options=dict(schedule=1, theta_milli=500, **opts))
 
 
 @pytest.mark.parametrize("wrap", [0, 1])
@@ -376,6 +378,18 @@ def test_full_config_invariants(cfg):
     p = gen(cfg)
     F, W, st = run_gpu(p, p.sweeps, "fp32")
     _invariants(p, F, W, 2e-4)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_nccl_jacobi_bulk_exchange_one_rank(prec):
+    """The Jacobi schedule's single T x |A| flow all-reduce per sweep on a one-rank NCCL
+    communicator, against the oracle's Jacobi sweep."""
+    import torch
+    torch.cuda.nccl.version()  # loads the NCCL the library resolves at run time
+    from paper_2106_14485_b200 import _lib
+    p = grid_problem(5, 6, 6, 40, 0.2, seed=41, cap=(0.3, 1.2))
+    assert_parity(p, 4, prec, oracle_kw=dict(schedule="jacobi", theta=0.5), nccl_uid=_lib.mmf_nccl_unique_id(),
+                  nranks=1, rank=0, options=dict(schedule=1, theta_milli=500))
 
 
 @pytest.mark.parametrize("prec", ["fp32", "fp64"])
