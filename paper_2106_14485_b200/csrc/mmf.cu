@@ -471,8 +471,7 @@ void derive_shapes(mmf_ctx* c) {
   // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width), NG
   // consumer groups of GW warps per pipeline (a warp owns 32 CPT = SW / GW commodities)
   c->pipe_fwd = false;
-  // (auto: for one 256-commodity slice the wide-lane forward is as fast; measured on [3])
-  if (c->pipe_bwd && c->pb.ns == 1 && c->ell_din > 0 && c->ell_din <= 32 && (c->pb.SW >= 512 || c->opt_fgw)) {
+  if (c->pipe_bwd && c->pb.ns == 1 && c->ell_din > 0 && c->ell_din <= 32) {
     const int SW = c->pb.SW;
     int gw = 8, ng = 1, np = 2;  // (the first compiled combination of this SW, unless options choose)
     bool first = true;
