@@ -1511,8 +1511,10 @@ template <class T_> struct Eng {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
     if (c->opt_kernels >= 2) {
-      // (the pipelined forward in readout mode where the sweep uses it)
-      const bool pipe = sizeof(M) == 4 && c->opt_kernels >= 5 && c->pipe_fwd && !c->comm && !MMF_FWD_DEDUP;
+      // (the pipelined forward in readout mode where it applies; its launch t yields the flows of step t - 1, so
+      // with a per-step exchange the wide-lane kernels are used)
+      const bool pipe = sizeof(M) == 4 && c->opt_kernels >= 5 && c->pipe_fwd && !(c->comm && exchange_each) &&
+                        !MMF_FWD_DEDUP;
       for (int t = 0; t <= c->T; ++t) {
         if (pipe && t > 0) {
           LaunchScope ls(c, K_FUSED, s);
