@@ -1,22 +1,27 @@
-// pipefwd.cuh — TMA-pipelined persistent forward step (option kernels = 5, fp32, one slice per node).
+// pipefwd.cuh — TMA-pipelined persistent forward step (kernels >= 5, fp32, one slice of Lp commodities per
+// node), and the three-pipeline backward (k_bwd_pipe2, at the end of the file).
 //
-// Forward kernel of step t (1 <= t <= T), one item per node j (all Lp commodities), the head-flow order of
-// headflow.cuh (Algorithm 2's Gauss-Seidel order):
+// Forward kernel of step t (1 <= t <= T), one item per node j (all Lp commodities), Algorithm 2's
+// Gauss-Seidel order:
 //   (i)   F_{t-1}[a] = K W_{t-1}[a] sum_l alpha_{t-1}[i_a,l] beta_t[j,l] for the in-arcs a -> j  (cor:proj P:1078)
 //   (ii)  W_{t-1}[a] <- min(W_{t-1}[a] d[a] / F_{t-1}[a], 1)                         (eq:sinkhorn_graph_Vineq P:861)
 //   (iii) alpha_t[j] = sum_{a -> j} alpha_{t-1}[i_a] K W_{t-1}[a] with the updated W    (eq:psi_hat P:1031-1036)
-// The producer warp stages, per item: the compacted rows alpha_{t-1}[i_a] (nonzero factor) and the node's
-// own row beta_t[j] (cp.async.bulk; contiguous ring slots) and the arc records (cp.async ring, prefetched);
-// the consumers load the dual-update operands d, W, K (and record slots) of their arcs with plain loads
-// at the start of the item, overlapped with the flow computation.
+// MODE 1: (i)-(iii); MODE 2: also a4 (t = T); MODE 3 (readout, Jacobi pass): (i) into Fout for every arc and
+// (iii) with the current factors, no update.
 //
-// Consumers (a group of 8 warps per item, 2 groups alternating items) compute the per-row terms
+// Each CTA runs NP pipelines; a pipeline is one producer warp and NG consumer groups of GW warps (default 2 x
+// (1 x 8)).  The producer stages, per item: the compacted rows alpha_{t-1}[i_a] (nonzero factor) by
+// cp.async.bulk into contiguous ring slots (items never wrap), the arc records and dual-update operands by
+// cp.async into a prefetch ring (8 items ahead), and prefetches the node's own row beta_t[j] into L2; the
+// consumers load that row from global memory at the start of the item.
+//
+// Consumers compute the per-row terms
 //   t_q[c] = alpha_q[c] K W_q 2^-E[c]     (E[c] = max_q exponent of alpha_q[c] K W_q, extended range)
 // once, in registers (the row count is a compile-time constant of the code path, switch on n).  Then
 //   flows:  F_q = sum_c t_q[c] * beta_lin[c],   beta_lin[c] = beta[j,c] 2^E[c]  (one FMA per element),
 //           reduced over the lanes by a transposed butterfly (9 shuffles for up to 8 rows) and over the
 //           group's warps in shared memory (fixed order: deterministic);
-//   update: one lane per arc applies (ii), refreshes the arc's ELL records and publishes r_q = W_new / W_old;
+//   update: one lane per arc applies (ii) branch-free, warp 0 refreshes the arc's records; r_q = W_new / W_old;
 //   alpha:  alpha_t[j,c] = 2^E[c] sum_q r_q t_q[c]   (one FMA per element)
 // — valid while every |log2 r_q| <= 40 (the dropped terms, below 2^-126 of the old maximum, stay below
 // 2^-46 of the new one); otherwise the item is recomputed from shared memory with the new factors.
@@ -25,11 +30,8 @@
 
 namespace mmf {
 
-// The forward CTA runs FWD_NP independent pipelines, each one producer warp + one consumer group of 8 warps
-// with its own share of the shared memory (row ring, descriptors, record ring): the producer's per-item
-// serial latency (~0.9 us, mostly issuing the item's ~12 TMA copies; measured with idle consumers) is what
-// limits a single pipeline.  An item's rows may wrap around its ring (consumers resolve the wrap per row),
-// so a ring needs only D + 1 slots.
+// Pipelines have their own share of the shared memory (row ring, descriptors, record ring): one producer warp
+// per SM cannot feed the consumers (its per-item issue of the TMA copies is serial), two can.
 constexpr int FWD_NP = 2;  // (pipelines per CTA of the backward's structure)
 constexpr int FWD_PW = PIPE_NWC + 1;  // warps per pipeline of the backward (8 consumers + producer)
 constexpr int FWD_SD = 8;             // item descriptors per pipeline of the backward (power of two)
