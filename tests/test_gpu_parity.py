@@ -232,6 +232,16 @@ def test_pipelined_hub_and_empty_items(L, nhub, opts):
     assert_parity(_hub_problem(L, nhub), 3, "fp32", options=opts)
 
 
+@pytest.mark.parametrize("L", [1019, 251])
+def test_pipelined_forward_large_ratio_recompute(L):
+    """Arcs with capacities 1e-14 of the flow they would carry: the first dual updates move W by more than 2^40,
+    so the pipelined forward takes its recompute-from-shared-memory path for those items."""
+    p = grid_problem(10, 10, 6, L, 0.2, seed=42, cap=(0.3, 1.2))
+    moving = np.flatnonzero(p.tail != p.head)
+    p.cap[moving[::7]] = 1e-14
+    assert_parity(p, 3, "fp32")
+
+
 @pytest.mark.parametrize("theta", [500, 1000, 200])
 @pytest.mark.parametrize("which", ["grid", "hub"])
 def test_jacobi_schedule(which, theta):
