@@ -232,6 +232,16 @@ def test_pipelined_hub_and_empty_items(L, nhub, opts):
     assert_parity(_hub_problem(L, nhub), 3, "fp32", options=opts)
 
 
+@pytest.mark.parametrize("L,marg,tv", [(1019, "dense", False), (1019, "point", True), (509, "dense", True),
+                                       (251, "point", True)])
+def test_pipelined_time_varying_and_dense(L, marg, tv):
+    """The production (pipelined) path with per-step costs and capacities ([T][A] K, d: per-step records and
+    dual-update operands), closed arcs, and dense marginals (a2 / a4 over every node)."""
+    p = grid_problem(9, 9, 6, L, 0.2, seed=43, cap=(0.3, 1.2), marginals=marg, time_varying=tv,
+                     closed_arcs=4 if marg == "dense" else 0)  # (closing arcs could cut a point OD pair's only path)
+    assert_parity(p, 3, "fp32")
+
+
 @pytest.mark.parametrize("L", [1019, 251])
 def test_pipelined_forward_large_ratio_recompute(L):
     """Arcs with capacities 1e-14 of the flow they would carry: the first dual updates move W by more than 2^40,
