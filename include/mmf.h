@@ -125,7 +125,9 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "fgw", "fng", "fnp"  pipelined forward: warps per consumer group (8, 4, 2), groups per pipeline,
  *              pipelines per CTA (0 = default; the compiled combinations are listed in pipefwd.cuh)
  *   "wintma"   window backward row blocks by 2-D tensor TMA (1) or cp.async (0)
- *   "order"    node order (kernels >= 2): 0 input, 1 reverse Cuthill-McKee, 2 BFS tiles (default)
+ *   "order"    node order: kernels 2..5: 0 input, 1 reverse Cuthill-McKee, 2 BFS tiles (default); kernels 6:
+ *              1 RCM, 3 the window kernel's cost model (used with bwd=2), other values: most neighbour overlap
+ *              between consecutive nodes (default)
  *   "cpt"      commodities per thread 0 (auto), 1, 2, 4, 8
  *   "tile", "halo", "cpc"  tile sizes of the kernels = 2 family
  *   "dry", "copy"  profiling modes of the pipelined kernels (results invalid; never in production) */

@@ -100,7 +100,8 @@ struct mmf_ctx {
   int opt_cpt = 0;      // commodities per lane (0 = auto: 2 for fp32, 1 for fp64)
   int opt_halo = 0;     // max in-/out-halo nodes per tile (0 = auto: 2 * tile)
   int opt_cpc = 0;      // commodity chunks per CTA (0 = auto)
-  int opt_order = 2;    // node order (kernels >= 2): 0 input order, 1 reverse Cuthill-McKee, 2 BFS tiles
+  int opt_order = 2;    // node order: kernels 2-5: 0 input order, 1 reverse Cuthill-McKee, 2 BFS tiles; kernels 6:
+                        // 1 RCM, 3 window cost model, else most neighbour overlap (choose_reuse_order)
   int opt_prefetch = 0; // wide kernels: L1 prefetch of significand rows in pass 1
   int opt_dry = 0;      // diagnostics: pipelined backward consumers skip the arithmetic
   int opt_copy = 0;     // pipelined kernels' row staging: 0 = TMA bulk copies, 1 = per-lane cp.async
@@ -792,8 +793,18 @@ void prepare(mmf_ctx* c) {
   std::vector<int> order;
   const int B = c->opt_kernels >= 2 ? c->opt_tile : std::max(N, 1);
   if (c->opt_kernels == 6 && c->opt_reorder) {
-    if (c->opt_bwd == 4) choose_reuse_order(c);  // (row-reuse backward: neighbour overlap of consecutive nodes)
-    else choose_window_order(c);
+    // node order: the window kernel's cost model for the window backward (bwd=2), plain RCM on request
+    // (order=1), else the order with the most neighbour overlap between consecutive nodes (measured best for
+    // the pipelined kernels: [4] 85.4 vs 87.1 ms per sweep with the window order, 94.8 with RCM)
+    if (c->opt_bwd == 2 || c->opt_order == 3) {
+      choose_window_order(c);
+    } else if (c->opt_order == 1) {
+      c->newid = rcm_newid(N, c->tail, c->head);
+      c->win_Wb = 0;
+      c->win_cpt = 4;
+    } else {
+      choose_reuse_order(c);
+    }
     c->h_tile_ptr.assign(1, 0);
     for (int v = B; v < N; v += B) c->h_tile_ptr.push_back(v);
     c->h_tile_ptr.push_back(N);
@@ -1979,7 +1990,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_tile = (int)value;
     }
     if (k == "order") {
-      if (value < 0 || value > 2) return fail(ctx, MMF_EINVAL, "order must be 0, 1 or 2");
+      if (value < 0 || value > 4) return fail(ctx, MMF_EINVAL, "order must be in [0, 4]");
       ctx->opt_order = (int)value;
     }
     if (k == "cpc") {
