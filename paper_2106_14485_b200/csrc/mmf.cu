@@ -108,6 +108,7 @@ struct mmf_ctx {
   int opt_wintma = 1;   // window kernels: 1 = 2-D TMA row-block loads, 0 = per-thread cp.async
   int opt_schedule = 0;      // 0 Gauss-Seidel (Algorithm 2), 1 damped Jacobi
   int opt_theta_milli = 500;  // Jacobi damping theta in 1/1000
+  int opt_stripw = 0;   // (experiments) restrict the neighbour-overlap order's strip candidates to this width
   int opt_wrap = -1;    // k_bwd_pipe2 ring wrap: -1 auto, 0 items never wrap, 1 items may wrap
   int opt_fgw = 0;      // pipelined forward: warps per consumer group (0 auto, 8, 4, 2)
   int opt_fng = 0;      // pipelined forward: consumer groups per pipeline (0 auto, 1 .. 6)
@@ -611,11 +612,11 @@ void choose_reuse_order(mmf_ctx* c) {
     std::nth_element(d.begin(), d.begin() + (size_t)(0.90 * (d.size() - 1)), d.end());
     const int b90 = d[(size_t)(0.90 * (d.size() - 1))];
     for (int w : {2, 4, 8, 16, 32})
-      if (b90 > 2 * w) cands.push_back(strip_newid(cands[base], b90, w));
+      if (b90 > 2 * w && (!c->opt_stripw || c->opt_stripw == w)) cands.push_back(strip_newid(cands[base], b90, w));
   }
   double best = -1.0;
   size_t bi = 0;
-  for (size_t ci = 0; ci < cands.size(); ++ci) {
+  for (size_t ci = (c->opt_stripw && cands.size() > 2) ? 2 : 0; ci < cands.size(); ++ci) {
     const double f = reuse_frac(c, cands[ci], true) + reuse_frac(c, cands[ci], false);
     if (getenv("MMF_VERBOSE")) fprintf(stderr, "[mmf] reuse order cand %zu: %.3f\n", ci, 0.5 * f);
     if (f > best + 1e-9) {
@@ -1950,7 +1951,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -1972,6 +1973,10 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     if (k == "theta_milli") {
       if (value < 0 || value > 1000) return fail(ctx, MMF_EINVAL, "theta_milli must be in [0, 1000]");
       ctx->opt_theta_milli = (int)value;
+    }
+    if (k == "stripw") {
+      if (value < 0 || value > 64) return fail(ctx, MMF_EINVAL, "stripw must be in [0, 64]");
+      ctx->opt_stripw = (int)value;
     }
     if (k == "wrap") {
       if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "wrap must be -1, 0 or 1");
