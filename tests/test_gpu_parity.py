@@ -142,7 +142,9 @@ def test_validation_errors():
                                        ("fp64", dict(tile=128)), ("fp32", dict(reorder=0)),
                                        ("fp32", dict(kernels=3)), ("fp64", dict(kernels=3)),
                                        ("fp32", dict(kernels=3, cpt=8)), ("fp32", dict(kernels=4, cpt=8)),
-                                       ("fp32", dict(kernels=6)), ("fp64", dict(kernels=6))])
+                                       ("fp32", dict(kernels=6)), ("fp64", dict(kernels=6)),
+                                       ("fp32", dict(order=1)), ("fp32", dict(order=3)), ("fp32", dict(stripw=4)),
+                                       ("fp32", dict(bwd=2, wintma=0)), ("fp32", dict(bwd=3))])
 def test_kernel_variants(prec, opts):
     """Every kernel configuration (reference per-node kernels, lane widths, tile sizes, no reordering)
     meets the same parity bar; several tiles, several chunks and a ragged commodity tail."""
