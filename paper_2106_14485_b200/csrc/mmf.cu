@@ -794,10 +794,12 @@ void prepare(mmf_ctx* c) {
   std::vector<int> order;
   const int B = c->opt_kernels >= 2 ? c->opt_tile : std::max(N, 1);
   if (c->opt_kernels == 6 && c->opt_reorder) {
-    // node order: the window kernel's cost model for the window backward (bwd=2), plain RCM on request
-    // (order=1), else the order with the most neighbour overlap between consecutive nodes (measured best for
-    // the pipelined kernels: [4] 85.4 vs 87.1 ms per sweep with the window order, 94.8 with RCM)
-    if (c->opt_bwd == 2 || c->opt_order == 3) {
+    // node order: the window kernel's cost model for the window backward (bwd=2) and for the other kernel
+    // families (measured better for them on [2]), plain RCM on request (order=1), else the order with the most
+    // neighbour overlap between consecutive nodes (measured best for the pipelined kernels: [4] 85.4 vs 87.1
+    // ms per sweep with the window order, 94.8 with RCM)
+    const bool pipelined = c->prec == MMF_FP32 && c->L >= 256;  // (where the pipelined kernels apply)
+    if (c->opt_bwd == 2 || c->opt_order == 3 || (!pipelined && c->opt_order != 4 && c->opt_order != 1)) {
       choose_window_order(c);
     } else if (c->opt_order == 1) {
       c->newid = rcm_newid(N, c->tail, c->head);

@@ -14,9 +14,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-fi
     python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e > gpurun_out/b_ncu.log 2>&1; echo "ncu launches rc=$?"
 python tools/launch_summary.py /tmp/launches.csv > gpurun_out/launches_final.txt 2>&1
 python tools/prof.py --config 4 --sweeps 1 > gpurun_out/plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_fwd_pipe -s 230 -c 1 -o /tmp/ncu_fwd \
+ncu --set full --clock-control none --import-source on -f -k regex:k_fwd_pipe -s 230 -c 1 -o /tmp/ncu_fwd \
     python tools/prof.py --config 4 --sweeps 1 > gpurun_out/ncu_pfwd.log 2>&1; echo "ncu fwd rc=$?"
 python tools/ncu_summary.py /tmp/ncu_fwd.ncu-rep > gpurun_out/ncu_fwd_cfg4_final.txt 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_bwd_pipe2 -s 230 -c 1 -o /tmp/ncu_bwd \
+ncu --set full --clock-control none --import-source on -f -k regex:k_bwd_pipe2 -s 230 -c 1 -o /tmp/ncu_bwd \
     python tools/prof.py --config 4 --sweeps 1 > gpurun_out/ncu_pbwd.log 2>&1; echo "ncu bwd rc=$?"
 python tools/ncu_summary.py /tmp/ncu_bwd.ncu-rep > gpurun_out/ncu_bwd_cfg4_final.txt 2>&1
