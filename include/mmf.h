@@ -130,7 +130,10 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *              between consecutive nodes (default)
  *   "cpt"      commodities per thread 0 (auto), 1, 2, 4, 8
  *   "tile", "halo", "cpc"  tile sizes of the kernels = 2 family
- *   "dry", "copy"  profiling modes of the pipelined kernels (results invalid; never in production) */
+ *   "wrap"     three-pipeline backward: -1 auto, 0 items never wrap around the ring, 1 items may wrap
+ *   "stripw"   (experiments) strip width of the neighbour-overlap node order (0 = chosen by its score)
+ *   "dry", "copy"  profiling / diagnostic modes of the pipelined kernels (dry 1: producers only, 2: no flows,
+ *              3: no dual update; results invalid; never in production) */
 mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);
 
 /* W = 1, UT = 1 on supp(muT), one backward pass (Alg. 2 "Initialize").  Async. */
