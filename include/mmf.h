@@ -77,15 +77,20 @@ mmf_status mmf_set_graph(mmf_ctx* ctx, int32_t N, int64_t n_arcs, const int32_t*
  * 1: cost is [T][n_arcs] (per-step topology/cost).  K = exp(-C/eps) is formed in fp64. */
 mmf_status mmf_set_costs(mmf_ctx* ctx, int32_t T, double eps, const double* cost, int time_varying);
 
-/* Capacities d_t[a] >= 0, +INFINITY = uncapacitated, 0 = closed; layout as for costs. */
+/* Capacities d_t[a] >= 0 of the bimarginal inequality constraints sum_l P_{t,t+1}(M^l) <= d_t (eq:omt_multi_graph_reg
+ * P:763-770 with V_<=; eq:multicommodity P:659-661): +INFINITY = uncapacitated (W = 1), 0 = closed (W = 0);
+ * layout as for costs.  NaN or negative -> MMF_EINVAL; before mmf_set_costs -> MMF_ESTATE. */
 mmf_status mmf_set_capacity(mmf_ctx* ctx, const double* cap, int time_varying);
 
-/* Dense source / sink distributions of commodities [l_begin, l_begin + l_count) of L_global:
- * mu0, muT are [l_count][N] row-major, >= 0, with equal per-commodity masses (rel. 1e-12). */
+/* Dense source / sink distributions R^(0,1), R^(0,T) of commodities [l_begin, l_begin + l_count) of L_global
+ * (the commodity-mode marginals of eq:multicommodity P:609-612, node form SURVEY 8.0): mu0, muT are [l_count][N]
+ * row-major, finite, >= 0, with equal per-commodity masses (rel. 1e-12); else MMF_EINVAL.  A rank of
+ * a sharded run passes only its own slice (rem:multi_tensor_scheme P:1139-1147). */
 mmf_status mmf_set_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count,
                              const double* mu0, const double* muT);
 
-/* Point-mass commodities: commodity l moves mass[l] > 0 from node src[l] to node dst[l]. */
+/* Point-mass commodities (the OD pairs of P:1168-1173): commodity l moves mass[l] > 0 (finite) from
+ * node src[l] to node dst[l] (ids in [0, N), else MMF_EINVAL); same slicing as mmf_set_marginals. */
 mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count,
                                    const int32_t* src, const int32_t* dst, const double* mass);
 
@@ -96,7 +101,8 @@ mmf_status mmf_workspace_bytes(const mmf_ctx* ctx, size_t* bytes);
  * mmf_init allocates an owned workspace with cudaMalloc. */
 mmf_status mmf_set_workspace(mmf_ctx* ctx, void* dptr, size_t bytes);
 
-/* Multi-GPU commodity sharding: join an NCCL communicator of `nranks` ranks from a 128-byte
+/* Multi-GPU commodity sharding (rem:multi_tensor_scheme P:1139-1147: the commodities couple only through the
+ * shared capacity duals, i.e. through the aggregate flows F_t = sum_l F^l_t): join an NCCL communicator of `nranks` ranks from a 128-byte
  * ncclUniqueId (bootstrapped by the caller, e.g. torch.distributed).  Every rank must then make the
  * same calls with identical graph / cost / capacity arrays and its own commodity slice; the
  * per-step edge flows F_t are all-reduced (sum) over NVLink before the capacity-dual update.
@@ -161,12 +167,14 @@ mmf_status mmf_solve(mmf_ctx* ctx, double tol, int32_t max_sweeps, int32_t check
  * arc order, this rank's commodities.  Recomputes the forward messages up to t.  Synchronises. */
 mmf_status mmf_read_commodity_flows(mmf_ctx* ctx, int32_t t, double* out_AxL);
 
-/* Checkpoint / resume.  The iteration state is the capacity duals W [T][n_arcs] and
- * the sink scaling UT (this rank's commodities) of the end-of-sweep state, plus the sweep count; records,
- * beta_t, U0 and alpha are recomputed from them on load, so a restored context continues exactly like the
- * saved one (bitwise, with the same options).  The buffer is opaque and versioned: W in user arc order, UT in
- * user node order, a header with the problem shape and a hash of the graph, checked by mmf_load_state
- * (MMF_EINVAL on mismatch).  mmf_save_state / mmf_load_state synchronise; call them after mmf_init. */
+/* Checkpoint / resume.  The iteration state is the capacity duals W [T][n_arcs], the sink
+ * scaling UT and the last source scaling U0 (this rank's commodities) of the end-of-sweep state, plus the sweep
+ * count; records and beta_t are recomputed on load (the next sweep's a2 recomputes U0 from them), so a restored
+ * context reads out and continues exactly like the saved one (bitwise, with the same options).  The buffer is
+ * opaque and versioned ("MMFSTAT2"): W in user arc order, UT and U0 in user node order, a header with the problem
+ * shape, a hash of the graph and a hash of T, eps, costs and capacities, checked by mmf_load_state (MMF_EINVAL on
+ * mismatch or a corrupt header).  mmf_save_state / mmf_load_state synchronise; call them after mmf_init.
+ * Before the first sweep U0 = 0 (Alg. 2 computes U0 first), so readouts then return zero flows. */
 mmf_status mmf_state_bytes(const mmf_ctx* ctx, size_t* bytes);
 mmf_status mmf_save_state(mmf_ctx* ctx, void* host_buf, size_t bytes);
 mmf_status mmf_load_state(mmf_ctx* ctx, const void* host_buf, size_t bytes);
@@ -175,7 +183,8 @@ mmf_status mmf_load_state(mmf_ctx* ctx, const void* host_buf, size_t bytes);
  * arc order: one extra forward pass without updates (cor:proj P:1078-1079).  Synchronises. */
 mmf_status mmf_read_edge_flows(mmf_ctx* ctx, double* out_TxA);
 
-/* Capacity duals W_t[a] in [0, 1], fp64, [T][n_arcs] user arc order (values below 2^-1074 read 0). */
+/* Capacity duals W_t[a] = u_t = exp(-lambda_t/eps) in [0, 1] (thm:solution P:777-788, the V_<= scalings updated by
+ * eq:sinkhorn_graph_Vineq P:861), fp64, [T][n_arcs] user arc order (values below 2^-1074 read 0).  Synchronises. */
 mmf_status mmf_read_cap_duals(mmf_ctx* ctx, double* out_TxA);
 
 /* Statistics of the end-of-sweep state (see mmf_stats).  Synchronises. */

@@ -102,11 +102,33 @@ class OracleState:
     in_seg: tuple        # arcs grouped by head (forward recursion)
     out_seg: tuple       # arcs grouped by tail (backward recursion)
     sweeps: int = 0
+    keep_forward: bool = True   # False: ``a`` holds only the two latest layers (see _TwoLayers)
 
 
-def oracle_init(problem) -> OracleState:
+class _TwoLayers:
+    """Storage-only variant of the forward-message store ``a`` for instances whose [T+1, L, N] float64
+    arrays do not fit in host memory (configs [4], [5] at full size): the sweep reads a_t and writes
+    a_{t+1} only, so two layers suffice; layer t lives in slot t % 2.  Readouts recompute the kept
+    layers (``forward_layers``) with the same arithmetic.  No step of the method changes."""
+
+    def __init__(self, L: int, N: int):
+        self.buf = np.full((2, L, N), NEG_INF)
+
+    def __getitem__(self, t):
+        return self.buf[t % 2]
+
+    def __setitem__(self, t, v):
+        self.buf[t % 2] = v
+
+
+def oracle_init(problem, b_store: Optional[np.ndarray] = None, keep_forward: bool = True) -> OracleState:
     """Step 1-2 of SURVEY §8(c): lK = -C/eps (fp64), W = 1, UT = 1 on supp(muT) (Q7),
-    then one backward pass (Alg. 2 "Initialize ... Compute Psi_t")."""
+    then one backward pass (Alg. 2 "Initialize ... Compute Psi_t").
+
+    Storage options (no effect on any value; pinned bitwise by tests/test_oracle_pins.py
+    test_storage_options_bitwise_equal): ``b_store`` a caller-provided float64 [T+1, L, N] array for the
+    backward messages (e.g. an np.memmap on disk: [4]'s store is 66 GB); ``keep_forward=False`` keeps
+    only two forward layers and recomputes the others for readouts."""
     p = problem
     T, A, N, L = p.T, p.A, p.N, p.L
     cost = np.broadcast_to(p.cost, (T, A)) if p.cost.ndim == 1 else p.cost
@@ -115,12 +137,20 @@ def oracle_init(problem) -> OracleState:
     logd = _log(np.asarray(cap, np.float64))
     mu0 = p.mu0
     muT = p.muT
+    if b_store is None:
+        b = np.full((T + 1, L, N), NEG_INF)
+    else:
+        assert b_store.shape == (T + 1, L, N) and b_store.dtype == np.float64
+        b = b_store
+        for t in range(T + 1):
+            b[t] = NEG_INF
     st = OracleState(
         problem=p, lK=lK, logd=logd, omega=np.zeros((T, A)),
         lam0=np.full((L, N), NEG_INF), lamT=np.where(muT > 0, 0.0, NEG_INF),
-        a=np.full((T + 1, L, N), NEG_INF), b=np.full((T + 1, L, N), NEG_INF),
+        a=np.full((T + 1, L, N), NEG_INF) if keep_forward else _TwoLayers(L, N), b=b,
         log_mu0=_log(mu0), log_muT=_log(muT),
-        in_seg=_segments(p.head.astype(np.int64), N), out_seg=_segments(p.tail.astype(np.int64), N))
+        in_seg=_segments(p.head.astype(np.int64), N), out_seg=_segments(p.tail.astype(np.int64), N),
+        keep_forward=keep_forward)
     backward(st)
     return st
 
@@ -230,6 +260,7 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     # readouts (edge flows, mass) are projections of the end-of-sweep tensor M(U0, W, UT): keep the forward
     # messages of that tensor, i.e. recomputed with the new W (under Gauss-Seidel the pass's own messages
     # already are; DESIGN.md §2 reading R-J)
+    st.a[0] = st.lam0          # (unchanged in the kept store; the two-layer store has overwritten slot 0)
     for t in range(p.T):
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
         st.a[t + 1] = seg_lse(Y, st.in_seg)
@@ -247,24 +278,55 @@ def oracle_run(problem, sweeps: int, schedule: str = "gs", theta: float = 1.0) -
     return st
 
 
+def forward_layers(st: OracleState, t_stop: Optional[int] = None):
+    """Yields (t, a_t) for t = 0..t_stop (default T): the forward messages of the end-of-sweep tensor.
+    Kept store: the last pass's own layers.  Two-layer store: recomputed from (lam0, omega) by the
+    forward recursion a_{t+1} = LSE_{a -> j}(a_t[i_a] + lK_t[a] + omega_t[a]) (eq:psi_hat P:1031-1036),
+    the sweep's own expression on the same operands (under Gauss-Seidel omega_t is final once alpha_{t+1}
+    is formed; under Jacobi the sweep recomputes them with the new omega, reading R-J), hence bitwise
+    the same layers."""
+    p = st.problem
+    t_stop = p.T if t_stop is None else t_stop
+    if st.keep_forward:
+        for t in range(t_stop + 1):
+            yield t, st.a[t]
+        return
+    cur = st.lam0                       # a_0 = lam0 (all -inf before the first sweep)
+    oi = st.in_seg[0]
+    tail_i = p.tail[oi]
+    for t in range(t_stop + 1):
+        yield t, cur
+        if t < t_stop:
+            Y = cur[:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
+            cur = seg_lse(Y, st.in_seg)
+
+
+def _commodity_flows_at(st: OracleState, t: int, a_t: np.ndarray) -> np.ndarray:
+    p = st.problem
+    return np.exp(a_t[:, p.tail] + (st.lK[t] + st.omega[t])[None, :] + st.b[t + 1][:, p.head]).T
+
+
 def readout_commodity_flows(st: OracleState, t: int) -> np.ndarray:
     """Per-commodity arc flow F^l_t[a] = alpha_t[i_a,l] K_t[a] W_t[a] beta_{t+1}[j_a,l]
     (cor:proj P:1078 in node form), from the kept forward messages and the latest backward pass."""
-    p = st.problem
-    return np.exp(st.a[t][:, p.tail] + (st.lK[t] + st.omega[t])[None, :] + st.b[t + 1][:, p.head]).T
+    if st.keep_forward:
+        return _commodity_flows_at(st, t, st.a[t])
+    for tt, a_t in forward_layers(st, t):
+        if tt == t:
+            return _commodity_flows_at(st, t, a_t)
 
 
 def readout_flows(st: OracleState) -> tuple:
     """(F [T, A], W [T, A]) : aggregate edge flows F_t[a] = sum_l F^l_t[a] and capacity duals."""
     p = st.problem
-    F = np.stack([readout_commodity_flows(st, t).sum(axis=1) for t in range(p.T)])
+    F = np.stack([_commodity_flows_at(st, t, a_t).sum(axis=1)
+                  for t, a_t in forward_layers(st, p.T - 1)]) if p.T else np.zeros((0, p.A))
     return F, np.exp(st.omega)
 
 
-def dual_objective(st: OracleState, mass: float) -> float:
-    """Dual objective of thm:solution (eq:omt_multi_graph_dual P:786-788) in node form with
-    U = exp(-Lambda/eps):  Phi = -eps*mass + eps*[sum mu0*lam0 + sum muT*lamT + sum d*omega],
-    with 0 * (+-inf) = 0 (P:109)."""
+def dual_terms(st: OracleState) -> tuple:
+    """The three linear terms of the dual objective (eq:omt_multi_graph_dual P:786-788, node form,
+    lambda = -eps log u): (sum mu0*lam0, sum muT*lamT, sum d*omega), with 0 * (+-inf) = 0."""
     p = st.problem
     mu0, muT = p.mu0, p.muT
     cap = np.broadcast_to(p.cap, st.omega.shape)
@@ -272,7 +334,15 @@ def dual_objective(st: OracleState, mass: float) -> float:
     sT = np.where(muT > 0, muT * np.where(np.isfinite(st.lamT), st.lamT, 0.0), 0.0).sum()
     fin = np.isfinite(cap) & (cap > 0)
     sd = (np.where(fin, cap, 0.0) * np.where(fin, st.omega, 0.0)).sum()
-    return float(p.eps * (-mass + s0 + sT + sd))
+    return s0, sT, sd
+
+
+def dual_objective(st: OracleState, mass: float) -> float:
+    """Dual objective of thm:solution (eq:omt_multi_graph_dual P:786-788) in node form with
+    U = exp(-Lambda/eps):  Phi = -eps*mass + eps*[sum mu0*lam0 + sum muT*lamT + sum d*omega],
+    with 0 * (+-inf) = 0 (P:109)."""
+    s0, sT, sd = dual_terms(st)
+    return float(st.problem.eps * (-mass + s0 + sT + sd))
 
 
 def stats(st: OracleState) -> dict:

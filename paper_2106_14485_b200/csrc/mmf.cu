@@ -1456,6 +1456,8 @@ template <class T_> struct Eng {
       size_t n = (size_t)c->T * c->A;
       k_init_w<T_><<<grid1d(n, 256), 256, 0, s>>>(p);
     }
+    // U0 = 0 until the first a2 (the oracle's lam0 = -inf): a readout before any sweep sees the zero tensor
+    zero_slot(c, s, p.u0m, p.u0e);
     if (p.inrec) {
       LaunchScope ls(c, K_OTHER, s);
       size_t n = (size_t)c->T * c->A;
@@ -1872,25 +1874,46 @@ namespace mmf {
 // ---- checkpoint / resume: W [T][A] (user arc order) and UT = beta_T [N][Lp] (user node
 // order) of the end-of-sweep state; everything else is recomputed from them on load
 struct StateHdr {
-  char magic[8];  // "MMFSTAT1"
+  char magic[8];  // "MMFSTAT2"
   int32_t prec, N, T, L, Lp, l_begin;
   int64_t A, sweeps;
-  uint64_t graph_hash;
+  uint64_t graph_hash;    // N, A, arcs
+  uint64_t problem_hash;  // T, eps, costs, capacities (bit patterns)
 };
-static uint64_t graph_hash(const mmf_ctx* c) {
+struct Fnv {
   uint64_t h = 1469598103934665603ull;
-  auto mix = [&](uint64_t x) {
+  void mix(uint64_t x) {
     h ^= x;
     h *= 1099511628211ull;
-  };
-  mix((uint64_t)c->N);
-  mix((uint64_t)c->A);
-  for (int64_t a = 0; a < c->A; ++a) mix(((uint64_t)(uint32_t)c->tail[a] << 32) | (uint32_t)c->head[a]);
-  return h;
+  }
+  void mixd(double d) {
+    uint64_t u;
+    memcpy(&u, &d, 8);
+    mix(u);
+  }
+};
+static uint64_t graph_hash(const mmf_ctx* c) {
+  Fnv f;
+  f.mix((uint64_t)c->N);
+  f.mix((uint64_t)c->A);
+  for (int64_t a = 0; a < c->A; ++a) f.mix(((uint64_t)(uint32_t)c->tail[a] << 32) | (uint32_t)c->head[a]);
+  return f.h;
 }
+static uint64_t problem_hash(const mmf_ctx* c) {
+  Fnv f;
+  f.mix((uint64_t)c->T);
+  f.mixd(c->eps);
+  f.mix((uint64_t)c->cost_tv);
+  for (double x : c->cost) f.mixd(x);
+  f.mix((uint64_t)c->cap_tv);
+  for (double x : c->cap) f.mixd(x);
+  return f.h;
+}
+// W [T][A] (user arc order), then UT = beta_T and U0 (the last a2's source scaling; readouts before the next sweep
+// start from it), each [N][Lp] significand + exponent planes in user node order
 static size_t state_bytes(const mmf_ctx* c) {
   const size_t se = c->prec == MMF_FP32 ? 2 : 4;
-  return sizeof(StateHdr) + (size_t)c->T * c->A * (c->sm() + 4) + (size_t)c->N * c->Lp * (c->sm() + se);
+  return sizeof(StateHdr) + (size_t)c->T * c->A * (c->sm() + 4) + 2 * (size_t)c->N * c->Lp * (c->sm() + se);
 }
 }  // namespace mmf
 
@@ -2354,7 +2377,7 @@ mmf_status mmf_save_state(mmf_ctx* ctx, void* buf, size_t bytes) {
   mmf_status st = mmf_sync(ctx);
   if (st != MMF_OK) return st;
   mmf::StateHdr h{};
-  memcpy(h.magic, "MMFSTAT1", 8);
+  memcpy(h.magic, "MMFSTAT2", 8);
   h.prec = (int32_t)ctx->prec;
   h.N = ctx->N;
   h.T = ctx->T;
@@ -2364,6 +2387,7 @@ mmf_status mmf_save_state(mmf_ctx* ctx, void* buf, size_t bytes) {
   h.A = ctx->A;
   h.sweeps = ctx->sweeps;
   h.graph_hash = mmf::graph_hash(ctx);
+  h.problem_hash = mmf::problem_hash(ctx);
   char* o = (char*)buf;
   memcpy(o, &h, sizeof h);
   o += sizeof h;
@@ -2373,12 +2397,8 @@ mmf_status mmf_save_state(mmf_ctx* ctx, void* buf, size_t bytes) {
   std::vector<int> we(TA);
   CU(cudaMemcpy(wm.data(), ctx->dp.Wm, wm.size(), cudaMemcpyDeviceToHost));
   CU(cudaMemcpy(we.data(), ctx->dp.We, TA * 4, cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(bm.data(), (char*)ctx->dp.bm + (size_t)ctx->T * NL * sm, bm.size(), cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(be.data(), (char*)ctx->dp.be + (size_t)ctx->T * NL * se, be.size(), cudaMemcpyDeviceToHost));
   char* owm = o;
   char* owe = owm + TA * sm;
-  char* obm = owe + TA * 4;
-  char* obe = obm + NL * sm;
   for (int t = 0; t < ctx->T; ++t)
     for (int64_t a = 0; a < ctx->A; ++a) {
       const size_t k = (size_t)t * ctx->A + ctx->int_of_arc[a], u = (size_t)t * ctx->A + a;
@@ -2386,9 +2406,20 @@ mmf_status mmf_save_state(mmf_ctx* ctx, void* buf, size_t bytes) {
       memcpy(owe + u * 4, &we[k], 4);
     }
   const size_t row_m = (size_t)ctx->Lp * sm, row_e = (size_t)ctx->Lp * se;
-  for (int v = 0; v < ctx->N; ++v) {
-    memcpy(obm + (size_t)v * row_m, bm.data() + (size_t)ctx->newid[v] * row_m, row_m);
-    memcpy(obe + (size_t)v * row_e, be.data() + (size_t)ctx->newid[v] * row_e, row_e);
+  char* ob = owe + TA * 4;
+  // UT = beta_T, then U0
+  const void* planes[2][2] = {{(char*)ctx->dp.bm + (size_t)ctx->T * NL * sm, (char*)ctx->dp.be + (size_t)ctx->T * NL * se},
+                              {ctx->dp.u0m, ctx->dp.u0e}};
+  for (int q = 0; q < 2; ++q) {
+    CU(cudaMemcpy(bm.data(), planes[q][0], bm.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(be.data(), planes[q][1], be.size(), cudaMemcpyDeviceToHost));
+    char* obm = ob;
+    char* obe = obm + NL * sm;
+    for (int v = 0; v < ctx->N; ++v) {
+      memcpy(obm + (size_t)v * row_m, bm.data() + (size_t)ctx->newid[v] * row_m, row_m);
+      memcpy(obe + (size_t)v * row_e, be.data() + (size_t)ctx->newid[v] * row_e, row_e);
+    }
+    ob = obe + NL * se;
   }
   return MMF_OK;
 }
@@ -2399,20 +2430,21 @@ mmf_status mmf_load_state(mmf_ctx* ctx, const void* buf, size_t bytes) {
   if (bytes < sizeof(mmf::StateHdr)) return fail(ctx, MMF_EINVAL, "state buffer too small");
   mmf::StateHdr h;
   memcpy(&h, buf, sizeof h);
-  if (memcmp(h.magic, "MMFSTAT1", 8) != 0) return fail(ctx, MMF_EINVAL, "not an mmf state");
+  if (memcmp(h.magic, "MMFSTAT2", 8) != 0) return fail(ctx, MMF_EINVAL, "not an mmf state (MMFSTAT2)");
   if (h.prec != (int32_t)ctx->prec || h.N != ctx->N || h.T != ctx->T || h.L != ctx->L || h.A != ctx->A ||
       h.l_begin != ctx->l_begin || h.graph_hash != mmf::graph_hash(ctx))
     return fail(ctx, MMF_EINVAL, "state was saved for another problem (graph, T, commodity slice or precision)");
+  if (h.problem_hash != mmf::problem_hash(ctx))
+    return fail(ctx, MMF_EINVAL, "state was saved for another problem (eps, costs or capacities differ)");
+  if (h.Lp <= 0 || h.Lp < h.L || h.sweeps < 0) return fail(ctx, MMF_EINVAL, "corrupt state header");
   const size_t TA = (size_t)ctx->T * ctx->A, sm = ctx->sm(), se = ctx->prec == MMF_FP32 ? 2 : 4;
   const size_t NL = (size_t)ctx->N * ctx->Lp, NLs = (size_t)ctx->N * h.Lp;
-  if (bytes < sizeof h + TA * (sm + 4) + NLs * (sm + se)) return fail(ctx, MMF_EINVAL, "state buffer truncated");
+  if (bytes < sizeof h + TA * (sm + 4) + 2 * NLs * (sm + se)) return fail(ctx, MMF_EINVAL, "state buffer truncated");
   mmf_status st = mmf_sync(ctx);
   if (st != MMF_OK) return st;
   const char* o = (const char*)buf + sizeof h;
   const char* owm = o;
   const char* owe = owm + TA * sm;
-  const char* obm = owe + TA * 4;
-  const char* obe = obm + NLs * sm;
   std::vector<char> wm(TA * sm), bm(NL * sm, 0), be(NL * se, 0);
   std::vector<int> we(TA);
   for (int t = 0; t < ctx->T; ++t)
@@ -2421,15 +2453,29 @@ mmf_status mmf_load_state(mmf_ctx* ctx, const void* buf, size_t bytes) {
       memcpy(wm.data() + k * sm, owm + u * sm, sm);
       memcpy(&we[k], owe + u * 4, 4);
     }
-  const int Lc = std::min(ctx->Lp, (int)h.Lp);  // (padding may differ between kernel configurations)
-  for (int v = 0; v < ctx->N; ++v) {
-    memcpy(bm.data() + (size_t)ctx->newid[v] * ctx->Lp * sm, obm + (size_t)v * h.Lp * sm, (size_t)Lc * sm);
-    memcpy(be.data() + (size_t)ctx->newid[v] * ctx->Lp * se, obe + (size_t)v * h.Lp * se, (size_t)Lc * se);
-  }
   CU(cudaMemcpy(ctx->dp.Wm, wm.data(), wm.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->dp.We, we.data(), TA * 4, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy((char*)ctx->dp.bm + (size_t)ctx->T * NL * sm, bm.data(), bm.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy((char*)ctx->dp.be + (size_t)ctx->T * NL * se, be.data(), be.size(), cudaMemcpyHostToDevice));
+  const int Lc = std::min(ctx->Lp, (int)h.Lp);  // (padding may differ between kernel configurations)
+  void* planes[2][2] = {{(char*)ctx->dp.bm + (size_t)ctx->T * NL * sm, (char*)ctx->dp.be + (size_t)ctx->T * NL * se},
+                        {ctx->dp.u0m, ctx->dp.u0e}};
+  const char* ob = owe + TA * 4;
+  for (int q = 0; q < 2; ++q) {
+    const char* obm = ob;
+    const char* obe = obm + NLs * sm;
+    std::fill(bm.begin(), bm.end(), 0);
+    std::fill(be.begin(), be.end(), 0);
+    if (ctx->prec == MMF_FP32)  // (padding lanes: exact zeros, exponent EZERO)
+      for (size_t k = 0; k < NL; ++k) ((int16_t*)be.data())[k] = (int16_t)EZERO;
+    else
+      for (size_t k = 0; k < NL; ++k) ((int32_t*)be.data())[k] = EZERO;
+    for (int v = 0; v < ctx->N; ++v) {
+      memcpy(bm.data() + (size_t)ctx->newid[v] * ctx->Lp * sm, obm + (size_t)v * h.Lp * sm, (size_t)Lc * sm);
+      memcpy(be.data() + (size_t)ctx->newid[v] * ctx->Lp * se, obe + (size_t)v * h.Lp * se, (size_t)Lc * se);
+    }
+    CU(cudaMemcpy(planes[q][0], bm.data(), bm.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(planes[q][1], be.data(), be.size(), cudaMemcpyHostToDevice));
+    ob = obe + NLs * se;
+  }
   st = dispatch(ctx, [&](auto eng) { return decltype(eng)::restore(ctx, ctx->stream); });
   if (st != MMF_OK) return st;
   ctx->sweeps = h.sweeps;

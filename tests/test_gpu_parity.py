@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle_run, readout_flows, stats as oracle_stats
+from oracle.sweep import dual_terms
 from workloads import gen, grid_problem
 from tests._metrics import max_rel_err, flow_floor, W_FLOOR
 
@@ -37,7 +38,26 @@ def run_gpu(p, sweeps, prec, **kw):
 def run_oracle(p, sweeps, **kw):
     st = oracle_run(p, sweeps, **kw)
     F, W = readout_flows(st)
-    return F, W, oracle_stats(st)
+    so = oracle_stats(st)
+    so["dual_scale"] = p.eps * (so["mass"] + sum(abs(x) for x in dual_terms(st)))
+    return F, W, so
+
+
+def assert_stats(sg, so, prec, F=None):
+    """Every mmf_read_stats field against the oracle's end-of-sweep statistics.  The dual
+    is a sum of large terms of both signs (eps * (-mass + <mu0, lam0> + <muT, lamT> + <d, omega>), thm:solution
+    P:786-788): its tolerance scales with the sum of their magnitudes; marginal mismatches and the capacity
+    violation are differences of near-equal numbers: absolute tolerances relative to the mass / flows."""
+    tol = 10 * TOL[prec]
+    m = abs(so["mass"])
+    assert abs(sg["mass"] - so["mass"]) <= tol * m, ("mass", sg["mass"], so["mass"])
+    assert abs(sg["primal"] - so["primal"]) <= tol * max(abs(so["primal"]), 1e-300), ("primal", sg["primal"], so["primal"])
+    assert abs(sg["dual"] - so["dual"]) <= tol * so["dual_scale"], ("dual", sg["dual"], so["dual"])
+    for k in ("src_mismatch", "sink_mismatch"):
+        assert abs(sg[k] - so[k]) <= tol * m, (k, sg[k], so[k])
+    fmax = float(np.max(F)) if F is not None and F.size else m
+    assert abs(sg["cap_violation"] - so["cap_violation"]) <= tol * fmax, ("cap_violation", sg["cap_violation"],
+                                                                          so["cap_violation"])
 
 
 def assert_parity(p, sweeps, prec, oracle_kw=None, **kw):
@@ -46,7 +66,8 @@ def assert_parity(p, sweeps, prec, oracle_kw=None, **kw):
     ef = max_rel_err(Fg, Fo, flow_floor(p))
     ew = max_rel_err(Wg, Wo, W_FLOOR)
     assert ef < TOL[prec] and ew < TOL[prec], (p.name, prec, ef, ew)
-    assert abs(sg["mass"] - so["mass"]) <= 10 * TOL[prec] * abs(so["mass"])
+    assert sg["sweeps"] == so["sweeps"] == sweeps
+    assert_stats(sg, so, prec, Fo)
     return ef, ew
 
 
@@ -425,3 +446,144 @@ def test_nccl_exchange_path_one_rank(prec):
     uid = _lib.mmf_nccl_unique_id()
     p = grid_problem(6, 7, 9, 150, 0.2, seed=26, cap=(0.3, 1.5))
     assert_parity(p, 6, prec, nccl_uid=uid, nranks=1, rank=0)
+
+
+# ---------------------------------------------------------------------------------------------
+# round 2: readouts before any sweep / right after a state load, error paths, [5]'s wide-lane forward,
+# the pipelined Jacobi bulk exchange, a negative control
+
+@pytest.mark.parametrize("prec,L", [("fp32", 1019), ("fp64", 37)])
+def test_readout_after_init_and_after_load_without_sweep(prec, L):
+    """mmf_init leaves U0 = 0 (Alg. 2 computes U0 first; the oracle's lam0 = -inf), so a readout before
+    any sweep returns the zero tensor's flows, equal to the oracle's 0-sweep readout; a state loaded into a fresh
+    context reads out (flows, duals, stats) bitwise like the context that saved it, without a sweep."""
+    from paper_2106_14485_b200 import Solver
+    p = grid_problem(9, 9, 7, L, 0.2, seed=38, cap=(0.3, 1.2))
+    Fo0, Wo0, so0 = run_oracle(p, 0)
+    with Solver(p, prec=prec) as a:
+        F0, W0 = a.edge_flows(), a.cap_duals()
+        assert np.array_equal(F0, Fo0) and np.array_equal(W0, Wo0)
+        assert a.stats()["mass"] == 0.0
+        a.sweep(3)
+        state = a.save_state()
+        Fa, Wa, sa = a.edge_flows(), a.cap_duals(), a.stats()
+    with Solver(p, prec=prec) as b:
+        b.load_state(state)
+        Fb, Wb, sb = b.edge_flows(), b.cap_duals(), b.stats()
+    assert np.array_equal(Fa, Fb) and np.array_equal(Wa, Wb)
+    assert sa == sb
+    Fo, Wo, so = run_oracle(p, 3)
+    assert max_rel_err(Fb, Fo, flow_floor(p)) < TOL[prec] and max_rel_err(Wb, Wo, W_FLOOR) < TOL[prec]
+    assert_stats(sb, so, prec, Fo)
+
+
+def test_load_state_rejects_other_costs_and_corrupt_header():
+    import dataclasses
+    from paper_2106_14485_b200 import MMFError, Solver
+    p = grid_problem(6, 6, 5, 40, 0.2, seed=38, cap=(0.3, 1.2))
+    with Solver(p, prec="fp32") as a:
+        a.sweep(1)
+        state = a.save_state()
+    for q in (dataclasses.replace(p, eps=0.21), dataclasses.replace(p, cost=p.cost * 1.01),
+              dataclasses.replace(p, cap=p.cap * 0.5)):
+        with Solver(q, prec="fp32") as c:
+            with pytest.raises(MMFError) as e:
+                c.load_state(state)
+            assert e.value.name == "MMF_EINVAL"
+    bad = bytearray(state)
+    bad[:8] = b"MMFSTAT1"
+    with Solver(p, prec="fp32") as c:
+        with pytest.raises(MMFError):
+            c.load_state(bytes(bad))
+        with pytest.raises(MMFError):
+            c.load_state(state[: len(state) // 2])
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_extended_exponent_overflow_is_sticky_erange(prec):
+    """Every walk costs 12 (T = 12 unit-cost steps) at eps = 1e-3: the messages reach e^-12000 = 2^-17312, past the
+    extended exponent's range (|e| <= 16000, xf.cuh): the sweep must raise MMF_ERANGE, not return
+    garbage.  At eps = 2e-3 (2^-8656) the same instance is in range and matches the log-domain oracle."""
+    from paper_2106_14485_b200 import MMFError
+    p = grid_problem(3, 3, 12, 2, 1e-3, seed=44, move_cost=1.0, stay_cost=1.0, cap=None)
+    with pytest.raises(MMFError) as e:
+        run_gpu(p, 1, prec)
+    assert e.value.name == "MMF_ERANGE"
+    import dataclasses
+    assert_parity(dataclasses.replace(p, eps=2e-3), 2, prec)
+
+
+def test_out_of_order_calls_are_estate():
+    """calling out of order returns MMF_ESTATE (sweep / readout before init, costs before graph,
+    a pre-init option after init)."""
+    import ctypes as C
+    from paper_2106_14485_b200 import _lib as L
+    lib = L.load()
+    ctx = L.mmf_create(0, L.MMF_FP32, 0)
+    try:
+        assert lib.mmf_sweep(ctx, 1) == 8
+        out = np.zeros(4)
+        assert lib.mmf_read_edge_flows(ctx, out.ctypes.data_as(C.POINTER(C.c_double))) == 8
+        cost = np.ones(4)
+        assert lib.mmf_set_costs(ctx, 2, 0.1, cost.ctypes.data_as(C.POINTER(C.c_double)), 0) == 8
+        assert lib.mmf_init(ctx) == 8
+    finally:
+        L.mmf_destroy(ctx)
+    p = grid_problem(3, 3, 4, 2, 0.5, seed=25)
+    from paper_2106_14485_b200 import MMFError, Solver
+    with Solver(p, prec="fp32") as s:
+        with pytest.raises(MMFError) as e:
+            L.mmf_set_option(s.ctx, "kernels", 3)
+        assert e.value.name == "MMF_ESTATE"
+
+
+@pytest.mark.parametrize("bad", ["N0", "T0", "arc", "point"])
+def test_setup_validation_einval(bad):
+    """SURVEY §8(b) setup validation: N < 1, T < 1, out-of-range arc ids, out-of-range point-mass nodes."""
+    import dataclasses
+    from paper_2106_14485_b200 import MMFError, Solver
+    p = grid_problem(3, 3, 4, 2, 0.5, seed=25)
+    if bad == "N0":
+        q = dataclasses.replace(p, N=0)
+    elif bad == "T0":
+        q = dataclasses.replace(p, T=0)
+    elif bad == "arc":
+        q = dataclasses.replace(p, head=np.where(np.arange(p.A) == 3, p.N, p.head).astype(np.int32))
+    else:
+        q = dataclasses.replace(p, dst=np.array([0, p.N], np.int32))
+    with pytest.raises(MMFError) as e:
+        Solver(q, prec="fp32")
+    assert e.value.name == "MMF_EINVAL"
+
+
+@pytest.mark.parametrize("L", [2051, 4099])
+def test_wide_lane_multi_group_forward_fp32_default_options(L):
+    """L > 1024: the forward of [5] (L = 8192) in its production configuration, the fp32 wide-lane kernel with 8
+    commodities per lane and several 2048-commodity groups per node ("global partials + last arriver", wide.cuh),
+    with the default options and a ragged commodity tail, against the live oracle element by element."""
+    p = grid_problem(8, 8, 6, L, 0.1, seed=45, cap=(0.5 * L / 100, 3.0 * L / 100))
+    assert_parity(p, 3, "fp32")
+
+
+def test_nccl_jacobi_bulk_exchange_pipelined_one_rank():
+    """The Jacobi schedule's bulk all-reduce with the pipelined readout-mode forward (MODE 3: fp32, L >= 256), on a
+    one-rank NCCL communicator, against the oracle's Jacobi sweep (the fast path behind the 76 ms/sweep
+    figure)."""
+    import torch
+    torch.cuda.nccl.version()
+    from paper_2106_14485_b200 import _lib
+    p = grid_problem(12, 12, 8, 1019, 0.1, seed=31, cap=(0.3, 1.5))
+    assert_parity(p, 4, "fp32", oracle_kw=dict(schedule="jacobi", theta=0.5), nccl_uid=_lib.mmf_nccl_unique_id(),
+                  nranks=1, rank=0, options=dict(schedule=1, theta_milli=500))
+
+
+def test_negative_control_broken_kernel_fails_parity():
+    """SURVEY §4 negative control: the parity harness must detect a wrong kernel.  The pipelined forward's
+    diagnostic mode dry=3 skips the capacity-dual update (results invalid by design): the same comparison that the
+    production path passes must fail on it."""
+    p = grid_problem(12, 12, 8, 1019, 0.1, seed=31, cap=(0.3, 1.5))
+    Fo, Wo, _ = run_oracle(p, 2)
+    Fg, Wg, _ = run_gpu(p, 2, "fp32", options=dict(dry=3))
+    assert max_rel_err(Wg, Wo, W_FLOOR) > 1e-2
+    Fg, Wg, _ = run_gpu(p, 2, "fp32")
+    assert max_rel_err(Wg, Wo, W_FLOOR) < TOL["fp32"]

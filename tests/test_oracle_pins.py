@@ -470,3 +470,191 @@ def test_solve_converges_and_satisfies_constraints():
     assert np.maximum(F - cap, 0.0)[np.isfinite(cap)].sum() / mass < 1e-8
     st0, conv0, k0, err0, hist0 = oracle_solve(p, 1e-8, 0)
     assert not conv0 and k0 == 0 and hist0 == [] and st0.sweeps == 0
+
+
+# ---------------------------------------------------------------------------------------------
+# round 2: the dual objective pinned completely (thm:solution P:777-788), storage options, sharding combine,
+# fp32-level conditioning probe, a negative control of the parity metric
+
+def _cost_tensor(p):
+    """C[l, v_0, ..., v_T] = sum_t C_t[v_t, v_{t+1}] (+inf off the graph), the cost tensor of eq:omt_multi_graph_reg
+    in node form, built literally by broadcasting."""
+    Ct = []
+    for t in range(p.T):
+        D = np.full((p.N, p.N), np.inf)
+        D[p.tail, p.head] = p.cost_t(t)
+        Ct.append(D)
+    C = np.zeros((1,) * 1 + (p.N,))
+    for t in range(p.T):
+        C = C[..., :, None] + Ct[t].reshape((1,) * (C.ndim - 1) + Ct[t].shape)
+    return np.broadcast_to(C, (p.L,) + C.shape[1:])
+
+
+@pytest.mark.parametrize("kw", [MICROS[0], MICROS[4], MICROS[6]])
+def test_dual_objective_equals_brute_force_dual(kw):
+    """eq:omt_multi_graph_dual (P:786-788): Phi = -eps <K, U> - sum <lambda_t, mu_t> - sum <lambda_t, d_t> with
+    u = exp(-lambda/eps), evaluated on the brute-force Sinkhorn's OWN scalings (oracle/brute.py, full-tensor
+    projections) and the full tensor's mass, equals the oracle's dual_objective after every sweep."""
+    p = _micro(kw)
+    st = oracle_init(p)
+    bs = BruteState(p)
+    cap = np.broadcast_to(p.cap, (p.T, p.A))
+    for k in range(6):
+        oracle_sweep(st)
+        brute_sweep(bs)
+        M = bs.tensor()
+        with np.errstate(divide="ignore"):
+            lam0, lamT, lamW = -p.eps * np.log(bs.U0), -p.eps * np.log(bs.UT), -p.eps * np.log(bs.W)
+        # <lambda, mu> with 0 * inf = 0 (P:109); lambda_t on capacitated arcs only (V_<=)
+        t0 = np.where(p.mu0 > 0, p.mu0 * lam0, 0.0).sum()
+        tT = np.where(p.muT > 0, p.muT * lamT, 0.0).sum()
+        fin = np.isfinite(cap) & (cap > 0)
+        tW = np.where(fin, cap * np.where(fin, lamW, 0.0), 0.0).sum()
+        phi = -p.eps * M.sum() - t0 - tT - tW
+        got = dual_objective(st, float(np.exp(st.a[p.T] + st.lamT).sum()))
+        assert abs(got - phi) <= 1e-11 * max(1.0, abs(phi)), (k, got, phi)
+
+
+@pytest.mark.parametrize("which", ["tight-micro", "tight-grid", "dense-slack"])
+def test_strong_duality_at_convergence(which):
+    """thm:solution (strong duality, the proof's Lagrangian): at the optimum the regularised primal
+    <C, M> + eps sum (M log M - M) of the brute-force tensor equals the dual objective.  With binding capacities
+    the capacity term sum d * log W carries a sizeable share of Phi (dropping it fails this pin)."""
+    if which == "tight-micro":
+        p = grid_problem(2, 3, 4, 2, 0.5, seed=2, cap=(0.3, 0.6))
+    elif which == "tight-grid":
+        p = grid_problem(3, 3, 4, 2, 0.5, seed=13, cap=(0.15, 0.4))
+    else:
+        p = grid_problem(2, 3, 4, 2, 0.6, seed=5, cap=(0.3, 0.7), marginals="dense")
+    st = oracle_init(p)
+    for _ in range(3000):
+        oracle_sweep(st)
+    M = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT))
+    C = _cost_tensor(p)
+    pos = M > 0
+    primal = (C[pos] * M[pos]).sum() + p.eps * (M[pos] * np.log(M[pos]) - M[pos]).sum()
+    mass = float(np.exp(st.a[p.T] + st.lamT).sum())
+    phi = dual_objective(st, mass)
+    from oracle.sweep import dual_terms
+    sd = dual_terms(st)[2]
+    assert stats(st)["cap_violation"] < 1e-12          # (a feasible instance, converged)
+    assert abs(primal - phi) <= 1e-9 * abs(phi), (primal, phi)
+    # complementary slackness behind it: F_t[a] = d_t[a] wherever W_t[a] < 1
+    F, W = readout_flows(st)
+    cap = np.broadcast_to(p.cap, F.shape)
+    bind = W < 1 - 1e-9
+    if which != "dense-slack":
+        assert abs(p.eps * sd) > 0.1 * abs(phi)        # (capacities bind: the term matters)
+        assert bind.any() and np.max(np.abs(F[bind] - cap[bind]) / cap[bind]) < 1e-8
+    else:
+        assert not bind.any() and sd == 0.0
+
+
+@pytest.mark.parametrize("schedule", ["gs", "jacobi"])
+def test_storage_options_bitwise_equal(schedule):
+    """oracle_init's storage options (an np.memmap backward store, two forward layers recomputed for readouts —
+    used for the full-size [4]/[5] fixtures) change no value: F, W and every statistic are bitwise equal to the
+    in-memory oracle's, for both schedules and at 0 sweeps."""
+    import os
+    import tempfile
+    from oracle import oracle_sweep_jacobi
+    for kw in [dict(), dict(marginals="dense", closed_arcs=2, time_varying=True)]:
+        p = grid_problem(4, 5, 6, 5, 0.3, seed=3, cap=(0.2, 0.6), **kw)
+        ref = oracle_init(p)
+        with tempfile.TemporaryDirectory() as d:
+            mm = np.lib.format.open_memmap(os.path.join(d, "b.npy"), mode="w+", dtype=np.float64,
+                                           shape=(p.T + 1, p.L, p.N))
+            st = oracle_init(p, b_store=mm, keep_forward=False)
+            for k in range(4):
+                F1, W1 = readout_flows(ref)
+                F2, W2 = readout_flows(st)
+                assert np.array_equal(F1, F2) and np.array_equal(W1, W2)
+                assert stats(ref) == stats(st)
+                for t in (0, p.T - 1):
+                    assert np.array_equal(readout_commodity_flows(ref, t), readout_commodity_flows(st, t))
+                if schedule == "gs":
+                    oracle_sweep(ref)
+                    oracle_sweep(st)
+                else:
+                    oracle_sweep_jacobi(ref, 0.5)
+                    oracle_sweep_jacobi(st, 0.5)
+            del st, mm
+
+
+def test_sharded_oracle_combine_equals_unsharded():
+    """oracle.shard (the commodity sharding the full-size fixtures use): G = 3 shards run in lock step in one
+    process, their per-arc log flow sums combined by combine_lse before every W_t update, and their statistics by
+    combine_stats, reproduce the unsharded oracle (rem:multi_tensor_scheme P:1139-1147) to rounding."""
+    import threading
+    from oracle.shard import combine_lse, shard_pieces, combine_stats
+    p = grid_problem(4, 5, 6, 7, 0.2, seed=41, cap=(0.2, 0.6))
+    G = 3
+    bounds = [(0, 3), (3, 5), (5, 7)]
+    shards = [oracle_init(p.commodity_slice(a, b)) for a, b in bounds]
+    bar = threading.Barrier(G)
+    box = [None] * G
+    out = {}
+
+    def worker(g):
+        def reduce_lse(v):
+            box[g] = np.array(v)
+            bar.wait()
+            r = combine_lse(np.stack(box))
+            bar.wait()
+            return r
+        for _ in range(5):
+            oracle_sweep(shards[g], reduce_lse=reduce_lse)
+        out[g] = shard_pieces(shards[g])
+
+    th = [threading.Thread(target=worker, args=(g,)) for g in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    s = combine_stats(p, [out[g] for g in range(G)], shards[0].omega, 5)
+    ref = oracle_run(p, 5)
+    F, W = readout_flows(ref)
+    so = stats(ref)
+    assert max_rel_err(s["F"], F, 1e-300) < 1e-12 and max_rel_err(s["W"], W, 1e-300) < 1e-12
+    for k in ("mass", "primal", "dual", "src_mismatch", "sink_mismatch", "cap_violation", "cap_excess"):
+        assert abs(s[k] - so[k]) <= 1e-11 * max(abs(so[k]), 1e-3), (k, s[k], so[k])
+    assert np.min(W) < 0.999
+
+
+def test_p8_conditioning_probe_fp32_inputs():
+    """P8 at the fp32 parity bar: the oracle on inputs perturbed as the fp32 path rounds them (K = exp(-C/eps) by
+    a relative 2^-24, capacities to float32) disagrees with itself by far less than 1e-4 after the Q21 sweep count,
+    on the BASELINE graphs and horizons at small L — so 1e-4 is attainable (an ill-conditioned config would show
+    here)."""
+    import dataclasses
+    from tests._metrics import flow_floor
+    cases = [(gen(1), 200), (gen(2, L=4, T=60), 100), (gen(4, L=2, T=40), 3), (gen(5, L=8, T=40), 3),
+             (gen(3, L=2, T=40), 10)]
+    for base, sweeps in cases:
+        rng = np.random.default_rng(0)
+        dK = rng.uniform(-2.0 ** -24, 2.0 ** -24, base.cost.shape)
+        pert = dataclasses.replace(base, cost=base.cost - base.eps * np.log1p(dK),
+                                   cap=base.cap.astype(np.float32).astype(np.float64))
+        F1, W1 = readout_flows(oracle_run(base, sweeps))
+        F2, W2 = readout_flows(oracle_run(pert, sweeps))
+        ef, ew = max_rel_err(F2, F1, flow_floor(base)), max_rel_err(W2, W1, 1e-30)
+        assert ef < 1e-5 and ew < 1e-5, (base.name, ef, ew)
+
+
+def test_parity_metric_negative_control():
+    """SURVEY §4 negative control of the parity metric itself (Q11): an oracle result with ONE capacity dual moved
+    by k ulp fails the fp64 bar once k ulp exceed 1e-10 relative, and one flow moved by 2e-4 relative fails fp32."""
+    p = grid_problem(3, 3, 5, 3, 0.3, seed=15, cap=(0.1, 0.4))
+    F, W = readout_flows(oracle_run(p, 5))
+    from tests._metrics import flow_floor
+    i = np.unravel_index(np.argmin(W), W.shape)
+    assert W[i] < 1
+    W2 = W.copy()
+    W2[i] = W[i] + 2 ** 20 * np.spacing(W[i])           # 2^20 ulp = 2.3e-10 relative
+    assert max_rel_err(W2, W, 1e-30) > 1e-10
+    W2[i] = W[i] + 2 ** 10 * np.spacing(W[i])           # 2^10 ulp = 2.3e-13: passes
+    assert max_rel_err(W2, W, 1e-30) < 1e-10
+    F2 = F.copy()
+    j = np.unravel_index(np.argmax(F), F.shape)
+    F2[j] *= 1 + 2e-4
+    assert max_rel_err(F2, F, flow_floor(p)) > 1e-4
