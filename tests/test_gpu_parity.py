@@ -471,7 +471,8 @@ def test_readout_after_init_and_after_load_without_sweep(prec, L):
         b.load_state(state)
         Fb, Wb, sb = b.edge_flows(), b.cap_duals(), b.stats()
     assert np.array_equal(Fa, Fb) and np.array_equal(Wa, Wb)
-    assert sa == sb
+    for k in sa:  # (the device statistics reduce with atomics: equal up to summation order)
+        assert abs(sa[k] - sb[k]) <= 1e-12 * max(abs(sa[k]), 1e-300), (k, sa[k], sb[k])
     Fo, Wo, so = run_oracle(p, 3)
     assert max_rel_err(Fb, Fo, flow_floor(p)) < TOL[prec] and max_rel_err(Wb, Wo, W_FLOOR) < TOL[prec]
     assert_stats(sb, so, prec, Fo)
@@ -578,12 +579,24 @@ def test_nccl_jacobi_bulk_exchange_pipelined_one_rank():
 
 
 def test_negative_control_broken_kernel_fails_parity():
-    """SURVEY §4 negative control: the parity harness must detect a wrong kernel.  The pipelined forward's
-    diagnostic mode dry=3 skips the capacity-dual update (results invalid by design): the same comparison that the
-    production path passes must fail on it."""
+    """SURVEY §4 negative control: the parity harness must detect a wrong result.  (a) The GPU run on an input with
+    ONE capacity changed by 0.1 % (a stand-in for a dropped or perturbed term) fails the fp32 comparison against the
+    oracle of the original input, which the unchanged run passes; (b) the pipelined forward's diagnostic mode dry=3
+    (skips the capacity-dual update: invalid by design) either fails the comparison or trips a sticky error."""
+    from paper_2106_14485_b200 import MMFError
     p = grid_problem(12, 12, 8, 1019, 0.1, seed=31, cap=(0.3, 1.5))
     Fo, Wo, _ = run_oracle(p, 2)
-    Fg, Wg, _ = run_gpu(p, 2, "fp32", options=dict(dry=3))
-    assert max_rel_err(Wg, Wo, W_FLOOR) > 1e-2
     Fg, Wg, _ = run_gpu(p, 2, "fp32")
-    assert max_rel_err(Wg, Wo, W_FLOOR) < TOL["fp32"]
+    assert max_rel_err(Wg, Wo, W_FLOOR) < TOL["fp32"] and max_rel_err(Fg, Fo, flow_floor(p)) < TOL["fp32"]
+    a = int(np.argmin(Wo.min(axis=0)))
+    assert Wo[:, a].min() < 0.99
+    import dataclasses
+    q = dataclasses.replace(p, cap=p.cap.copy())
+    q.cap[a] *= 1.001
+    Fg, Wg, _ = run_gpu(q, 2, "fp32")
+    assert max_rel_err(Wg, Wo, W_FLOOR) > TOL["fp32"] and max_rel_err(Fg, Fo, flow_floor(p)) > TOL["fp32"]
+    try:
+        Fg, Wg, _ = run_gpu(p, 2, "fp32", options=dict(dry=3))
+        assert max_rel_err(Wg, Wo, W_FLOOR) > 1e-2
+    except MMFError:
+        pass
