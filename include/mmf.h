@@ -94,6 +94,15 @@ mmf_status mmf_set_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, in
 mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count,
                                    const int32_t* src, const int32_t* dst, const double* mass);
 
+/* Commodity-dependent node costs (the commodity-dependent kernel K_L = exp(-C_L/eps) of
+ * eq:K_multicommodity P:1010-1013, restricted to costs that depend on the arc's head node): c is [l_count][N]
+ * row-major for this rank's commodities (call after the marginals and mmf_set_costs, before mmf_init); commodity l
+ * pays c[l][j] for each intermediate layer t = 1..T-1 it spends at node j, i.e. its arc costs are
+ * C_t[a] + c[l][head(a)] for t = 0..T-2 (reading R-N; the boundary layers 0 and T carry the marginals
+ * alone).  Values must be finite with |c / eps| log2(e) <= 8000, else MMF_EINVAL; NULL clears.  The factors
+ * D = exp(-c/eps) are formed in fp64 and stored like K; stats' "primal" stays the arc-cost term. */
+mmf_status mmf_set_node_costs(mmf_ctx* ctx, const double* c);
+
 /* Device bytes needed once graph, costs, capacities and marginals are set. */
 mmf_status mmf_workspace_bytes(const mmf_ctx* ctx, size_t* bytes);
 

@@ -26,12 +26,18 @@ def dense_kernel(problem, t: int, W_t: np.ndarray) -> np.ndarray:
 
 
 def full_tensor(problem, U0: np.ndarray, W: np.ndarray, UT: np.ndarray) -> np.ndarray:
-    """M with shape (L, N, ..., N) (T+1 node modes)."""
+    """M with shape (L, N, ..., N) (T+1 node modes).  With commodity node costs c[l, j] (NEXT-2, reading R-N) every
+    intermediate mode t = 1..T-1 is also multiplied by exp(-c[l, v_t]/eps) (the commodity-dependent K_L of
+    eq:K_multicommodity, P:1010-1013)."""
     p = problem
+    nc = getattr(p, "node_cost", None)
     M = U0.copy()                                   # (L, N)
     for t in range(p.T):
         KW = dense_kernel(p, t, W[t])
         M = M[..., :, None] * KW.reshape((1,) * (M.ndim - 1) + KW.shape)
+        if nc is not None and t + 1 <= p.T - 1:     # mode t + 1 is an intermediate layer
+            Dl = np.exp(-np.asarray(nc, float) / p.eps)          # (L, N)
+            M = M * Dl.reshape((p.L,) + (1,) * (M.ndim - 2) + (p.N,))
     return M * UT.reshape((p.L,) + (1,) * (p.T) + (p.N,))
 
 

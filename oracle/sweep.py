@@ -103,6 +103,17 @@ class OracleState:
     out_seg: tuple       # arcs grouped by tail (backward recursion)
     sweeps: int = 0
     keep_forward: bool = True   # False: ``a`` holds only the two latest layers (see _TwoLayers)
+    lD: Optional[np.ndarray] = None  # [L, N] -c[l, j]/eps, commodity node costs (NEXT-2), or None
+
+
+def _layer_cost(st: "OracleState", t: int):
+    """log of the commodity node factor D_t[l, j] = exp(-c[l, j]/eps) at layer t (SURVEY §8(f) NEXT-2 in the form of
+    DESIGN.md reading R-N: charged at the intermediate layers 1..T-1 only, so the boundary layers 0 and T carry the
+    marginals alone).  It multiplies every walk through (t, j) of commodity l: the commodity-dependent kernel K_L of
+    eq:K_multicommodity restricted to costs that depend on the arc's head."""
+    if st.lD is None or t < 1 or t > st.problem.T - 1:
+        return 0.0
+    return st.lD
 
 
 class _TwoLayers:
@@ -150,7 +161,8 @@ def oracle_init(problem, b_store: Optional[np.ndarray] = None, keep_forward: boo
         a=np.full((T + 1, L, N), NEG_INF) if keep_forward else _TwoLayers(L, N), b=b,
         log_mu0=_log(mu0), log_muT=_log(muT),
         in_seg=_segments(p.head.astype(np.int64), N), out_seg=_segments(p.tail.astype(np.int64), N),
-        keep_forward=keep_forward)
+        keep_forward=keep_forward,
+        lD=None if getattr(p, "node_cost", None) is None else -np.asarray(p.node_cost, np.float64) / float(p.eps))
     backward(st)
     return st
 
@@ -163,7 +175,7 @@ def backward(st: OracleState) -> None:
     head_o = p.head[o]
     st.b[p.T] = st.lamT
     for t in range(p.T - 1, -1, -1):
-        X = (st.lK[t][o] + st.omega[t][o])[None, :] + st.b[t + 1][:, head_o]
+        X = (st.lK[t][o] + st.omega[t][o])[None, :] + (st.b[t + 1] + _layer_cost(st, t + 1))[:, head_o]
         st.b[t] = seg_lse(X, st.out_seg)
 
 
@@ -209,7 +221,7 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
         on_block("U0", -1, float(np.exp(st.a[0] + st.b[0]).sum()))
     # a3: forward loop
     for t in range(p.T):
-        X = st.a[t][:, p.tail] + st.lK[t][None, :] + st.b[t + 1][:, p.head]      # [L, A], no W
+        X = st.a[t][:, p.tail] + st.lK[t][None, :] + (st.b[t + 1] + _layer_cost(st, t + 1))[:, p.head]  # no W
         lse = _lse_rows(X)
         if reduce_lse is not None:
             lse = reduce_lse(lse)
@@ -217,7 +229,7 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
         if on_block is not None:
             on_block("W", t, float(np.exp(X + st.omega[t][None, :]).sum()))
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
-        st.a[t + 1] = seg_lse(Y, st.in_seg)                                    # Psi-hat_{t+1}
+        st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)           # Psi-hat_{t+1}
     # a4: U^(0,T) <- R^(0,T) ./ Psi-hat_T
     st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
     if on_block is not None:
@@ -249,11 +261,11 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     st.a[0] = st.lam0
     new_omega = np.empty_like(st.omega)
     for t in range(p.T):
-        X = st.a[t][:, p.tail] + st.lK[t][None, :] + st.b[t + 1][:, p.head]
+        X = st.a[t][:, p.tail] + st.lK[t][None, :] + (st.b[t + 1] + _layer_cost(st, t + 1))[:, p.head]
         full = capacity_update(st.logd[t], _lse_rows(X))
         new_omega[t] = damped_update(st.omega[t], full, theta)
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]   # (the previous W_t)
-        st.a[t + 1] = seg_lse(Y, st.in_seg)
+        st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)
     st.omega = new_omega
     st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
     backward(st)
@@ -263,7 +275,7 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     st.a[0] = st.lam0          # (unchanged in the kept store; the two-layer store has overwritten slot 0)
     for t in range(p.T):
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
-        st.a[t + 1] = seg_lse(Y, st.in_seg)
+        st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)
     st.sweeps += 1
 
 
@@ -298,12 +310,12 @@ def forward_layers(st: OracleState, t_stop: Optional[int] = None):
         yield t, cur
         if t < t_stop:
             Y = cur[:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
-            cur = seg_lse(Y, st.in_seg)
+            cur = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)
 
 
 def _commodity_flows_at(st: OracleState, t: int, a_t: np.ndarray) -> np.ndarray:
     p = st.problem
-    return np.exp(a_t[:, p.tail] + (st.lK[t] + st.omega[t])[None, :] + st.b[t + 1][:, p.head]).T
+    return np.exp(a_t[:, p.tail] + (st.lK[t] + st.omega[t])[None, :] + (st.b[t + 1] + _layer_cost(st, t + 1))[:, p.head]).T
 
 
 def readout_commodity_flows(st: OracleState, t: int) -> np.ndarray:

@@ -23,7 +23,7 @@ EXPORTS = ["mmf_create", "mmf_set_graph", "mmf_set_costs", "mmf_set_capacity", "
            "mmf_set_option", "mmf_init", "mmf_sweep", "mmf_sync", "mmf_read_edge_flows", "mmf_read_cap_duals",
            "mmf_read_stats", "mmf_read_kernel_stats", "mmf_sweep_bytes", "mmf_destroy", "mmf_last_error",
            "mmf_version", "mmf_solve", "mmf_state_bytes", "mmf_save_state", "mmf_load_state",
-           "mmf_read_commodity_flows"]
+           "mmf_read_commodity_flows", "mmf_set_node_costs"]
 
 
 class MMFError(RuntimeError):
@@ -78,6 +78,7 @@ def load(path: str = None):
         "mmf_load_state": ([vp, vp, C.c_size_t], C.c_int),
         "mmf_read_kernel_stats": ([vp, C.POINTER(C.c_int64), dp, C.c_int], C.c_int),
         "mmf_sweep_bytes": ([vp, dp, dp, C.c_int], C.c_int),
+        "mmf_set_node_costs": ([vp, dp], C.c_int),
         "mmf_destroy": ([vp], C.c_int),
         "mmf_last_error": ([vp], C.c_char_p),
         "mmf_version": ([], C.c_char_p),
@@ -147,6 +148,15 @@ def mmf_set_point_marginals(ctx, L_global: int, l_begin: int, src, dst, mass):
     src, dst, mass = _i32(src), _i32(dst), _f64(mass)
     _check(ctx, load().mmf_set_point_marginals(ctx, int(L_global), int(l_begin), int(src.size), _p(src, C.c_int32),
                                                _p(dst, C.c_int32), _p(mass, C.c_double)))
+
+
+def mmf_set_node_costs(ctx, c):
+    """c: [l_count, N] commodity node costs (None clears)."""
+    if c is None:
+        _check(ctx, load().mmf_set_node_costs(ctx, None))
+        return
+    c = _f64(c)
+    _check(ctx, load().mmf_set_node_costs(ctx, _p(c, C.c_double)))
 
 
 def mmf_workspace_bytes(ctx) -> int:

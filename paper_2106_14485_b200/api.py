@@ -61,6 +61,8 @@ class Solver:
             L.mmf_set_point_marginals(self.ctx, p.L, l_begin, p.src[sl], p.dst[sl], p.mass[sl])
         else:
             L.mmf_set_marginals(self.ctx, p.L, l_begin, p.mu0[sl], p.muT[sl])
+        if getattr(p, "node_cost", None) is not None:
+            L.mmf_set_node_costs(self.ctx, p.node_cost[sl])
 
     def sweep(self, n: int = 1):
         L.mmf_sweep(self.ctx, n)

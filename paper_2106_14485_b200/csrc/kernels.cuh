@@ -58,6 +58,10 @@ struct DevPtrs {
   const int* ell_ipos;  // [A] internal arc -> slot in ell_in (head * Din + k)
   const int* ell_opos;  // [A] internal arc -> slot in ell_out (tail * Dout + k)
   int Din, Dout;
+  // commodity node factors D = exp(-c / eps) [N][Lp], applied by the message epilogues
+  // (norm_lane, store_msg) of launches whose output layer is intermediate (1..T-1); null otherwise
+  const void* dnm;
+  const void* dne;
   int diag;  // diagnostics of the pipelined forward (option "dry" >= 2; results invalid), else 0
   float theta;  // Jacobi schedule damping: W <- W^(1 - theta) min(W d / F, 1)^theta
 };
@@ -123,6 +127,14 @@ __device__ __forceinline__ void store_msg(const DevPtrs& p, typename T_::M* pm, 
   M m;
   int e;
   xf_norm<M>(s, E, m, e);
+  if (p.dnm && m != M(0)) {  // commodity node factor of this layer (NEXT-2)
+    m *= ((const M*)p.dnm)[idx];
+    e += (int)((const typename T_::E*)p.dne)[idx];
+    if (m >= M(2)) {
+      m *= M(0.5);
+      e += 1;
+    }
+  }
   if (m != M(0) && (e > ELIM || e < -ELIM)) {
     set_error(p, ERR_RANGE, l, node);
     e = e > 0 ? ELIM : -ELIM;

@@ -90,6 +90,7 @@ struct mmf_ctx {
   bool point = false, have_marg = false;
   std::vector<double> mu0, muT, mass;
   std::vector<int> src, dst;
+  std::vector<double> node_cost;  // [L][N] this rank's commodities (NEXT-2), empty = none
 
   // ---- options
   bool opt_graph = true, opt_reorder = true, opt_profile = false;
@@ -946,6 +947,8 @@ size_t layout(mmf_ctx* c, char* base) {
   p.be = at(L.take((T + 1) * N * Lp * se));
   p.u0m = at(L.take(N * Lp * sm));
   p.u0e = at(L.take(N * Lp * se));
+  p.dnm = c->node_cost.empty() ? nullptr : at(L.take(N * Lp * sm));
+  p.dne = c->node_cost.empty() ? nullptr : at(L.take(N * Lp * se));
   if (!c->point) {
     p.mu0m = at(L.take(N * Lp * sm));
     p.mu0e = at(L.take(N * Lp * se));
@@ -1068,6 +1071,17 @@ template <class T_> struct Eng {
   typedef typename T_::M M;
   typedef typename T_::E E;
 
+  // the device pointers for a launch whose output messages are layer `layer`: the commodity node factor D (NEXT-2,
+  // reading R-N) applies at the intermediate layers 1..T-1 only
+  static DevPtrs lay(const mmf_ctx* c, int layer) {
+    DevPtrs d = c->dp;
+    if (layer < 1 || layer > c->T - 1) {
+      d.dnm = nullptr;
+      d.dne = nullptr;
+    }
+    return d;
+  }
+
   static void zero_slot(mmf_ctx* c, cudaStream_t s, void* pm, void* pe) {
     LaunchScope ls(c, K_BOUNDARY, s);
     size_t n = (size_t)c->N * c->Lp;
@@ -1096,7 +1110,7 @@ template <class T_> struct Eng {
     dim3 grid(c->N, c->G);
     for (int t = c->T - 1; t >= 0; --t) {
       LaunchScope ls(c, K_BWD, s);
-      k_bwd<T_><<<grid, c->block, 0, s>>>(c->dp, t);
+      k_bwd<T_><<<grid, c->block, 0, s>>>(lay(c, t), t);
     }
   }
 
@@ -1137,7 +1151,7 @@ template <class T_> struct Eng {
     }
     {
       LaunchScope ls(c, K_UPDATE, s);
-      k_spmm_fwd<T_><<<grid, c->block, 0, s>>>(p, t);
+      k_spmm_fwd<T_><<<grid, c->block, 0, s>>>(lay(c, t + 1), t);
     }
     return MMF_OK;
   }
@@ -1145,7 +1159,7 @@ template <class T_> struct Eng {
   // ---------------- node-tile path (opt_kernels == 2)
   template <int CPT, int MODE, int FMODE> static void launch_fwd(mmf_ctx* c, cudaStream_t s, int t, size_t smem) {
     dim3 grid(c->ntiles, c->pc.ngroup);
-    k_fwd_tile<T_, CPT, MODE, FMODE><<<grid, TILE_THREADS, smem, s>>>(c->dp, c->tm, c->pc, t);
+    k_fwd_tile<T_, CPT, MODE, FMODE><<<grid, TILE_THREADS, smem, s>>>(lay(c, t), c->tm, c->pc, t);
   }
   template <int CPT> static void tiled_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
     const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
@@ -1165,7 +1179,7 @@ template <class T_> struct Eng {
   template <int CPT> static void tiled_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     dim3 grid(c->ntiles, c->pc.ngroup);
     k_bwd_tile<T_, CPT><<<grid, TILE_THREADS, BwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_oa), s>>>(
-        c->dp, c->tm, c->pc, t);
+        lay(c, t), c->tm, c->pc, t);
   }
   template <int CPT> static cudaError_t tiled_attrs_cpt(mmf_ctx* c) {
     const int fwd = (int)FwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_hin, c->max_ia, c->max_oa);
@@ -1190,7 +1204,7 @@ template <class T_> struct Eng {
   // ---------------- wide-lane path (opt_kernels == 3)
   template <int CPT, int MODE, int FMODE> static void launch_fwd_wide(mmf_ctx* c, cudaStream_t s, int t) {
     dim3 grid((c->N + c->wc.npc - 1) / c->wc.npc, c->wc.ngroup);
-    k_fwd_wide<T_, CPT, MODE, FMODE><<<grid, WIDE_THREADS, wide_smem<M>(c->wc.max_oa, c->wc.cpcta), s>>>(c->dp, c->wc, t);
+    k_fwd_wide<T_, CPT, MODE, FMODE><<<grid, WIDE_THREADS, wide_smem<M>(c->wc.max_oa, c->wc.cpcta), s>>>(lay(c, t), c->wc, t);
   }
   template <int CPT> static void wide_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
     const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
@@ -1208,13 +1222,13 @@ template <class T_> struct Eng {
   }
   template <int CPT> static void wide_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     dim3 grid((c->N + c->wc.npc - 1) / c->wc.npc, c->wc.ngroup);
-    k_bwd_wide<T_, CPT><<<grid, WIDE_THREADS, wide_smem<M>(0, 1), s>>>(c->dp, c->wc, t);
+    k_bwd_wide<T_, CPT><<<grid, WIDE_THREADS, wide_smem<M>(0, 1), s>>>(lay(c, t), c->wc, t);
   }
   // ---------------- head-flow register-gather path (opt_kernels == 4)
   template <int CPT, int MODE, bool KEEP> static void launch_fwd_head(mmf_ctx* c, cudaStream_t s, int t) {
     const HeadCfg& h = c->hc;
     dim3 grid((c->N + h.npc - 1) / h.npc);
-    k_fwd_head<T_, CPT, MODE, KEEP><<<grid, h.npc * h.wpn * 32, head_smem<M>(h.max_ia, h.nch), s>>>(c->dp, h, t);
+    k_fwd_head<T_, CPT, MODE, KEEP><<<grid, h.npc * h.wpn * 32, head_smem<M>(h.max_ia, h.nch), s>>>(lay(c, t), h, t);
   }
   template <int CPT> static void head_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
@@ -1237,7 +1251,7 @@ template <class T_> struct Eng {
   }
   template <int CPT> static void head_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     const size_t warps = (size_t)c->N * c->hc.nch;
-    k_bwd_head<T_, CPT><<<(unsigned)((warps + HF_WARPS - 1) / HF_WARPS), HF_WARPS * 32, 0, s>>>(c->dp, c->hc, t);
+    k_bwd_head<T_, CPT><<<(unsigned)((warps + HF_WARPS - 1) / HF_WARPS), HF_WARPS * 32, 0, s>>>(lay(c, t), c->hc, t);
   }
   static void tiled_fwd(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
     LaunchScope ls(c, K_FUSED, s);
@@ -1256,7 +1270,7 @@ template <class T_> struct Eng {
     const PipeCfg5& pc = c->pf;
     const unsigned grid = (unsigned)std::min((c->N + NP - 1) / NP, c->sms);
     k_fwd_pipe<CPT, GW, NG, NP, MODE>
-        <<<grid, fwd_threads<GW, NG, NP>(), NP * pfwd_smem(pc.R, pc.D, pc.SW, NG).total, s>>>(c->dp, pc, t);
+        <<<grid, fwd_threads<GW, NG, NP>(), NP * pfwd_smem(pc.R, pc.D, pc.SW, NG).total, s>>>(lay(c, t), pc, t);
   }
   template <int MODE> static void pipe_fwd_mode(mmf_ctx* c, cudaStream_t s, int t) {
     const int SW = c->pf.SW, gw = c->pf_gw, ng = c->pf_ng, np = c->pf_np;
@@ -1280,12 +1294,12 @@ template <class T_> struct Eng {
     const PipeCfg5& pc = c->pb2;
     const size_t share = (pipe_smem(pc.R, FWD_SD, pc.D, pc.SW).total + 127) / 128 * 128;
     const unsigned grid = (unsigned)std::min((pc.nitems + BWD_NP - 1) / BWD_NP, c->sms);
-    k_bwd_pipe2<CPT><<<grid, BWD_THREADS, BWD_NP * share, s>>>(c->dp, pc, t);
+    k_bwd_pipe2<CPT><<<grid, BWD_THREADS, BWD_NP * share, s>>>(lay(c, t), pc, t);
   }
   template <int CPT> static void pipe_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     const PipeCfg5& pc = c->pb;
     const unsigned grid = (unsigned)std::min(pc.nitems, c->sms);
-    k_bwd_pipe<CPT><<<grid, PIPE_THREADS, pipe_smem(pc.R, pc.SD, pc.D, pc.SW).total, s>>>(c->dp, pc, t);
+    k_bwd_pipe<CPT><<<grid, PIPE_THREADS, pipe_smem(pc.R, pc.SD, pc.D, pc.SW).total, s>>>(lay(c, t), pc, t);
   }
   static void tiled_bwd(mmf_ctx* c, cudaStream_t s, int t) {
     LaunchScope ls(c, K_BWD, s);
@@ -1295,19 +1309,19 @@ template <class T_> struct Eng {
         const unsigned grid = (unsigned)(w.ns * w.nseg);
         const int tma = c->win_tma ? 1 : 0;
         if (c->win_cpt == 4)
-          k_bwd_win<4><<<grid, WIN_THREADS, win_smem<4>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
+          k_bwd_win<4><<<grid, WIN_THREADS, win_smem<4>(w).total, s>>>(lay(c, t), w, c->wdo, c->tmb, tma, t);
         else if (c->win_cpt == 2)
-          k_bwd_win<2><<<grid, WIN_THREADS, win_smem<2>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
+          k_bwd_win<2><<<grid, WIN_THREADS, win_smem<2>(w).total, s>>>(lay(c, t), w, c->wdo, c->tmb, tma, t);
         else
-          k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(c->dp, w, c->wdo, c->tmb, tma, t);
+          k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(lay(c, t), w, c->wdo, c->tmb, tma, t);
         return;
       }
       if (c->ru_bwd) {
         const PipeCfg5& pc = c->pr;
         const unsigned grid = (unsigned)std::min((c->N + RU_NP - 1) / RU_NP, c->sms);
         const size_t sm = RU_NP * ru_smem(pc.R, pc.D, pc.SW).total;
-        if (pc.SW == 1024) k_bwd_reuse<4><<<grid, RU_THREADS, sm, s>>>(c->dp, pc, t);
-        else k_bwd_reuse<2><<<grid, RU_THREADS, sm, s>>>(c->dp, pc, t);
+        if (pc.SW == 1024) k_bwd_reuse<4><<<grid, RU_THREADS, sm, s>>>(lay(c, t), pc, t);
+        else k_bwd_reuse<2><<<grid, RU_THREADS, sm, s>>>(lay(c, t), pc, t);
         return;
       }
       if (c->pipe2_bwd) {
@@ -1804,6 +1818,30 @@ mmf_status finalize(mmf_ctx* ctx) {
     CU(cudaMemcpyAsync((void*)p.pdst, hd.data(), c->L * 4, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync((void*)p.pmass, c->mass.data(), c->L * 8, cudaMemcpyHostToDevice, s));
   }
+  // commodity node factors D[l, j] = exp(-c[l, j] / eps) (NEXT-2), formed in fp64 like K, [N][Lp] internal order;
+  // padded commodities carry D = 1
+  std::vector<char> hDm, hDe;
+  if (!c->node_cost.empty()) {
+    const size_t n = (size_t)N * c->Lp;
+    hDm.assign(n * sm, 0);
+    hDe.assign(n * se, 0);
+    for (int v = 0; v < N; ++v)
+      for (int l = 0; l < c->Lp; ++l) {
+        double m = 1.0;
+        int e = 0;
+        if (l < c->L) k_to_xf(-c->node_cost[(size_t)l * N + v] / c->eps, m, e);
+        const size_t k = (size_t)c->newid[v] * c->Lp + l;
+        if (f32) {
+          ((float*)hDm.data())[k] = (float)m;
+          ((int16_t*)hDe.data())[k] = (int16_t)e;
+        } else {
+          ((double*)hDm.data())[k] = m;
+          ((int32_t*)hDe.data())[k] = e;
+        }
+      }
+    CU(cudaMemcpyAsync((void*)p.dnm, hDm.data(), hDm.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaMemcpyAsync((void*)p.dne, hDe.data(), hDe.size(), cudaMemcpyHostToDevice, s));
+  }
   CU(cudaMemsetAsync(p.err, 0, 8, s));
   CU(cudaMemsetAsync(p.errloc, 0, 8, s));
   // host staging buffers die at return: wait for the copies
@@ -1907,6 +1945,8 @@ static uint64_t problem_hash(const mmf_ctx* c) {
   for (double x : c->cost) f.mixd(x);
   f.mix((uint64_t)c->cap_tv);
   for (double x : c->cap) f.mixd(x);
+  f.mix((uint64_t)c->node_cost.size());
+  for (double x : c->node_cost) f.mixd(x);
   return f.h;
 }
 // W [T][A] (user arc order), then UT = beta_T and U0 (the last a2's source scaling; readouts before the next sweep
@@ -2130,6 +2170,7 @@ mmf_status mmf_set_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, in
   ctx->l_begin = l_begin;
   ctx->L = l_count;
   ctx->point = false;
+  if (ctx->node_cost.size() != (size_t)l_count * N) ctx->node_cost.clear();
   ctx->mu0.assign(mu0, mu0 + (size_t)l_count * N);
   ctx->muT.assign(muT, muT + (size_t)l_count * N);
   ctx->have_marg = true;
@@ -2151,10 +2192,31 @@ mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_beg
   ctx->l_begin = l_begin;
   ctx->L = l_count;
   ctx->point = true;
+  if (ctx->node_cost.size() != (size_t)l_count * ctx->N) ctx->node_cost.clear();
   ctx->src.assign(src, src + l_count);
   ctx->dst.assign(dst, dst + l_count);
   ctx->mass.assign(mass, mass + l_count);
   ctx->have_marg = true;
+  return MMF_OK;
+}
+
+mmf_status mmf_set_node_costs(mmf_ctx* ctx, const double* c) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
+  if (!ctx->have_marg || !ctx->have_cost) return fail(ctx, MMF_ESTATE, "mmf_set_costs and the marginals first");
+  if (!c) {
+    ctx->node_cost.clear();
+    ctx->prepared = false;
+    return MMF_OK;
+  }
+  const size_t n = (size_t)ctx->L * ctx->N;
+  // D = exp(-c / eps) must be representable as an extended-range factor: |c / eps| log2(e) <= ELIM / 2
+  const double lim = 0.5 * ELIM / 1.4426950408889634;
+  for (size_t k = 0; k < n; ++k)
+    if (!std::isfinite(c[k]) || std::fabs(c[k] / ctx->eps) > lim)
+      return fail(ctx, MMF_EINVAL, "node cost not finite or |c / eps| beyond the extended range");
+  ctx->node_cost.assign(c, c + n);
+  ctx->prepared = false;
   return MMF_OK;
 }
 

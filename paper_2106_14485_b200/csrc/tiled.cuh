@@ -169,6 +169,15 @@ __device__ __forceinline__ void norm_lane(const DevPtrs& p, const typename T_::M
     } else {
       xf_norm<M>(s[c], E[c], m, e);
     }
+    if (p.dnm && m != M(0)) {  // commodity node factor of this layer (NEXT-2)
+      const size_t k = (size_t)node * p.Lp + l0 + c;
+      m *= ((const M*)p.dnm)[k];
+      e += (int)((const typename T_::E*)p.dne)[k];
+      if (m >= M(2)) {
+        m *= M(0.5);
+        e += 1;
+      }
+    }
     if (e > ELIM || (m != M(0) && e < -ELIM)) {
       set_error(p, ERR_RANGE, l0 + c, node);
       e = e > 0 ? ELIM : -ELIM;

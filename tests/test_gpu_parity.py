@@ -600,3 +600,53 @@ def test_negative_control_broken_kernel_fails_parity():
         assert max_rel_err(Wg, Wo, W_FLOOR) > 1e-2
     except MMFError:
         pass
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-2: commodity-dependent node costs (the factor D = exp(-c/eps) at the intermediate layers)
+
+def _node_cost(p, scale, seed=0):
+    import dataclasses
+    rng = np.random.default_rng(seed)
+    return dataclasses.replace(p, node_cost=rng.uniform(0.0, scale, size=(p.L, p.N)))
+
+
+@pytest.mark.parametrize("prec,L,marg,opts", [("fp64", 37, "point", {}), ("fp32", 1019, "point", {}),
+                                              ("fp32", 150, "dense", {}), ("fp64", 20, "dense", dict(kernels=1)),
+                                              ("fp32", 150, "point", dict(kernels=2)), ("fp32", 300, "point", dict(kernels=3)),
+                                              ("fp32", 60, "point", dict(kernels=4)), ("fp32", 1019, "point", dict(bwd=2)),
+                                              ("fp32", 2051, "point", {})])
+def test_node_costs_parity(prec, L, marg, opts):
+    """Commodity node costs on every kernel family (pipelined forward/backward, wide-lane incl. the L > 1024 multi-group
+    forward, head-flow, tiles, per-node reference kernels, sliding window) against the oracle (pinned by brute force
+    in tests/test_oracle_pins.py), flows, duals and every statistic."""
+    p = _node_cost(grid_problem(7, 8, 6, L, 0.2, seed=46, cap=(0.3 * max(L, 100) / 100, 1.2 * max(L, 100) / 100),
+                                marginals=marg), 0.5, seed=1)
+    assert_parity(p, 4, prec, options=opts)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "fp64"])
+def test_node_costs_jacobi_readout_and_resume(prec):
+    """Node costs with the Jacobi schedule, the per-commodity flow readout and checkpoint/resume (the state's problem
+    hash covers the node costs: a state of the same problem without them is rejected)."""
+    from oracle import readout_commodity_flows
+    from paper_2106_14485_b200 import MMFError, Solver
+    L = 1019 if prec == "fp32" else 37
+    base = grid_problem(9, 9, 6, L, 0.2, seed=47, cap=(0.3, 1.2))
+    p = _node_cost(base, 0.4, seed=2)
+    assert_parity(p, 3, prec, oracle_kw=dict(schedule="jacobi", theta=0.5), options=dict(schedule=1, theta_milli=500))
+    st = oracle_run(p, 3)
+    with Solver(p, prec=prec) as s:
+        s.sweep(3)
+        Fl = s.commodity_flows(2)
+        assert max_rel_err(Fl, readout_commodity_flows(st, 2), 1e-30 * float(p.mass.max())) < TOL[prec]
+        state = s.save_state()
+    with Solver(p, prec=prec) as s:
+        s.load_state(state)
+        s.sweep(1)
+        F = s.edge_flows()
+    Fo, _ = readout_flows(oracle_run(p, 4))
+    assert max_rel_err(F, Fo, flow_floor(p)) < TOL[prec]
+    with Solver(base, prec=prec) as s:
+        with pytest.raises(MMFError):
+            s.load_state(state)

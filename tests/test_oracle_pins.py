@@ -658,3 +658,102 @@ def test_parity_metric_negative_control():
     j = np.unravel_index(np.argmax(F), F.shape)
     F2[j] *= 1 + 2e-4
     assert max_rel_err(F2, F, flow_floor(p)) > 1e-4
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-2: commodity-dependent node costs c[l, j] at the intermediate layers (reading R-N)
+
+def _with_node_cost(p, seed, scale=1.0, kind="random"):
+    import dataclasses
+    rng = np.random.default_rng(seed)
+    if kind == "random":
+        c = rng.uniform(0.0, scale, size=(p.L, p.N))
+    elif kind == "const":
+        c = np.full((p.L, p.N), scale)
+    elif kind == "per-commodity":
+        c = np.repeat(rng.uniform(0.0, scale, size=(p.L, 1)), p.N, axis=1)
+    else:  # "per-node": the same for every commodity
+        c = np.repeat(rng.uniform(0.0, scale, size=(1, p.N)), p.L, axis=0)
+    return dataclasses.replace(p, node_cost=c)
+
+
+@pytest.mark.parametrize("kw", [MICROS[0], MICROS[1], MICROS[4], MICROS[5], MICROS[6]])
+def test_node_costs_iterates_identical_to_full_tensor_sinkhorn(kw):
+    """P1 with commodity node costs: 10 GS sweeps of prp:sinkhorn whose projections are literal sums of the full
+    tensor M[l, v] = U0 prod_t K_t W_t prod_{t=1}^{T-1} exp(-c[l, v_t]/eps) UT (oracle/brute.py) equal the oracle's
+    message-passing sweeps iterate by iterate, and the readout equals the tensor's projections."""
+    p = _with_node_cost(_micro(kw), seed=7, scale=0.8)
+    st = oracle_init(p)
+    bs = BruteState(p)
+    for k in range(10):
+        oracle_sweep(st)
+        brute_sweep(bs)
+        assert max_rel_err(np.exp(st.lam0), bs.U0, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.omega), bs.W, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.lamT), bs.UT, 1e-300) < 1e-12, k
+    M = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT))
+    F, _ = readout_flows(st)
+    assert max_rel_err(F, arc_flows(p, M), 1e-300) < 1e-12
+    for t in (0, p.T - 1):
+        from oracle.brute import commodity_arc_flows
+        assert max_rel_err(readout_commodity_flows(st, t), commodity_arc_flows(p, M, t), 1e-300) < 1e-12
+    assert abs(stats(st)["mass"] - M.sum()) <= 1e-12 * M.sum()
+
+
+@pytest.mark.parametrize("kind", ["const", "per-commodity"])
+def test_node_costs_gauge_invariance(kind):
+    """A node cost that is the same at every node for a commodity (c[l, j] = g_l) charges every walk of commodity l the
+    same (T-1) g_l: the optimal tensor of each commodity is unchanged up to its scalings, so the flows and capacity
+    duals equal those without node costs after every sweep (to rounding)."""
+    p = grid_problem(3, 4, 6, 3, 0.3, seed=16, cap=(0.1, 0.5))
+    q = _with_node_cost(p, seed=3, scale=0.7, kind=kind)
+    a, b = oracle_init(p), oracle_init(q)
+    for _ in range(6):
+        oracle_sweep(a)
+        oracle_sweep(b)
+        Fa, Wa = readout_flows(a)
+        Fb, Wb = readout_flows(b)
+        assert max_rel_err(Fb, Fa, 1e-300) < 1e-11 and max_rel_err(Wb, Wa, 1e-300) < 1e-11
+    assert np.min(Wa) < 0.99
+
+
+def test_node_costs_commodity_independent_reduce_to_arc_costs():
+    """A node cost that does not depend on the commodity (c[l, j] = g_j) is an arc cost: it equals the problem with
+    time-varying arc costs C_t[a] + g[head(a)] for t = 0..T-2 (and C_{T-1}[a] on the last step, reading R-N), which
+    the oracle solves through the already pinned commodity-independent path: identical flows and duals."""
+    import dataclasses
+    p = grid_problem(3, 4, 6, 3, 0.3, seed=17, cap=(0.1, 0.5))
+    q = _with_node_cost(p, seed=5, scale=0.9, kind="per-node")
+    g = q.node_cost[0]
+    cost = np.broadcast_to(p.cost, (p.T, p.A)).copy()
+    cost[: p.T - 1] += g[p.head][None, :]
+    r = dataclasses.replace(p, cost=cost)
+    a, b = oracle_run(q, 6), oracle_run(r, 6)
+    Fa, Wa = readout_flows(a)
+    Fb, Wb = readout_flows(b)
+    assert max_rel_err(Fa, Fb, 1e-300) < 1e-11 and max_rel_err(Wa, Wb, 1e-300) < 1e-11
+    assert np.min(Wa) < 0.99
+
+
+def test_node_costs_dual_monotone_and_strong_duality():
+    """prp:sinkhorn with K_L: the dual objective (now with the commodity-dependent kernel in <K, U>) is non-decreasing
+    after every block, and at convergence equals the regularised primal of the brute-force tensor whose cost includes
+    the node costs (thm:solution P:777-788)."""
+    p = _with_node_cost(grid_problem(3, 3, 4, 2, 0.5, seed=13, cap=(0.15, 0.4)), seed=9, scale=0.6)
+    st = oracle_init(p)
+    vals = []
+    for _ in range(20):
+        oracle_sweep(st, on_block=lambda kind, t, mass: vals.append(dual_objective(st, mass)))
+    v = np.array(vals)
+    assert np.all(np.diff(v) >= -1e-12 * np.abs(v).max())
+    for _ in range(3000):
+        oracle_sweep(st)
+    M = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT))
+    C = np.array(_cost_tensor(p))
+    for t in range(1, p.T):  # node cost of mode t
+        C = C + p.node_cost.reshape((p.L,) + (1,) * t + (p.N,) + (1,) * (p.T - t))
+    pos = M > 0
+    primal = (C[pos] * M[pos]).sum() + p.eps * (M[pos] * np.log(M[pos]) - M[pos]).sum()
+    phi = dual_objective(st, float(np.exp(st.a[p.T] + st.lamT).sum()))
+    assert stats(st)["cap_violation"] < 1e-12
+    assert abs(primal - phi) <= 1e-9 * abs(phi), (primal, phi)

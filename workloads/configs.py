@@ -62,6 +62,9 @@ class Problem:
     sweeps: int = 10
     coords: Optional[np.ndarray] = None
     meta: dict = dataclasses.field(default_factory=dict)
+    # commodity-dependent node costs c[l, j] (finite), charged to commodity l for every
+    # intermediate layer t = 1..T-1 it spends at node j (reading R-N); None = commodity-independent costs
+    node_cost: Optional[np.ndarray] = None
 
     @property
     def A(self) -> int:
@@ -110,7 +113,7 @@ class Problem:
         """Sub-problem with commodities [l0, l1) (same graph, costs, caps)."""
         kw = dataclasses.asdict(self)
         kw.update(L=l1 - l0, name=f"{self.name}[{l0}:{l1}]")
-        for k in ("src", "dst", "mass", "mu0_dense", "muT_dense"):
+        for k in ("src", "dst", "mass", "mu0_dense", "muT_dense", "node_cost"):
             v = getattr(self, k)
             kw[k] = None if v is None else v[l0:l1].copy()
         return Problem(**kw)
