@@ -142,8 +142,27 @@ def l2_note(p, prec, nl):
             "(small parity config, not the bench workload)")
 
 
+def self_launch(args):
+    """--gpus N without a torchrun environment: launch N ranks here (one per GPU, 127.0.0.1 rendezvous) with the same
+    arguments; rank 0's JSON line passes through."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        sys.exit(self_launch(args))
+    if world_env is not None and int(world_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world_env}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -230,7 +249,7 @@ def main():
             "frac": achieved / peak, "peak_source": peak_kind, "traffic": traffic,
             "share_of_step": kinds[dom]["ms"] / tot_ms,
             "bytes_per_launch": dom_bytes_per_launch, "avg_launch_ms": dom_launch_ms}
-    sweep_gbs = bytes_total / (ms_step / 1e3) / 1e9 * (p.L and (l1 - l0) / p.L or 1)
+    sweep_gbs = bytes_total / (ms_step / 1e3) / 1e9  # (per GPU: mmf_sweep_bytes counts this rank's commodities)
 
     e2e = None
     if not args.no_e2e:

@@ -157,6 +157,16 @@ mmf_status mmf_init(mmf_ctx* ctx);
 /* Enqueue n full sweeps (a2..a5) on the stream.  Async; errors surface at mmf_sync / read_*. */
 mmf_status mmf_sweep(mmf_ctx* ctx, int32_t n);
 
+/* Virtual ranks (the coupling of rem:multi_tensor_scheme P:1139-1147 on one device): ctxs[0..G-1]
+ * (1 <= G <= 8) are initialised contexts of the same problem on the same device and stream, each holding one
+ * commodity slice (mmf_set_*_marginals with l_begin / l_count), no NCCL, option kernels >= 3, Gauss-Seidel.  Runs n
+ * sweeps of all of them together with the multi-GPU exchange path's kernels: per forward step every shard's partial
+ * flows F_t -> a device-side sum in fixed shard order (in place of ncclAllReduce) -> every shard's dual update.  The
+ * capacity duals stay identical across the contexts; each context's edge-flow readout covers its own commodities.
+ * Async, no CUDA graph; errors surface at mmf_sync.  MMF_EINVAL on mismatched contexts, MMF_ESTATE if one is not
+ * initialised. */
+mmf_status mmf_sweep_group(mmf_ctx* const* ctxs, int32_t G, int32_t n);
+
 /* Wait for the stream; report sticky device errors (MMF_EINFEASIBLE / MMF_ERANGE, with the first
  * (commodity, node) in mmf_last_error) and NCCL async errors. */
 mmf_status mmf_sync(mmf_ctx* ctx);

@@ -23,7 +23,7 @@ EXPORTS = ["mmf_create", "mmf_set_graph", "mmf_set_costs", "mmf_set_capacity", "
            "mmf_set_option", "mmf_init", "mmf_sweep", "mmf_sync", "mmf_read_edge_flows", "mmf_read_cap_duals",
            "mmf_read_stats", "mmf_read_kernel_stats", "mmf_sweep_bytes", "mmf_destroy", "mmf_last_error",
            "mmf_version", "mmf_solve", "mmf_state_bytes", "mmf_save_state", "mmf_load_state",
-           "mmf_read_commodity_flows", "mmf_set_node_costs"]
+           "mmf_read_commodity_flows", "mmf_set_node_costs", "mmf_sweep_group"]
 
 
 class MMFError(RuntimeError):
@@ -79,6 +79,7 @@ def load(path: str = None):
         "mmf_read_kernel_stats": ([vp, C.POINTER(C.c_int64), dp, C.c_int], C.c_int),
         "mmf_sweep_bytes": ([vp, dp, dp, C.c_int], C.c_int),
         "mmf_set_node_costs": ([vp, dp], C.c_int),
+        "mmf_sweep_group": ([C.POINTER(vp), i32, i32], C.c_int),
         "mmf_destroy": ([vp], C.c_int),
         "mmf_last_error": ([vp], C.c_char_p),
         "mmf_version": ([], C.c_char_p),
@@ -192,6 +193,12 @@ def mmf_init(ctx):
 
 def mmf_sweep(ctx, n: int):
     _check(ctx, load().mmf_sweep(ctx, int(n)))
+
+
+def mmf_sweep_group(ctxs, n: int):
+    """Virtual ranks: sweep the contexts (commodity shards of one problem on one device) together."""
+    arr = (C.c_void_p * len(ctxs))(*[c.value for c in ctxs])
+    _check(ctxs[0], load().mmf_sweep_group(arr, len(ctxs), int(n)))
 
 
 def mmf_sync(ctx):

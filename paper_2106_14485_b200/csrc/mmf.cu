@@ -189,6 +189,13 @@ mmf_status fail(mmf_ctx* c, mmf_status s, const std::string& msg) {
   return s;
 }
 
+#define CU2(c, call)                                                                               \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess)                                                                         \
+      return fail(c, MMF_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));               \
+  } while (0)
+
 #define CU(call)                                                                                   \
   do {                                                                                             \
     cudaError_t e_ = (call);                                                                       \
@@ -1061,6 +1068,18 @@ struct LaunchScope {
   }
 };
 
+struct VSum {
+  void* f[8];
+};
+// F = sum over the virtual ranks' partial flows (fixed order), written back to every rank's buffer
+template <class M> __global__ void k_vsum(VSum v, int G, int64_t A) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < A; a += (int64_t)gridDim.x * blockDim.x) {
+    M x = M(0);
+    for (int g = 0; g < G; ++g) x += ((const M*)v.f[g])[a];
+    for (int g = 0; g < G; ++g) ((M*)v.f[g])[a] = x;
+  }
+}
+
 inline unsigned grid1d(size_t n, int bs) {
   size_t g = (n + bs - 1) / bs;
   if (g > 148u * 16u) g = 148u * 16u;
@@ -1372,6 +1391,32 @@ template <class T_> struct Eng {
     if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
     LaunchScope ls(c, K_REDUCE, s);
     k_dual<T_><<<(unsigned)((c->A + 255) / 256), 256, 0, s>>>(p, t);
+    return MMF_OK;
+  }
+
+  // virtual ranks: G contexts on one device, each one commodity shard, swept together with the
+  // multi-GPU exchange path's kernels (partial flows of the shard -> sum -> dual update) and a device-side sum in
+  // place of ncclAllReduce (fixed shard order)
+  static mmf_status group_sweep(mmf_ctx* const* cs, int G, cudaStream_t s) {
+    mmf_ctx* c0 = cs[0];
+    VSum vs{};
+    for (int g = 0; g < G; ++g) vs.f[g] = cs[g]->dp.Fsum;
+    const unsigned ga = (unsigned)((c0->A + 255) / 256);
+    for (int t = 0; t <= c0->T; ++t) {
+      for (int g = 0; g < G; ++g) tiled_fwd(cs[g], s, t, 1);  // alpha_t of the shard; its partial F_t -> Fsum
+      if (t < c0->T) {
+        {
+          LaunchScope ls(c0, K_REDUCE, s);
+          k_vsum<M><<<ga, 256, 0, s>>>(vs, G, c0->A);
+        }
+        for (int g = 0; g < G; ++g) {
+          LaunchScope ls(cs[g], K_REDUCE, s);
+          k_dual<T_><<<ga, 256, 0, s>>>(cs[g]->dp, t);
+        }
+      }
+    }
+    for (int g = 0; g < G; ++g)
+      for (int t = c0->T - 1; t >= 0; --t) tiled_bwd(cs[g], s, t);  // a5
     return MMF_OK;
   }
 
@@ -2339,6 +2384,29 @@ mmf_status mmf_sweep(mmf_ctx* ctx, int32_t n) {
   CU(cudaEventRecord(ctx->ev_priv, ctx->priv));
   CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_priv, 0));
   ctx->sweeps += n;
+  return MMF_OK;
+}
+
+mmf_status mmf_sweep_group(mmf_ctx* const* ctxs, int32_t G, int32_t n) {
+  if (!ctxs || G < 1 || G > 8) return MMF_EINVAL;
+  mmf_ctx* c0 = ctxs[0];
+  if (!c0) return MMF_EINVAL;
+  for (int g = 0; g < G; ++g) {
+    mmf_ctx* c = ctxs[g];
+    if (!c || !c->inited) return fail(c0, MMF_ESTATE, "every context must be initialised");
+    if (c->comm) return fail(c0, MMF_EINVAL, "virtual ranks do not use NCCL");
+    if (c->device != c0->device || c->stream != c0->stream || c->prec != c0->prec || c->N != c0->N ||
+        c->A != c0->A || c->T != c0->T || c->opt_schedule != 0 || c->opt_kernels < 3 || c->opt_kernels != c0->opt_kernels)
+      return fail(c0, MMF_EINVAL, "virtual ranks: same device, stream, precision, problem shape; kernels >= 3; GS");
+  }
+  if (n < 0) return fail(c0, MMF_EINVAL, "n < 0");
+  CU2(c0, cudaSetDevice(c0->device));
+  for (int k = 0; k < n; ++k) {
+    mmf_status st = dispatch(c0, [&](auto eng) { return decltype(eng)::group_sweep(ctxs, G, c0->stream); });
+    if (st != MMF_OK) return st;
+  }
+  CU2(c0, cudaGetLastError());
+  for (int g = 0; g < G; ++g) ctxs[g]->sweeps += n;
   return MMF_OK;
 }
 
