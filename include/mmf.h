@@ -103,6 +103,17 @@ mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_beg
  * D = exp(-c/eps) are formed in fp64 and stored like K; stats' "primal" stays the arc-cost term. */
 mmf_status mmf_set_node_costs(mmf_ctx* ctx, const double* c);
 
+/* Per-commodity entry / exit times (rem:multi_tensor_scheme P:1139-1149 and P:692-693:
+ * commodities that enter and leave the network at different times, each with its own transport tensor): commodity l
+ * of this context's slice is in the network on layers t_in[l] .. t_out[l] (0 <= t_in < t_out <= T): its source mass
+ * sits at layer t_in, its sink mass at layer t_out, and it uses no arc outside steps t_in .. t_out - 1.  Point-mass
+ * commodities and a single rank only (else MMF_EINVAL); call after the marginals, before mmf_workspace_bytes /
+ * mmf_init (then the problem is fixed: further set_* calls return MMF_ESTATE).  Realised inside the library by
+ * holding nodes (a source holding node whose release arc exists only at step t_in - 1, a sink holding node whose
+ * absorb arc exists only at step t_out; zero cost, K = 0 at the other steps), which every readout hides: outputs keep the user's [T][n_arcs]
+ * shape and arc order.  NULL clears. */
+mmf_status mmf_set_commodity_times(mmf_ctx* ctx, const int32_t* t_in, const int32_t* t_out);
+
 /* Device bytes needed once graph, costs, capacities and marginals are set. */
 mmf_status mmf_workspace_bytes(const mmf_ctx* ctx, size_t* bytes);
 

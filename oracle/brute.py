@@ -113,3 +113,75 @@ def brute_sweep(bs: BruteState) -> None:
         raise RuntimeError("infeasible sink")
     bs.UT = bs.UT * r
     bs.sweeps += 1
+
+
+# ---------------------------------------------------------------------------------------------------------------
+# NEXT-4 entry / exit times (rem:multi_tensor_scheme P:1139-1149): one transport tensor per commodity l
+# over its own layers t_in[l] .. t_out[l] (eq:multicommodity_tensor_problem), the capacity duals shared.
+
+def commodity_window_tensor(problem, l: int, U0_l, W, UT_l) -> np.ndarray:
+    """M^l[v_{t_in}, ..., v_{t_out}] = U0[v_{t_in}] prod_{t = t_in}^{t_out - 1} KW_t[v_t, v_{t+1}]
+    (x exp(-c[l, v_s]/eps) at the intermediate layers s = 1..T-1 inside the window, s > t_in) UT[v_{t_out}]."""
+    p = problem
+    t0, t1 = int(p.t_in[l]), int(p.t_out[l])
+    nc = getattr(p, "node_cost", None)
+    M = np.asarray(U0_l, float).copy()
+    for t in range(t0, t1):
+        KW = dense_kernel(p, t, W[t])
+        M = M[..., :, None] * KW.reshape((1,) * (M.ndim - 1) + KW.shape)
+        if nc is not None and t + 1 <= p.T - 1:
+            M = M * np.exp(-np.asarray(nc[l], float) / p.eps).reshape((1,) * (M.ndim - 1) + (p.N,))
+    return M * np.asarray(UT_l, float).reshape((1,) * (M.ndim - 1) + (p.N,))
+
+
+class BruteTimes:
+    """Gauss-Seidel Sinkhorn (prp:sinkhorn; the order of eq:Sinkhorn_multi_tensor P:1141-1145: u_1^l, u_t, u_T^l) on
+    the per-commodity window tensors, every projection a literal sum."""
+
+    def __init__(self, problem):
+        p = problem
+        self.p = p
+        self.U0 = np.ones((p.L, p.N))
+        self.W = np.ones((p.T, p.A))
+        self.UT = (p.muT > 0).astype(float)
+
+    def tensors(self):
+        return [commodity_window_tensor(self.p, l, self.U0[l], self.W, self.UT[l]) for l in range(self.p.L)]
+
+    def flows(self):
+        """Aggregate arc flows F_t[a] (zero outside each commodity's window): [T, A]."""
+        p = self.p
+        F = np.zeros((p.T, p.A))
+        for l, M in enumerate(self.tensors()):
+            t0 = int(p.t_in[l])
+            for t in range(t0, int(p.t_out[l])):
+                k = t - t0
+                axes = tuple(x for x in range(M.ndim) if x not in (k, k + 1))
+                B = M.sum(axis=axes)
+                F[t] += B[p.tail, p.head]
+        return F
+
+    def sweep(self):
+        p = self.p
+        for l, M in enumerate(self.tensors()):       # u_1^l blocks: source marginal at layer t_in
+            P0 = M.sum(axis=tuple(range(1, M.ndim)))
+            r = _ratio(p.mu0[l], P0)
+            if np.isinf(r).any():
+                raise RuntimeError("infeasible source")
+            self.U0[l] = self.U0[l] * r
+        for t in range(p.T):                          # u_t blocks: shared capacity duals
+            F = self.flows()[t]
+            cap = np.asarray(p.cap_t(t), float)
+            with np.errstate(invalid="ignore", divide="ignore"):
+                ratio = np.where(F > 0, cap / np.where(F > 0, F, 1.0), np.inf)
+            with np.errstate(invalid="ignore"):
+                neww = np.minimum(self.W[t] * ratio, 1.0)
+            neww = np.where(cap == 0, 0.0, neww)
+            neww = np.where(np.isinf(cap), 1.0, neww)
+            self.W[t] = neww
+        for l, M in enumerate(self.tensors()):       # u_T^l blocks: sink marginal at layer t_out
+            PT = M.sum(axis=tuple(range(M.ndim - 1)))
+            r = _ratio(p.muT[l], PT)
+            if np.isinf(r).any():
+                raise RuntimeError("infeasible sink")
+            self.UT[l] = self.UT[l] * r

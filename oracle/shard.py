@@ -27,6 +27,7 @@ def shard_pieces(st: OracleState) -> dict:
     """This shard's additive contributions to the end-of-sweep statistics:
     its edge flows, tensor mass, marginal L1 mismatches and the dual's commodity terms."""
     p = st.problem
+    assert st.t_in is None and st.t_out is None, "sharded fixtures: no commodity times"
     F, _ = readout_flows(st)
     PT = np.exp(st.a[p.T] + st.lamT)          # (both stores hold a_T after a pass)
     P0 = np.exp(st.lam0 + st.b[0])

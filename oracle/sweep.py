@@ -104,6 +104,21 @@ class OracleState:
     sweeps: int = 0
     keep_forward: bool = True   # False: ``a`` holds only the two latest layers (see _TwoLayers)
     lD: Optional[np.ndarray] = None  # [L, N] -c[l, j]/eps, commodity node costs (NEXT-2), or None
+    t_in: Optional[np.ndarray] = None   # [L] entry layer of each commodity (NEXT-4 entry/exit times), or None = 0
+    t_out: Optional[np.ndarray] = None  # [L] exit layer, or None = T
+
+
+def _at_layers(arr, layers: np.ndarray) -> np.ndarray:
+    """[L, N] slice of a [T+1, L, N] message store taking commodity l at layer layers[l]."""
+    return arr[layers, np.arange(layers.size)]
+
+
+def _src_layer(st) -> np.ndarray:
+    return st.t_in if st.t_in is not None else np.zeros(st.problem.L, np.int64)
+
+
+def _sink_layer(st) -> np.ndarray:
+    return st.t_out if st.t_out is not None else np.full(st.problem.L, st.problem.T, np.int64)
 
 
 def _layer_cost(st: "OracleState", t: int):
@@ -163,6 +178,13 @@ def oracle_init(problem, b_store: Optional[np.ndarray] = None, keep_forward: boo
         in_seg=_segments(p.head.astype(np.int64), N), out_seg=_segments(p.tail.astype(np.int64), N),
         keep_forward=keep_forward,
         lD=None if getattr(p, "node_cost", None) is None else -np.asarray(p.node_cost, np.float64) / float(p.eps))
+    if getattr(p, "t_in", None) is not None or getattr(p, "t_out", None) is not None:
+        # NEXT-4 entry / exit times (rem:multi_tensor_scheme P:1139-1149): commodity l's transport tensor
+        # spans the layers t_in[l] .. t_out[l]; its source scaling sits at layer t_in[l], its sink scaling at t_out[l]
+        assert keep_forward, "commodity times need the kept forward store"
+        st.t_in = np.zeros(L, np.int64) if p.t_in is None else np.asarray(p.t_in, np.int64)
+        st.t_out = np.full(L, T, np.int64) if p.t_out is None else np.asarray(p.t_out, np.int64)
+        assert np.all((0 <= st.t_in) & (st.t_in < st.t_out) & (st.t_out <= T))
     backward(st)
     return st
 
@@ -173,10 +195,14 @@ def backward(st: OracleState) -> None:
     p = st.problem
     o = st.out_seg[0]
     head_o = p.head[o]
-    st.b[p.T] = st.lamT
+    tout = _sink_layer(st)
+    st.b[p.T] = np.where((tout == p.T)[:, None], st.lamT, NEG_INF)
     for t in range(p.T - 1, -1, -1):
         X = (st.lK[t][o] + st.omega[t][o])[None, :] + (st.b[t + 1] + _layer_cost(st, t + 1))[:, head_o]
         st.b[t] = seg_lse(X, st.out_seg)
+        if st.t_out is not None and np.any(tout == t):  # commodities leaving at layer t: beta_t = UT there
+            sel = tout == t
+            st.b[t][sel] = st.lamT[sel]
 
 
 def _boundary(log_mu: np.ndarray, msg: np.ndarray, where: str) -> np.ndarray:
@@ -201,6 +227,32 @@ def capacity_update(logd_t: np.ndarray, log_ks: np.ndarray) -> np.ndarray:
     return om
 
 
+def _enter(st: OracleState, t: int) -> None:
+    """Commodities entering at layer t (t_in = t > 0): alpha_t = U0 there (their alpha below t_in is zero, so the
+    recursion left -inf in place)."""
+    if st.t_in is not None and np.any(st.t_in == t):
+        sel = st.t_in == t
+        st.a[t][sel] = st.lam0[sel]
+
+
+def _mass_now(st: OracleState, t: int, X: Optional[np.ndarray] = None) -> float:
+    """Mass <K, U> of the current tensor during a sweep (after the U0 block: t = -1; after W_t: t; after UT: T), per
+    commodity from the layer where its messages are current: before its window (t < t_in) lam0 + beta_{t_in}; inside,
+    the step-t flows sum_a F^l_t[a] (X are the step's log terms without W); after it (t >= t_out) alpha_{t_out} + lamT."""
+    p = st.problem
+    tin, tout = _src_layer(st), _sink_layer(st)
+    m = np.zeros(p.L)
+    pre = np.exp(st.lam0 + _at_layers(st.b, tin)).sum(axis=1)
+    if t < 0:
+        return float(pre.sum())
+    post = np.exp(_at_layers(st.a, tout) + st.lamT).sum(axis=1)
+    if t >= p.T:
+        return float(post.sum())
+    inside = np.exp(X + st.omega[t][None, :]).sum(axis=1)
+    m = np.where(t < tin, pre, np.where(t >= tout, post, inside))
+    return float(m.sum())
+
+
 def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
                  reduce_lse: Optional[Callable] = None) -> None:
     """One Gauss-Seidel sweep in Algorithm 2's order.
@@ -214,11 +266,12 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
     p = st.problem
     oi = st.in_seg[0]
     tail_i = p.tail[oi]
-    # a2: U^(0,1) <- R^(0,1) ./ Psi_1
-    st.lam0 = _boundary(st.log_mu0, st.b[0], "source")
-    st.a[0] = st.lam0
+    tin, tout = _src_layer(st), _sink_layer(st)
+    # a2: U^(0,1) <- R^(0,1) ./ Psi_1, at each commodity's entry layer
+    st.lam0 = _boundary(st.log_mu0, _at_layers(st.b, tin) if st.t_in is not None else st.b[0], "source")
+    st.a[0] = st.lam0 if st.t_in is None else np.where((tin == 0)[:, None], st.lam0, NEG_INF)
     if on_block is not None:
-        on_block("U0", -1, float(np.exp(st.a[0] + st.b[0]).sum()))
+        on_block("U0", -1, _mass_now(st, -1))
     # a3: forward loop
     for t in range(p.T):
         X = st.a[t][:, p.tail] + st.lK[t][None, :] + (st.b[t + 1] + _layer_cost(st, t + 1))[:, p.head]  # no W
@@ -227,13 +280,15 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
             lse = reduce_lse(lse)
         st.omega[t] = capacity_update(st.logd[t], lse)
         if on_block is not None:
-            on_block("W", t, float(np.exp(X + st.omega[t][None, :]).sum()))
+            on_block("W", t, float(np.exp(X + st.omega[t][None, :]).sum()) if st.t_in is None and st.t_out is None
+                     else _mass_now(st, t, X))
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
         st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)           # Psi-hat_{t+1}
-    # a4: U^(0,T) <- R^(0,T) ./ Psi-hat_T
-    st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
+        _enter(st, t + 1)
+    # a4: U^(0,T) <- R^(0,T) ./ Psi-hat_T, at each commodity's exit layer
+    st.lamT = _boundary(st.log_muT, _at_layers(st.a, tout) if st.t_out is not None else st.a[p.T], "sink")
     if on_block is not None:
-        on_block("UT", p.T, float(np.exp(st.a[p.T] + st.lamT).sum()))
+        on_block("UT", p.T, _mass_now(st, p.T))
     # a5: backward recompute
     backward(st)
     st.sweeps += 1
@@ -257,8 +312,9 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     p = st.problem
     oi = st.in_seg[0]
     tail_i = p.tail[oi]
-    st.lam0 = _boundary(st.log_mu0, st.b[0], "source")
-    st.a[0] = st.lam0
+    tin, tout = _src_layer(st), _sink_layer(st)
+    st.lam0 = _boundary(st.log_mu0, _at_layers(st.b, tin) if st.t_in is not None else st.b[0], "source")
+    st.a[0] = st.lam0 if st.t_in is None else np.where((tin == 0)[:, None], st.lam0, NEG_INF)
     new_omega = np.empty_like(st.omega)
     for t in range(p.T):
         X = st.a[t][:, p.tail] + st.lK[t][None, :] + (st.b[t + 1] + _layer_cost(st, t + 1))[:, p.head]
@@ -266,16 +322,19 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
         new_omega[t] = damped_update(st.omega[t], full, theta)
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]   # (the previous W_t)
         st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)
+        _enter(st, t + 1)
     st.omega = new_omega
-    st.lamT = _boundary(st.log_muT, st.a[p.T], "sink")
+    st.lamT = _boundary(st.log_muT, _at_layers(st.a, tout) if st.t_out is not None else st.a[p.T], "sink")
     backward(st)
     # readouts (edge flows, mass) are projections of the end-of-sweep tensor M(U0, W, UT): keep the forward
     # messages of that tensor, i.e. recomputed with the new W (under Gauss-Seidel the pass's own messages
     # already are; DESIGN.md §2 reading R-J)
-    st.a[0] = st.lam0          # (unchanged in the kept store; the two-layer store has overwritten slot 0)
+    # (unchanged in the kept store; the two-layer store has overwritten slot 0)
+    st.a[0] = st.lam0 if st.t_in is None else np.where((tin == 0)[:, None], st.lam0, NEG_INF)
     for t in range(p.T):
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
         st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)
+        _enter(st, t + 1)
     st.sweeps += 1
 
 
@@ -303,6 +362,7 @@ def forward_layers(st: OracleState, t_stop: Optional[int] = None):
         for t in range(t_stop + 1):
             yield t, st.a[t]
         return
+    assert st.t_in is None, "commodity times need the kept forward store"
     cur = st.lam0                       # a_0 = lam0 (all -inf before the first sweep)
     oi = st.in_seg[0]
     tail_i = p.tail[oi]
@@ -363,9 +423,10 @@ def stats(st: OracleState) -> dict:
     F, W = readout_flows(st)
     cost = np.broadcast_to(p.cost, F.shape)
     cap = np.broadcast_to(p.cap, F.shape)
-    mass = float(np.exp(st.a[p.T] + st.lamT).sum())
-    P0 = np.exp(st.lam0 + st.b[0])              # source marginal of the end-of-sweep tensor
-    PT = np.exp(st.a[p.T] + st.lamT)            # sink marginal
+    # source / sink marginals of the end-of-sweep tensor (at each commodity's entry / exit layer)
+    P0 = np.exp(st.lam0 + (_at_layers(st.b, st.t_in) if st.t_in is not None else st.b[0]))
+    PT = np.exp((_at_layers(st.a, st.t_out) if st.t_out is not None else st.a[p.T]) + st.lamT)
+    mass = float(PT.sum())
     return {
         "mass": mass,
         "primal": float((cost * F).sum()),

@@ -23,7 +23,8 @@ EXPORTS = ["mmf_create", "mmf_set_graph", "mmf_set_costs", "mmf_set_capacity", "
            "mmf_set_option", "mmf_init", "mmf_sweep", "mmf_sync", "mmf_read_edge_flows", "mmf_read_cap_duals",
            "mmf_read_stats", "mmf_read_kernel_stats", "mmf_sweep_bytes", "mmf_destroy", "mmf_last_error",
            "mmf_version", "mmf_solve", "mmf_state_bytes", "mmf_save_state", "mmf_load_state",
-           "mmf_read_commodity_flows", "mmf_set_node_costs", "mmf_sweep_group"]
+           "mmf_read_commodity_flows", "mmf_set_node_costs", "mmf_sweep_group",
+           "mmf_set_commodity_times"]
 
 
 class MMFError(RuntimeError):
@@ -80,6 +81,7 @@ def load(path: str = None):
         "mmf_sweep_bytes": ([vp, dp, dp, C.c_int], C.c_int),
         "mmf_set_node_costs": ([vp, dp], C.c_int),
         "mmf_sweep_group": ([C.POINTER(vp), i32, i32], C.c_int),
+        "mmf_set_commodity_times": ([vp, ip, ip], C.c_int),
         "mmf_destroy": ([vp], C.c_int),
         "mmf_last_error": ([vp], C.c_char_p),
         "mmf_version": ([], C.c_char_p),
@@ -158,6 +160,15 @@ def mmf_set_node_costs(ctx, c):
         return
     c = _f64(c)
     _check(ctx, load().mmf_set_node_costs(ctx, _p(c, C.c_double)))
+
+
+def mmf_set_commodity_times(ctx, t_in, t_out):
+    """Per-commodity entry / exit layers of this context's commodities (None clears)."""
+    if t_in is None:
+        _check(ctx, load().mmf_set_commodity_times(ctx, None, None))
+        return
+    t_in, t_out = _i32(t_in), _i32(t_out)
+    _check(ctx, load().mmf_set_commodity_times(ctx, _p(t_in, C.c_int32), _p(t_out, C.c_int32)))
 
 
 def mmf_workspace_bytes(ctx) -> int:

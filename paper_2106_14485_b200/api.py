@@ -63,6 +63,10 @@ class Solver:
             L.mmf_set_marginals(self.ctx, p.L, l_begin, p.mu0[sl], p.muT[sl])
         if getattr(p, "node_cost", None) is not None:
             L.mmf_set_node_costs(self.ctx, p.node_cost[sl])
+        if getattr(p, "t_in", None) is not None or getattr(p, "t_out", None) is not None:
+            t_in = np.zeros(p.L, np.int32) if p.t_in is None else np.asarray(p.t_in, np.int32)
+            t_out = np.full(p.L, p.T, np.int32) if p.t_out is None else np.asarray(p.t_out, np.int32)
+            L.mmf_set_commodity_times(self.ctx, t_in[sl], t_out[sl])
 
     def sweep(self, n: int = 1):
         L.mmf_sweep(self.ctx, n)

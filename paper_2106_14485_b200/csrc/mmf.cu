@@ -91,6 +91,15 @@ struct mmf_ctx {
   std::vector<double> mu0, muT, mass;
   std::vector<int> src, dst;
   std::vector<double> node_cost;  // [L][N] this rank's commodities (NEXT-2), empty = none
+  // NEXT-4 entry / exit times (point-mass commodities): t_in / t_out per commodity, empty = 0 / T.  Realised by
+  // augmenting the graph before the first layout (augment_times): per commodity a source holding node (its loop and
+  // a release arc to the source that exists only at step t_in - 1) and a sink holding node (an absorb arc from the sink that exists
+  // only at step t_out, and its loop); user arcs keep their positions, readouts cover them only.
+  std::vector<int> t_in, t_out;
+  bool augmented = false;
+  int N_user = 0;
+  int64_t A_user = 0;
+  std::vector<double> cost_user, cap_user;  // (the user's arrays: primal / violation in mmf_read_stats)
 
   // ---- options
   bool opt_graph = true, opt_reorder = true, opt_profile = false;
@@ -795,8 +804,74 @@ bool make_tmaps(mmf_ctx* c, void* msig, void* mexp, int slots, int SW, WinTmaps&
   return true;
 }
 
+void augment_times(mmf_ctx* c) {
+  if (c->augmented) return;
+  c->N_user = c->N;
+  c->A_user = c->A;
+  c->cost_user = c->cost;
+  c->cap_user = c->cap;
+  if (c->t_in.empty()) return;
+  const int T = c->T;
+  const int64_t A0 = c->A;
+  std::vector<int> ta, ha;                 // appended arcs
+  std::vector<std::vector<double>> costa;  // their per-step costs: 0 when open, +inf (absent, K = 0) otherwise
+  auto arc = [&](int u, int v, int open_step) {  // open_step < 0: always open
+    ta.push_back(u);
+    ha.push_back(v);
+    std::vector<double> cp(T, INFINITY);
+    for (int t = 0; t < T; ++t)
+      if (open_step < 0 || t == open_step) cp[t] = 0.0;
+    costa.push_back(cp);
+  };
+  int N = c->N;
+  for (int l = 0; l < c->L; ++l) {
+    if (c->t_in[l] > 0) {
+      const int h = N++;
+      arc(h, h, -1);
+      arc(h, c->src[l], c->t_in[l] - 1);
+      c->src[l] = h;
+    }
+    if (c->t_out[l] < T) {
+      const int g = N++;
+      arc(c->dst[l], g, c->t_out[l]);
+      arc(g, g, -1);
+      c->dst[l] = g;
+    }
+  }
+  const int64_t A1 = A0 + (int64_t)ta.size();
+  c->tail.insert(c->tail.end(), ta.begin(), ta.end());
+  c->head.insert(c->head.end(), ha.begin(), ha.end());
+  // costs become per step (the appended arcs exist at their open steps only: cost +inf = absent from the graph,
+  // P:691, so K = 0 there from the start, as in the native multi-tensor form); capacities: the appended arcs are free
+  std::vector<double> cc((size_t)T * A1);
+  for (int t = 0; t < T; ++t) {
+    for (int64_t a = 0; a < A0; ++a) cc[(size_t)t * A1 + a] = c->cost[(c->cost_tv ? (size_t)t * A0 : 0) + a];
+    for (size_t q = 0; q < ta.size(); ++q) cc[(size_t)t * A1 + A0 + q] = costa[q][t];
+  }
+  c->cost.swap(cc);
+  c->cost_tv = true;
+  if (c->cap_tv) {
+    std::vector<double> kc((size_t)T * A1, INFINITY);
+    for (int t = 0; t < T; ++t) std::copy(c->cap.begin() + (size_t)t * A0, c->cap.begin() + (size_t)(t + 1) * A0, kc.begin() + (size_t)t * A1);
+    c->cap.swap(kc);
+  } else {
+    c->cap.resize(A1, INFINITY);
+  }
+  // node costs: 0 at the holding nodes
+  if (!c->node_cost.empty()) {
+    std::vector<double> nc((size_t)c->L * N, 0.0);
+    for (int l = 0; l < c->L; ++l)
+      std::copy(c->node_cost.begin() + (size_t)l * c->N, c->node_cost.begin() + (size_t)(l + 1) * c->N, nc.begin() + (size_t)l * N);
+    c->node_cost.swap(nc);
+  }
+  c->N = N;
+  c->A = A1;
+  c->augmented = true;
+}
+
 void prepare(mmf_ctx* c) {
   if (c->prepared) return;
+  augment_times(c);
   const int N = c->N;
   const int64_t A = c->A;
   std::vector<int> order;
@@ -1795,9 +1870,10 @@ mmf_status finalize(mmf_ctx* ctx) {
   std::vector<int> hKe((size_t)TK * A);
   for (int t = 0; t < TK; ++t)
     for (int64_t a = 0; a < A; ++a) {
-      double m;
-      int e;
-      k_to_xf(-c->cost[(size_t)t * A + a] / c->eps, m, e);
+      double m = 0.0;
+      int e = 0;
+      const double ca = c->cost[(size_t)t * A + a];
+      if (std::isfinite(ca)) k_to_xf(-ca / c->eps, m, e);  // (+inf: an arc absent at this step, K = 0)
       size_t k = (size_t)t * A + c->int_of_arc[a];
       if (f32)
         ((float*)hKm.data())[k] = (float)m;
@@ -1903,17 +1979,17 @@ namespace mmf {
 // readouts in user arc order, converted to fp64 on the device ([T][A]: t * A + user arc <- t * A + internal arc)
 template <class M>
 __global__ void k_export_flows(const M* __restrict__ src, const int* __restrict__ ioa, double* __restrict__ out,
-                               int64_t A, int64_t n) {
+                               int64_t A, int64_t Au, int64_t n) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = k / A, a = k - t * A;
+    const int64_t t = k / Au, a = k - t * Au;  // (Au = user arcs: the first Au of the A internal ones' user order)
     out[k] = (double)src[t * A + ioa[a]];
   }
 }
 template <class M>
 __global__ void k_export_duals(const M* __restrict__ wm, const int* __restrict__ we, const int* __restrict__ ioa,
-                               double* __restrict__ out, int64_t A, int64_t n) {
+                               double* __restrict__ out, int64_t A, int64_t Au, int64_t n) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = k / A, a = k - t * A;
+    const int64_t t = k / Au, a = k - t * Au;
     const int64_t i = t * A + ioa[a];
     const double m = (double)wm[i];
     out[k] = m == 0.0 ? 0.0 : ldexp(m, we[i]);  // (values below 2^-1074 read 0)
@@ -1930,7 +2006,7 @@ static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
   }
   mmf_status st = mmf_sync(ctx);
   if (st != MMF_OK) return st;
-  const int64_t A = ctx->A, n = (int64_t)ctx->T * A;
+  const int64_t A = ctx->A, Au = ctx->A_user, n = (int64_t)ctx->T * Au;
   if (!ctx->d_int_of_arc) {
     CU(cudaMalloc(&ctx->d_int_of_arc, (size_t)A * sizeof(int)));
     CU(cudaMemcpy(ctx->d_int_of_arc, ctx->int_of_arc.data(), (size_t)A * sizeof(int), cudaMemcpyHostToDevice));
@@ -1939,11 +2015,11 @@ static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
   double* d = ctx->d_export;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 8 * 148);
   if (ctx->prec == MMF_FP32) {
-    if (what == 0) k_export_flows<float><<<grid, 256, 0, ctx->stream>>>((const float*)ctx->dp.Fout, ctx->d_int_of_arc, d, A, n);
-    else k_export_duals<float><<<grid, 256, 0, ctx->stream>>>((const float*)ctx->dp.Wm, ctx->dp.We, ctx->d_int_of_arc, d, A, n);
+    if (what == 0) k_export_flows<float><<<grid, 256, 0, ctx->stream>>>((const float*)ctx->dp.Fout, ctx->d_int_of_arc, d, A, Au, n);
+    else k_export_duals<float><<<grid, 256, 0, ctx->stream>>>((const float*)ctx->dp.Wm, ctx->dp.We, ctx->d_int_of_arc, d, A, Au, n);
   } else {
-    if (what == 0) k_export_flows<double><<<grid, 256, 0, ctx->stream>>>((const double*)ctx->dp.Fout, ctx->d_int_of_arc, d, A, n);
-    else k_export_duals<double><<<grid, 256, 0, ctx->stream>>>((const double*)ctx->dp.Wm, ctx->dp.We, ctx->d_int_of_arc, d, A, n);
+    if (what == 0) k_export_flows<double><<<grid, 256, 0, ctx->stream>>>((const double*)ctx->dp.Fout, ctx->d_int_of_arc, d, A, Au, n);
+    else k_export_duals<double><<<grid, 256, 0, ctx->stream>>>((const double*)ctx->dp.Wm, ctx->dp.We, ctx->d_int_of_arc, d, A, Au, n);
   }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
@@ -2129,6 +2205,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
 
 mmf_status mmf_set_graph(mmf_ctx* ctx, int32_t N, int64_t n_arcs, const int32_t* tail, const int32_t* head) {
   if (!ctx) return MMF_EINVAL;
+  if (ctx->augmented) return fail(ctx, MMF_ESTATE, "problem fixed once the layout was taken with commodity times");
   if (ctx->inited) return fail(ctx, MMF_ESTATE, "graph already initialised");
   if (N < 1) return fail(ctx, MMF_EINVAL, "N must be >= 1");
   if (n_arcs < 1 || n_arcs > (int64_t)0x7fffffff) return fail(ctx, MMF_EINVAL, "n_arcs out of range");
@@ -2153,6 +2230,7 @@ mmf_status mmf_set_graph(mmf_ctx* ctx, int32_t N, int64_t n_arcs, const int32_t*
 
 mmf_status mmf_set_costs(mmf_ctx* ctx, int32_t T, double eps, const double* cost, int time_varying) {
   if (!ctx) return MMF_EINVAL;
+  if (ctx->augmented) return fail(ctx, MMF_ESTATE, "problem fixed once the layout was taken with commodity times");
   if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
   if (ctx->N == 0) return fail(ctx, MMF_ESTATE, "mmf_set_graph first");
   if (T < 1) return fail(ctx, MMF_EINVAL, "T must be >= 1");
@@ -2172,6 +2250,7 @@ mmf_status mmf_set_costs(mmf_ctx* ctx, int32_t T, double eps, const double* cost
 
 mmf_status mmf_set_capacity(mmf_ctx* ctx, const double* cap, int time_varying) {
   if (!ctx) return MMF_EINVAL;
+  if (ctx->augmented) return fail(ctx, MMF_ESTATE, "problem fixed once the layout was taken with commodity times");
   if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
   if (!ctx->have_cost) return fail(ctx, MMF_ESTATE, "mmf_set_costs first");
   if (!cap) return fail(ctx, MMF_EINVAL, "cap NULL");
@@ -2186,6 +2265,7 @@ mmf_status mmf_set_capacity(mmf_ctx* ctx, const double* cap, int time_varying) {
 
 static mmf_status check_slice(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, int32_t l_count) {
   if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
+  if (ctx->augmented) return fail(ctx, MMF_ESTATE, "problem fixed once the layout was taken with commodity times");
   if (ctx->N == 0) return fail(ctx, MMF_ESTATE, "mmf_set_graph first");
   if (L_global < 1 || l_count < 1 || l_begin < 0 || l_begin + l_count > L_global)
     return fail(ctx, MMF_EINVAL, "bad commodity slice");
@@ -2247,6 +2327,7 @@ mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_beg
 
 mmf_status mmf_set_node_costs(mmf_ctx* ctx, const double* c) {
   if (!ctx) return MMF_EINVAL;
+  if (ctx->augmented) return fail(ctx, MMF_ESTATE, "problem fixed once the layout was taken with commodity times");
   if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
   if (!ctx->have_marg || !ctx->have_cost) return fail(ctx, MMF_ESTATE, "mmf_set_costs and the marginals first");
   if (!c) {
@@ -2261,6 +2342,26 @@ mmf_status mmf_set_node_costs(mmf_ctx* ctx, const double* c) {
     if (!std::isfinite(c[k]) || std::fabs(c[k] / ctx->eps) > lim)
       return fail(ctx, MMF_EINVAL, "node cost not finite or |c / eps| beyond the extended range");
   ctx->node_cost.assign(c, c + n);
+  ctx->prepared = false;
+  return MMF_OK;
+}
+
+mmf_status mmf_set_commodity_times(mmf_ctx* ctx, const int32_t* t_in, const int32_t* t_out) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited || ctx->augmented) return fail(ctx, MMF_ESTATE, "commodity times must be set before the layout");
+  if (!ctx->have_marg || !ctx->have_cost) return fail(ctx, MMF_ESTATE, "mmf_set_costs and the marginals first");
+  if (!t_in || !t_out) {
+    ctx->t_in.clear();
+    ctx->t_out.clear();
+    return MMF_OK;
+  }
+  if (!ctx->point) return fail(ctx, MMF_EINVAL, "commodity times need point-mass commodities");
+  if (ctx->comm) return fail(ctx, MMF_EINVAL, "commodity times: single rank (the holding nodes are per commodity)");
+  for (int l = 0; l < ctx->L; ++l)
+    if (!(t_in[l] >= 0 && t_in[l] < t_out[l] && t_out[l] <= ctx->T))
+      return fail(ctx, MMF_EINVAL, "commodity " + std::to_string(l + ctx->l_begin) + ": need 0 <= t_in < t_out <= T");
+  ctx->t_in.assign(t_in, t_in + ctx->L);
+  ctx->t_out.assign(t_out, t_out + ctx->L);
   ctx->prepared = false;
   return MMF_OK;
 }
@@ -2312,6 +2413,7 @@ mmf_status mmf_attach_nccl(mmf_ctx* ctx, const void* unique_id128, int nranks, i
   if (!ctx || !unique_id128) return MMF_EINVAL;
   if (ctx->inited) return fail(ctx, MMF_ESTATE, "attach NCCL before mmf_init");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(ctx, MMF_EINVAL, "bad nranks/rank");
+  if (!ctx->t_in.empty()) return fail(ctx, MMF_EINVAL, "commodity times: single rank");
   NcclApi& api = nccl_api();
   if (!api.ok) return fail(ctx, MMF_ENCCL, "libnccl.so.2 not found in the process");
   NcclUid uid;
@@ -2485,7 +2587,8 @@ mmf_status mmf_read_commodity_flows(mmf_ctx* ctx, int32_t t, double* out) {
   CU(cudaMalloc(&d, (size_t)n * sizeof(double)));
   st = dispatch(ctx, [&](auto eng) { return decltype(eng)::commodity_flows(ctx, ctx->stream, t, d); });
   cudaError_t e = st == MMF_OK ? cudaGetLastError() : cudaSuccess;
-  if (st == MMF_OK && e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (st == MMF_OK && e == cudaSuccess)
+    e = cudaMemcpyAsync(out, d, (size_t)ctx->A_user * ctx->L * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
   if (st == MMF_OK && e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
   cudaFree(d);
   if (st != MMF_OK) return st;
@@ -2615,7 +2718,7 @@ mmf_status mmf_load_state(mmf_ctx* ctx, const void* buf, size_t bytes) {
 mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {
   if (!ctx || !out) return MMF_EINVAL;
   if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
-  const size_t TA = (size_t)ctx->T * ctx->A;
+  const size_t TA = (size_t)ctx->T * ctx->A_user;
   std::vector<double> F(TA);
   mmf_status st = mmf_read_edge_flows(ctx, F.data());  // also leaves alpha_T of the end-of-sweep state
   if (st != MMF_OK) return st;
@@ -2630,12 +2733,13 @@ mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {
   double s[8];
   CU(cudaMemcpy(s, ctx->dp.stats, sizeof s, cudaMemcpyDeviceToHost));
   double primal = 0, viol = 0;
-  const int64_t A = ctx->A;
+  const int64_t A = ctx->A_user;  // (user arcs; the user's cost / capacity arrays)
+  const bool ctv = ctx->cost_user.size() > (size_t)A, ktv = ctx->cap_user.size() > (size_t)A;
   for (int t = 0; t < ctx->T; ++t)
     for (int64_t a = 0; a < A; ++a) {
       const double f = F[(size_t)t * A + a];
-      primal += ctx->cost[(ctx->cost_tv ? (size_t)t * A : 0) + a] * f;
-      const double d = ctx->cap[(ctx->cap_tv ? (size_t)t * A : 0) + a];
+      primal += ctx->cost_user[(ctv ? (size_t)t * A : 0) + a] * f;
+      const double d = ctx->cap_user[(ktv ? (size_t)t * A : 0) + a];
       if (std::isfinite(d)) viol = std::max(viol, f - d);
     }
   out->sweeps = ctx->sweeps;

@@ -682,3 +682,39 @@ def test_virtual_ranks_equal_unsharded(prec, L, G, marg):
     Fo, Wo, _ = run_oracle(p, 5)
     assert max_rel_err(F, Fo, flow_floor(p)) < TOL[prec] and max_rel_err(Ws[0], Wo, W_FLOOR) < TOL[prec]
     assert np.min(Wo) < 0.99
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-4: per-commodity entry / exit times
+
+def _times(p, seed, T):
+    """Horizon T with every commodity's window at least as long as the horizon its OD pair was drawn for (p.T)."""
+    import dataclasses
+    rng = np.random.default_rng(seed)
+    t_in = rng.integers(0, T - p.T + 1, size=p.L)
+    t_out = np.minimum(t_in + p.T + rng.integers(0, 2, size=p.L), T)
+    return dataclasses.replace(p, T=T, t_in=t_in, t_out=t_out)
+
+
+@pytest.mark.parametrize("prec,L,opts", [("fp64", 23, {}), ("fp32", 1019, {}), ("fp32", 150, dict(kernels=1)),
+                                        ("fp32", 300, dict(kernels=3)), ("fp32", 1019, dict(schedule=1, theta_milli=500))])
+def test_commodity_times_parity(prec, L, opts):
+    """Commodities entering and leaving at their own layers (the library's holding-node construction, hidden from the
+    readouts) against the oracle's native multi-tensor sweep (pinned by per-commodity window tensors), flows, duals and
+    statistics; flows of a commodity vanish outside its window."""
+    p = _times(grid_problem(8, 8, 8, L, 0.2, seed=49, cap=(0.3 * max(L, 100) / 100, 1.2 * max(L, 100) / 100)), seed=3,
+               T=12)
+    assert np.any(p.t_in > 0) and np.any(p.t_out < p.T)
+    okw = dict(schedule="jacobi", theta=0.5) if opts.get("schedule") else None
+    assert_parity(p, 4, prec, oracle_kw=okw, options=opts)
+    if L == 23:
+        from oracle import readout_commodity_flows
+        from paper_2106_14485_b200 import Solver
+        st = oracle_run(p, 4)
+        with Solver(p, prec=prec) as s:
+            s.sweep(4)
+            for t in (0, 4, p.T - 1):
+                Fl = s.commodity_flows(t)
+                assert max_rel_err(Fl, readout_commodity_flows(st, t), 1e-30) < TOL[prec]
+                absent = (t < p.t_in) | (t >= p.t_out)
+                assert np.all(Fl[:, absent] == 0.0)

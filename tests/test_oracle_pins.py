@@ -11,7 +11,7 @@ import pytest
 
 from oracle import (oracle_init, oracle_sweep, oracle_run, readout_flows, readout_commodity_flows,
                     dual_objective, stats, OracleInfeasible)
-from oracle.brute import BruteState, brute_sweep, full_tensor, arc_flows, commodity_marginal
+from oracle.brute import BruteState, brute_sweep, full_tensor, arc_flows, commodity_marginal, BruteTimes
 from oracle.lp import solve_lp, count_walks, time_expanded_counts
 from oracle.twins import LinearTwin, MpTwin
 from workloads import gen, grid_problem, fig1_problem
@@ -757,3 +757,82 @@ def test_node_costs_dual_monotone_and_strong_duality():
     phi = dual_objective(st, float(np.exp(st.a[p.T] + st.lamT).sum()))
     assert stats(st)["cap_violation"] < 1e-12
     assert abs(primal - phi) <= 1e-9 * abs(phi), (primal, phi)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-4: per-commodity entry / exit times (rem:multi_tensor_scheme P:1139-1149)
+
+def _times_problem(seed=0, T=6, L=3, node_cost=False, marginals="point", cap=(0.15, 0.5), rows=2, cols=3):
+    import dataclasses
+    p = grid_problem(rows, cols, T, L, 0.5, seed=seed, cap=cap, marginals=marginals)
+    rng = np.random.default_rng(seed)
+    t_in = rng.integers(0, 2, size=L)
+    t_out = np.maximum(t_in + 3, T - rng.integers(0, 2, size=L))
+    t_out = np.minimum(t_out, T)
+    q = dataclasses.replace(p, t_in=t_in, t_out=t_out)
+    if node_cost:
+        q = dataclasses.replace(q, node_cost=rng.uniform(0, 0.5, size=(L, p.N)))
+    return q
+
+
+@pytest.mark.parametrize("kw", [dict(seed=1), dict(seed=2, marginals="dense"), dict(seed=3, node_cost=True),
+                                dict(seed=4, L=2, T=5)])
+def test_commodity_times_iterates_identical_to_window_tensors(kw):
+    """P1 with entry / exit times: 8 GS sweeps of the per-commodity window tensors (oracle/brute.py BruteTimes, every
+    projection a literal sum) equal the oracle's sweeps iterate by iterate (U0, W, UT), and its flows vanish outside
+    each commodity's window."""
+    p = _times_problem(**kw)
+    assert np.any(p.t_in > 0) and np.any(p.t_out < p.T)
+    st = oracle_init(p)
+    bt = BruteTimes(p)
+    for k in range(8):
+        oracle_sweep(st)
+        bt.sweep()
+        assert max_rel_err(np.exp(st.lam0), bt.U0, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.omega), bt.W, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.lamT), bt.UT, 1e-300) < 1e-12, k
+    F, _ = readout_flows(st)
+    assert max_rel_err(F, bt.flows(), 1e-300) < 1e-12
+    for l in range(p.L):
+        for t in list(range(0, p.t_in[l])) + list(range(p.t_out[l], p.T)):
+            assert np.all(readout_commodity_flows(st, t)[:, l] == 0.0)
+    s = stats(st)
+    assert abs(s["mass"] - sum(M.sum() for M in bt.tensors())) <= 1e-12 * s["mass"]
+
+
+def test_commodity_times_full_window_equals_plain():
+    """t_in = 0 and t_out = T for every commodity is Algorithm 2 itself (to rounding)."""
+    import dataclasses
+    p = grid_problem(3, 3, 5, 3, 0.3, seed=12, cap=(0.1, 0.4))
+    q = dataclasses.replace(p, t_in=np.zeros(3, int), t_out=np.full(3, 5))
+    a, b = oracle_run(p, 5), oracle_run(q, 5)
+    Fa, Wa = readout_flows(a)
+    Fb, Wb = readout_flows(b)
+    assert max_rel_err(Fb, Fa, 1e-300) < 1e-14 and max_rel_err(Wb, Wa, 1e-300) < 1e-14
+
+
+def test_commodity_times_shifted_window_is_a_shorter_horizon():
+    """Time shift: with time-invariant costs and no capacities, a commodity present on layers [t_in, t_out] moves
+    exactly like the same commodity on a horizon of t_out - t_in steps (the Schroedinger bridge of remark P:922-928
+    only sees the window): its flows are the shorter problem's, shifted by t_in."""
+    import dataclasses
+    p = grid_problem(3, 3, 7, 1, 0.4, seed=11, cap=None)
+    q = dataclasses.replace(p, t_in=np.array([2]), t_out=np.array([6]))
+    r = dataclasses.replace(p, T=4)
+    Fq, _ = readout_flows(oracle_run(q, 3))
+    Fr, _ = readout_flows(oracle_run(r, 3))
+    assert max_rel_err(Fq[2:6], Fr, 1e-300) < 1e-12
+    assert np.all(Fq[:2] == 0) and np.all(Fq[6:] == 0)
+
+
+def test_commodity_times_dual_monotone():
+    """prp:sinkhorn on the multi-tensor form (eq:Sinkhorn_multi_tensor P:1141-1145): the dual objective is
+    non-decreasing after every block (U0, each W_t, UT) with the per-commodity windows."""
+    p = _times_problem(seed=5, L=3, T=6, cap=(0.1, 0.3))
+    st = oracle_init(p)
+    vals = []
+    for _ in range(15):
+        oracle_sweep(st, on_block=lambda kind, t, mass: vals.append(dual_objective(st, mass)))
+    v = np.array(vals)
+    assert np.all(np.diff(v) >= -1e-12 * np.abs(v).max()), np.diff(v).min()
+    assert v[-1] > v[0]

@@ -65,6 +65,10 @@ class Problem:
     # commodity-dependent node costs c[l, j] (finite), charged to commodity l for every
     # intermediate layer t = 1..T-1 it spends at node j (reading R-N); None = commodity-independent costs
     node_cost: Optional[np.ndarray] = None
+    # per-commodity entry / exit layers 0 <= t_in[l] < t_out[l] <= T (rem:multi_tensor_scheme
+    # P:1139-1149); None = 0 / T
+    t_in: Optional[np.ndarray] = None
+    t_out: Optional[np.ndarray] = None
 
     @property
     def A(self) -> int:
@@ -113,7 +117,7 @@ class Problem:
         """Sub-problem with commodities [l0, l1) (same graph, costs, caps)."""
         kw = dataclasses.asdict(self)
         kw.update(L=l1 - l0, name=f"{self.name}[{l0}:{l1}]")
-        for k in ("src", "dst", "mass", "mu0_dense", "muT_dense", "node_cost"):
+        for k in ("src", "dst", "mass", "mu0_dense", "muT_dense", "node_cost", "t_in", "t_out"):
             v = getattr(self, k)
             kw[k] = None if v is None else v[l0:l1].copy()
         return Problem(**kw)
