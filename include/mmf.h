@@ -147,6 +147,8 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "schedule" 0 = Gauss-Seidel (Algorithm 2, default), 1 = damped Jacobi (every W_t from
  *              one alpha/beta pair, W <- W^(1-theta) min(W d / F, 1)^theta; one all-reduce of the T x n_arcs
  *              flows per sweep on the multi-GPU path)
+ *              2 = symmetric Gauss-Seidel (Algorithm 2's forward pass, then a backward pass that
+ *              updates every W_t again before forming beta_t; keeps all T + 1 alpha layers, one extra flow pass)
  *   "theta_milli"  Jacobi damping theta in 1/1000 (0 .. 1000, default 500)
  *   "fgw", "fng", "fnp"  pipelined forward: warps per consumer group (8, 4, 2), groups per pipeline,
  *              pipelines per CTA (0 = default; the compiled combinations are listed in pipefwd.cuh)

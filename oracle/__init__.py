@@ -15,4 +15,4 @@ one ``-m "not gpu"`` test in ``tests/test_oracle_pins.py``.
 """
 from .sweep import (OracleState, OracleInfeasible, oracle_init, oracle_sweep, oracle_run, readout_flows,  # noqa: F401
                     readout_commodity_flows, dual_objective, stats, oracle_sweep_jacobi, damped_update,
-                    solve_error, oracle_solve)
+                    solve_error, oracle_solve, oracle_sweep_symmetric)

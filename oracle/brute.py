@@ -86,6 +86,27 @@ class BruteState:
         return full_tensor(self.p, self.U0, self.W, self.UT)
 
 
+def _brute_w_block(bs: BruteState, t: int) -> None:
+    """u_t <- min(u_t ⊙ d ./ P_t(K⊙U), 1) with the step-t bimarginals of the full tensor (eq:sinkhorn_graph_Vineq)."""
+    p = bs.p
+    F = arc_flows(p, bs.tensor())[t]
+    cap = np.asarray(p.cap_t(t), float)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        ratio = np.where(F > 0, cap / np.where(F > 0, F, 1.0), np.inf)
+    with np.errstate(invalid="ignore"):
+        neww = np.minimum(bs.W[t] * ratio, 1.0)
+    neww = np.where(cap == 0, 0.0, neww)
+    neww = np.where(np.isinf(cap), 1.0, neww)
+    bs.W[t] = neww
+
+
+def brute_sweep_symmetric(bs: BruteState) -> None:
+    """Symmetric GS (NEXT-1): the GS sweep's blocks, then W_{T-1} .. W_0 again, every projection from the full tensor."""
+    brute_sweep(bs)
+    for t in range(bs.p.T - 1, -1, -1):
+        _brute_w_block(bs, t)
+
+
 def brute_sweep(bs: BruteState) -> None:
     """One GS sweep of eq:sinkhorn_graph with projections of the full tensor."""
     p = bs.p
@@ -121,11 +142,14 @@ def brute_sweep(bs: BruteState) -> None:
 
 def commodity_window_tensor(problem, l: int, U0_l, W, UT_l) -> np.ndarray:
     """M^l[v_{t_in}, ..., v_{t_out}] = U0[v_{t_in}] prod_{t = t_in}^{t_out - 1} KW_t[v_t, v_{t+1}]
-    (x exp(-c[l, v_s]/eps) at the intermediate layers s = 1..T-1 inside the window, s > t_in) UT[v_{t_out}]."""
+    (x exp(-c[l, v_s]/eps) at every layer s of the window that is an intermediate layer 1..T-1 of the horizon)
+    UT[v_{t_out}]."""
     p = problem
     t0, t1 = int(p.t_in[l]), int(p.t_out[l])
     nc = getattr(p, "node_cost", None)
     M = np.asarray(U0_l, float).copy()
+    if nc is not None and 1 <= t0 <= p.T - 1:  # (the entry layer is an intermediate layer of the horizon)
+        M = M * np.exp(-np.asarray(nc[l], float) / p.eps)
     for t in range(t0, t1):
         KW = dense_kernel(p, t, W[t])
         M = M[..., :, None] * KW.reshape((1,) * (M.ndim - 1) + KW.shape)

@@ -229,10 +229,23 @@ def capacity_update(logd_t: np.ndarray, log_ks: np.ndarray) -> np.ndarray:
 
 def _enter(st: OracleState, t: int) -> None:
     """Commodities entering at layer t (t_in = t > 0): alpha_t = U0 there (their alpha below t_in is zero, so the
-    recursion left -inf in place)."""
+    recursion left -inf in place), times the layer's node factor: a commodity pays its node cost at every
+    intermediate layer 1..T-1 of its window, the boundary layers of the window included (reading R-N with times;
+    at a boundary layer the factor only rescales U0 / UT, the flows do not depend on it)."""
     if st.t_in is not None and np.any(st.t_in == t):
         sel = st.t_in == t
-        st.a[t][sel] = st.lam0[sel]
+        lc = _layer_cost(st, t)
+        st.a[t][sel] = st.lam0[sel] + (lc[sel] if isinstance(lc, np.ndarray) else lc)
+
+
+def _src_msg(st: OracleState) -> np.ndarray:
+    """log beta-hat at each commodity's entry layer: beta_{t_in} times the node factor of that layer (the source
+    marginal at t_in is U0 beta-hat; alpha_{t_in} = U0 times the factor, so alpha_{t_in} beta_{t_in} = mu0 after a2)."""
+    b = _at_layers(st.b, st.t_in)
+    if st.lD is not None:
+        mid = (st.t_in >= 1) & (st.t_in <= st.problem.T - 1)
+        b = b + np.where(mid[:, None], st.lD, 0.0)
+    return b
 
 
 def _mass_now(st: OracleState, t: int, X: Optional[np.ndarray] = None) -> float:
@@ -242,7 +255,7 @@ def _mass_now(st: OracleState, t: int, X: Optional[np.ndarray] = None) -> float:
     p = st.problem
     tin, tout = _src_layer(st), _sink_layer(st)
     m = np.zeros(p.L)
-    pre = np.exp(st.lam0 + _at_layers(st.b, tin)).sum(axis=1)
+    pre = np.exp(st.lam0 + (_src_msg(st) if st.t_in is not None else st.b[0])).sum(axis=1)
     if t < 0:
         return float(pre.sum())
     post = np.exp(_at_layers(st.a, tout) + st.lamT).sum(axis=1)
@@ -254,7 +267,7 @@ def _mass_now(st: OracleState, t: int, X: Optional[np.ndarray] = None) -> float:
 
 
 def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
-                 reduce_lse: Optional[Callable] = None) -> None:
+                 reduce_lse: Optional[Callable] = None, _backward: bool = True) -> None:
     """One Gauss-Seidel sweep in Algorithm 2's order.
 
     on_block(kind, t, mass) is called after every dual block update (kind in {"U0", "W", "UT"}),
@@ -268,7 +281,7 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
     tail_i = p.tail[oi]
     tin, tout = _src_layer(st), _sink_layer(st)
     # a2: U^(0,1) <- R^(0,1) ./ Psi_1, at each commodity's entry layer
-    st.lam0 = _boundary(st.log_mu0, _at_layers(st.b, tin) if st.t_in is not None else st.b[0], "source")
+    st.lam0 = _boundary(st.log_mu0, _src_msg(st) if st.t_in is not None else st.b[0], "source")
     st.a[0] = st.lam0 if st.t_in is None else np.where((tin == 0)[:, None], st.lam0, NEG_INF)
     if on_block is not None:
         on_block("U0", -1, _mass_now(st, -1))
@@ -290,7 +303,8 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
     if on_block is not None:
         on_block("UT", p.T, _mass_now(st, p.T))
     # a5: backward recompute
-    backward(st)
+    if _backward:
+        backward(st)
     st.sweeps += 1
 
 
@@ -313,7 +327,7 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     oi = st.in_seg[0]
     tail_i = p.tail[oi]
     tin, tout = _src_layer(st), _sink_layer(st)
-    st.lam0 = _boundary(st.log_mu0, _at_layers(st.b, tin) if st.t_in is not None else st.b[0], "source")
+    st.lam0 = _boundary(st.log_mu0, _src_msg(st) if st.t_in is not None else st.b[0], "source")
     st.a[0] = st.lam0 if st.t_in is None else np.where((tin == 0)[:, None], st.lam0, NEG_INF)
     new_omega = np.empty_like(st.omega)
     for t in range(p.T):
@@ -338,12 +352,49 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     st.sweeps += 1
 
 
+def oracle_sweep_symmetric(st: OracleState, on_block: Optional[Callable] = None) -> None:
+    """One sweep of the symmetric Gauss-Seidel schedule: Algorithm 2's forward pass (U0 block,
+    W_0 .. W_{T-1} blocks, UT block), then a backward pass that updates every W_t again before forming
+    beta_t (blocks W_{T-1} .. W_0): each update is the same exact block maximisation (prp:sinkhorn P:861, in
+    Algorithm 2's form P:1093) on the current tensor, so any such cyclic block order is a valid BCA order
+    (P:853-891).  Readouts use forward messages recomputed with the final W (reading R-J)."""
+    p = st.problem
+    oracle_sweep(st, on_block=on_block, _backward=False)
+    o = st.out_seg[0]
+    head_o = p.head[o]
+    tout = _sink_layer(st)
+    st.b[p.T] = np.where((tout == p.T)[:, None], st.lamT, NEG_INF)
+    for t in range(p.T - 1, -1, -1):
+        bh = st.b[t + 1] + _layer_cost(st, t + 1)
+        X = st.a[t][:, p.tail] + st.lK[t][None, :] + bh[:, p.head]            # current tensor, no W
+        st.omega[t] = capacity_update(st.logd[t], _lse_rows(X))
+        if on_block is not None:
+            on_block("W", t, _mass_now(st, t, X) if st.t_in is not None or st.t_out is not None
+                     else float(np.exp(X + st.omega[t][None, :]).sum()))
+        Xb = (st.lK[t][o] + st.omega[t][o])[None, :] + bh[:, head_o]
+        st.b[t] = seg_lse(Xb, st.out_seg)                                        # Psi_t with the new W_t
+        if st.t_out is not None and np.any(tout == t):
+            sel = tout == t
+            st.b[t][sel] = st.lamT[sel]
+    # forward messages of the end-of-sweep tensor (every W_t changed after its alpha_{t+1} was formed)
+    oi = st.in_seg[0]
+    tail_i = p.tail[oi]
+    st.a[0] = st.lam0 if st.t_in is None else np.where((_src_layer(st) == 0)[:, None], st.lam0, NEG_INF)
+    for t in range(p.T):
+        Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
+        st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)
+        _enter(st, t + 1)
+
+
 def oracle_run(problem, sweeps: int, schedule: str = "gs", theta: float = 1.0) -> OracleState:
-    """sweeps of Algorithm 2 (schedule "gs") or of the damped Jacobi schedule ("jacobi")."""
+    """sweeps of Algorithm 2 (schedule "gs"), of the damped Jacobi schedule ("jacobi") or of the symmetric
+    Gauss-Seidel schedule ("sym"), SURVEY §8(f) NEXT-1."""
     st = oracle_init(problem)
     for _ in range(sweeps):
         if schedule == "gs":
             oracle_sweep(st)
+        elif schedule == "sym":
+            oracle_sweep_symmetric(st)
         else:
             oracle_sweep_jacobi(st, theta)
     return st
@@ -424,7 +475,7 @@ def stats(st: OracleState) -> dict:
     cost = np.broadcast_to(p.cost, F.shape)
     cap = np.broadcast_to(p.cap, F.shape)
     # source / sink marginals of the end-of-sweep tensor (at each commodity's entry / exit layer)
-    P0 = np.exp(st.lam0 + (_at_layers(st.b, st.t_in) if st.t_in is not None else st.b[0]))
+    P0 = np.exp(st.lam0 + (_src_msg(st) if st.t_in is not None else st.b[0]))
     PT = np.exp((_at_layers(st.a, st.t_out) if st.t_out is not None else st.a[p.T]) + st.lamT)
     mass = float(PT.sum())
     return {
@@ -463,6 +514,8 @@ def oracle_solve(problem, tol: float, max_sweeps: int, check_every: int = 1, sch
         for _ in range(min(check_every, max_sweeps - done)):
             if schedule == "gs":
                 oracle_sweep(st)
+            elif schedule == "sym":
+                oracle_sweep_symmetric(st)
             else:
                 oracle_sweep_jacobi(st, theta)
         done = st.sweeps

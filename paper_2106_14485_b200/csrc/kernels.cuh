@@ -62,6 +62,7 @@ struct DevPtrs {
   // (norm_lane, store_msg) of launches whose output layer is intermediate (1..T-1); null otherwise
   const void* dnm;
   const void* dne;
+  int akeep;  // 1: the alpha store keeps every layer (slot t; symmetric GS), 0: double buffer (slot t & 1)
   int diag;  // diagnostics of the pipelined forward (option "dry" >= 2; results invalid), else 0
   float theta;  // Jacobi schedule damping: W <- W^(1 - theta) min(W d / F, 1)^theta
 };
@@ -108,8 +109,8 @@ template <class T_> struct View {
   __device__ __forceinline__ M* Wm(int t) const { return (M*)p.Wm + (size_t)t * p.A; }
   __device__ __forceinline__ int* We(int t) const { return p.We + (size_t)t * p.A; }
   __device__ __forceinline__ size_t slot(int s) const { return (size_t)s * p.N * p.Lp; }
-  __device__ __forceinline__ M* am(int t) const { return (M*)p.am + slot(t & 1); }
-  __device__ __forceinline__ E* ae(int t) const { return (E*)p.ae + slot(t & 1); }
+  __device__ __forceinline__ M* am(int t) const { return (M*)p.am + slot(p.akeep ? t : (t & 1)); }
+  __device__ __forceinline__ E* ae(int t) const { return (E*)p.ae + slot(p.akeep ? t : (t & 1)); }
   __device__ __forceinline__ M* bm(int t) const { return (M*)p.bm + slot(t); }
   __device__ __forceinline__ E* be(int t) const { return (E*)p.be + slot(t); }
 };

@@ -1023,8 +1023,10 @@ size_t layout(mmf_ctx* c, char* base) {
   p.dcap = at(L.take(TC * A * sm));
   p.Wm = at(L.take(T * A * sm));
   p.We = (int*)at(L.take(T * A * 4));
-  p.am = at(L.take(2 * N * Lp * sm));
-  p.ae = at(L.take(2 * N * Lp * se));
+  const size_t aslots = c->opt_schedule == 2 ? T + 1 : 2;  // (symmetric GS keeps every alpha_t)
+  p.am = at(L.take(aslots * N * Lp * sm));
+  p.ae = at(L.take(aslots * N * Lp * se));
+  p.akeep = c->opt_schedule == 2 ? 1 : 0;
   p.bm = at(L.take((T + 1) * N * Lp * sm));
   p.be = at(L.take((T + 1) * N * Lp * se));
   p.u0m = at(L.take(N * Lp * sm));
@@ -1497,14 +1499,22 @@ template <class T_> struct Eng {
 
   static mmf_status enqueue_sweep(mmf_ctx* c, cudaStream_t s) {
     if (c->opt_schedule == 1) return jacobi_sweep(c, s);
+    if (c->opt_schedule == 2) return symmetric_sweep(c, s);
+    return gs_sweep(c, s, true);
+  }
+
+  // Algorithm 2's sweep (a2, forward with the W updates, a4, and the backward pass a5 when do_bwd)
+  static mmf_status gs_sweep(mmf_ctx* c, cudaStream_t s, bool do_bwd) {
     if (c->opt_kernels >= 5 && c->pipe_fwd && !c->comm) {
       for (int t = 0; t <= c->T; ++t) pipe_fwd(c, s, t);       // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
-      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      if (do_bwd)
+        for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
       return MMF_OK;
     }
     if (c->opt_kernels == 4 && !c->comm) {
       for (int t = 0; t <= c->T; ++t) head_fwd(c, s, t);       // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
-      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      if (do_bwd)
+        for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
       return MMF_OK;
     }
     if (c->opt_kernels >= 2) {
@@ -1516,7 +1526,8 @@ template <class T_> struct Eng {
           if (st != MMF_OK) return st;
         }
       }
-      for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      if (do_bwd)
+        for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
       return MMF_OK;
     }
     boundary(c, s, 0);  // a2
@@ -1525,7 +1536,50 @@ template <class T_> struct Eng {
       if (st != MMF_OK) return st;
     }
     boundary(c, s, 1);  // a4
-    bwd_pass(c, s);     // a5
+    if (do_bwd) bwd_pass(c, s);  // a5
+    return MMF_OK;
+  }
+
+  // symmetric Gauss-Seidel (option schedule = 2): Algorithm 2's forward pass, then a backward
+  // pass that updates W_t again before forming beta_t: per step the flows F_t of the current tensor (alpha_t kept
+  // from the forward pass: the alpha store has T + 1 slots; beta_{t+1} fresh), the dual update of W_t (all-reduced
+  // flows on the multi-GPU path), the backward step
+  static mmf_status symmetric_sweep(mmf_ctx* c, cudaStream_t s) {
+    mmf_status st = gs_sweep(c, s, false);
+    if (st != MMF_OK) return st;
+    const bool pipe = sizeof(M) == 4 && c->opt_kernels >= 5 && c->pipe_fwd && !c->comm;
+    const unsigned ga = (unsigned)((c->A + 255) / 256);
+    for (int t = c->T - 1; t >= 0; --t) {
+      // flows of step t into Fout[t] (the readout launches; the alpha they rewrite is unchanged: W_{<=t} are as the
+      // forward pass left them)
+      if (pipe) {
+        LaunchScope ls(c, K_FUSED, s);
+        pipe_fwd_mode<3>(c, s, t + 1);
+      } else if (c->opt_kernels >= 2) {
+        tiled_fwd(c, s, t, 2);
+      } else {
+        st = fwd_step(c, s, t, 1);
+        if (st != MMF_OK) return st;
+      }
+      M* Ft = (M*)c->dp.Fout + (size_t)t * c->A;
+      if (c->comm && (pipe || c->opt_kernels >= 2)) {  // (fwd_step all-reduced already)
+        int r = nccl_api().AllReduce(Ft, Ft, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64, NCCL_SUM,
+                                     c->comm, s);
+        if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
+      }
+      {
+        DevPtrs d = c->dp;
+        d.Fsum = Ft;
+        LaunchScope ls(c, K_UPDATE, s);
+        k_dual<T_><<<ga, 256, 0, s>>>(d, t);
+      }
+      if (c->opt_kernels >= 2) {
+        tiled_bwd(c, s, t);
+      } else {
+        LaunchScope ls(c, K_BWD, s);
+        k_bwd<T_><<<dim3(c->N, c->G), c->block, 0, s>>>(lay(c, t), t);
+      }
+    }
     return MMF_OK;
   }
 
@@ -2153,7 +2207,8 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_fng = (int)value;
     }
     if (k == "schedule") {
-      if (value < 0 || value > 1) return fail(ctx, MMF_EINVAL, "schedule must be 0 (Gauss-Seidel) or 1 (Jacobi)");
+      if (value < 0 || value > 2)
+        return fail(ctx, MMF_EINVAL, "schedule must be 0 (Gauss-Seidel), 1 (Jacobi) or 2 (symmetric Gauss-Seidel)");
       ctx->opt_schedule = (int)value;
     }
     if (k == "theta_milli") {

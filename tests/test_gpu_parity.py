@@ -718,3 +718,27 @@ def test_commodity_times_parity(prec, L, opts):
                 assert max_rel_err(Fl, readout_commodity_flows(st, t), 1e-30) < TOL[prec]
                 absent = (t < p.t_in) | (t >= p.t_out)
                 assert np.all(Fl[:, absent] == 0.0)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-1 remainder: symmetric Gauss-Seidel (option schedule = 2)
+
+@pytest.mark.parametrize("prec,L,marg,opts", [("fp32", 1019, "point", {}), ("fp64", 37, "point", {}),
+                                              ("fp64", 20, "dense", dict(kernels=1)), ("fp32", 300, "point", dict(kernels=3)),
+                                              ("fp32", 60, "point", dict(kernels=4)), ("fp32", 150, "dense", dict(kernels=2))])
+def test_symmetric_gs_parity(prec, L, marg, opts):
+    """W updated in the forward and the backward pass (oracle_sweep_symmetric, pinned by the brute-force symmetric
+    sweep) on every kernel family, flows, duals and statistics."""
+    p = grid_problem(8, 8, 7, L, 0.2, seed=50, cap=(0.3 * max(L, 100) / 100, 1.2 * max(L, 100) / 100)
+                     if marg == "point" else (0.05, 0.2), marginals=marg)
+    assert_parity(p, 4, prec, oracle_kw=dict(schedule="sym"), options=dict(schedule=2, **opts))
+
+
+def test_symmetric_gs_with_node_costs_and_times():
+    import dataclasses
+    p = grid_problem(8, 8, 8, 1019, 0.2, seed=51, cap=(3.0, 12.0))
+    rng = np.random.default_rng(4)
+    t_in = rng.integers(0, 3, size=p.L)
+    p = dataclasses.replace(p, T=10, t_in=t_in, t_out=np.minimum(t_in + 8, 10),
+                            node_cost=rng.uniform(0, 0.3, size=(p.L, p.N)))
+    assert_parity(p, 3, "fp32", oracle_kw=dict(schedule="sym"), options=dict(schedule=2))

@@ -836,3 +836,46 @@ def test_commodity_times_dual_monotone():
     v = np.array(vals)
     assert np.all(np.diff(v) >= -1e-12 * np.abs(v).max()), np.diff(v).min()
     assert v[-1] > v[0]
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-1 remainder: symmetric Gauss-Seidel (W updated in the forward and the backward pass)
+
+from oracle import oracle_sweep_symmetric  # noqa: E402
+from oracle.brute import brute_sweep_symmetric  # noqa: E402
+
+
+@pytest.mark.parametrize("kw", [MICROS[0], MICROS[1], MICROS[4], MICROS[6]])
+def test_symmetric_gs_iterates_identical_to_full_tensor(kw):
+    """Every block of the symmetric sweep (U0, W_0..W_{T-1}, UT, W_{T-1}..W_0) is prp:sinkhorn's update with the
+    projections of the full tensor: 8 sweeps iterate-identical to the brute-force symmetric sweep, and the readout
+    equals the end-of-sweep tensor's projections."""
+    p = _micro(kw)
+    st = oracle_init(p)
+    bs = BruteState(p)
+    for k in range(8):
+        oracle_sweep_symmetric(st)
+        brute_sweep_symmetric(bs)
+        assert max_rel_err(np.exp(st.lam0), bs.U0, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.omega), bs.W, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.lamT), bs.UT, 1e-300) < 1e-12, k
+    F, _ = readout_flows(st)
+    assert max_rel_err(F, arc_flows(p, bs.tensor()), 1e-300) < 1e-12
+
+
+def test_symmetric_gs_dual_monotone_and_same_optimum():
+    """BCA with the symmetric block order: the dual never decreases after any block, and the iteration
+    reaches the Gauss-Seidel optimum (the unique minimiser)."""
+    p = grid_problem(3, 3, 4, 2, 0.5, seed=13, cap=(0.15, 0.4))
+    st = oracle_init(p)
+    vals = []
+    for _ in range(20):
+        oracle_sweep_symmetric(st, on_block=lambda kind, t, mass: vals.append(dual_objective(st, mass)))
+    v = np.array(vals)
+    assert np.all(np.diff(v) >= -1e-12 * np.abs(v).max())
+    sym = oracle_run(p, 300, schedule="sym")
+    gs = oracle_run(p, 300)
+    Fs, Ws = readout_flows(sym)
+    Fg, Wg = readout_flows(gs)
+    assert max_rel_err(Ws, Wg, 1e-12) < 1e-8 and max_rel_err(Fs, Fg, 1e-12) < 1e-8
+    assert np.any(Wg < 0.99)
