@@ -60,7 +60,8 @@ typedef struct {
   double src_mismatch;   /* sum_{l,i} |U0 beta_0 - mu0|   (end-of-sweep source marginal error, L1) */
   double sink_mismatch;  /* sum_{l,j} |alpha_T UT - muT| (≈ 0 right after a4) */
   double cap_violation;  /* max_{t,a} (F_t[a] - d_t[a])_+ over capacitated arcs */
-  double dual;           /* thm:solution dual objective: eps*(-mass + <mu0,log U0> + <muT,log UT> + <d,log W>) */
+  double dual;           /* thm:solution dual objective: eps*(-mass + <mu0,log U0> + <muT,log UT> + <d,log W>
+                            + <d_node, log u_node>) */
   double primal;         /* sum_{t,a} C_t[a] F_t[a] */
 } mmf_stats;
 
@@ -102,6 +103,19 @@ mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_beg
  * alone).  Values must be finite with |c / eps| log2(e) <= 8000, else MMF_EINVAL; NULL clears.  The factors
  * D = exp(-c/eps) are formed in fp64 and stored like K; stats' "primal" stays the arc-cost term. */
 mmf_status mmf_set_node_costs(mmf_ctx* ctx, const double* c);
+
+/* Node (state) capacities: the paper's inequality constraints on the state marginals,
+ * P_t(M) <= d_t for the intermediate layers (eq:multicommodity P:676-683, Algorithm 2's u_t update P:1093; with the
+ * arc-state and traffic-routing state spaces of P:612, P:704-720 the states are the nodes of this library's graph):
+ * sum_l alpha_t[j,l] beta_t[j,l] <= d_t[j] for t = 1..T-1, with a shared dual u_t[j] in [0, 1] updated in the
+ * forward pass right after alpha_t.  cap is [N] (every layer) or [T+1][N] (time_varying; layers 0 and T ignored), user
+ * node order, +INFINITY free, 0 closed; NaN / negative -> MMF_EINVAL; call after mmf_set_costs, before the layout.
+ * Supported on the pipelined fp32 path (L >= 256) and kernels = 1, Gauss-Seidel and symmetric schedules, one rank
+ * (else MMF_EINVAL at mmf_init); checkpoints do not cover them.  NULL clears. */
+mmf_status mmf_set_node_capacity(mmf_ctx* ctx, const double* cap, int time_varying);
+
+/* The node-capacity duals u_t[j] (fp64, [T+1][N] user node order; 1 at free nodes and at layers 0, T).  Synchronises. */
+mmf_status mmf_read_node_duals(mmf_ctx* ctx, double* out_T1xN);
 
 /* Per-commodity entry / exit times (rem:multi_tensor_scheme P:1139-1149 and P:692-693:
  * commodities that enter and leave the network at different times, each with its own transport tensor): commodity l

@@ -25,7 +25,7 @@ def dense_kernel(problem, t: int, W_t: np.ndarray) -> np.ndarray:
     return K
 
 
-def full_tensor(problem, U0: np.ndarray, W: np.ndarray, UT: np.ndarray) -> np.ndarray:
+def full_tensor(problem, U0: np.ndarray, W: np.ndarray, UT: np.ndarray, Un: np.ndarray = None) -> np.ndarray:
     """M with shape (L, N, ..., N) (T+1 node modes).  With commodity node costs c[l, j] (NEXT-2, reading R-N) every
     intermediate mode t = 1..T-1 is also multiplied by exp(-c[l, v_t]/eps) (the commodity-dependent K_L of
     eq:K_multicommodity, P:1010-1013)."""
@@ -38,6 +38,8 @@ def full_tensor(problem, U0: np.ndarray, W: np.ndarray, UT: np.ndarray) -> np.nd
         if nc is not None and t + 1 <= p.T - 1:     # mode t + 1 is an intermediate layer
             Dl = np.exp(-np.asarray(nc, float) / p.eps)          # (L, N)
             M = M * Dl.reshape((p.L,) + (1,) * (M.ndim - 2) + (p.N,))
+        if Un is not None and t + 1 <= p.T - 1:     # node-capacity duals u_{t+1} (NEXT-3)
+            M = M * np.asarray(Un[t + 1], float).reshape((1,) * (M.ndim - 1) + (p.N,))
     return M * UT.reshape((p.L,) + (1,) * (p.T) + (p.N,))
 
 
@@ -80,10 +82,11 @@ class BruteState:
         self.U0 = np.ones((p.L, p.N))
         self.W = np.ones((p.T, p.A))
         self.UT = (p.muT > 0).astype(float)     # Q7: all-ones on the support
+        self.Un = np.ones((p.T + 1, p.N)) if getattr(p, "node_cap", None) is not None else None
         self.sweeps = 0
 
     def tensor(self):
-        return full_tensor(self.p, self.U0, self.W, self.UT)
+        return full_tensor(self.p, self.U0, self.W, self.UT, self.Un)
 
 
 def _brute_w_block(bs: BruteState, t: int) -> None:
@@ -98,6 +101,21 @@ def _brute_w_block(bs: BruteState, t: int) -> None:
     neww = np.where(cap == 0, 0.0, neww)
     neww = np.where(np.isinf(cap), 1.0, neww)
     bs.W[t] = neww
+
+
+def _brute_node_block(bs: BruteState, t: int) -> None:
+    """u_t <- min(u_t ⊙ d_t ./ P_t(K⊙U), 1) on the node marginal of layer t summed over the commodities."""
+    p = bs.p
+    P = commodity_marginal(bs.tensor(), t).sum(axis=0)
+    nc = np.asarray(p.node_cap, float)
+    d = nc if nc.ndim == 1 else nc[t]
+    with np.errstate(invalid="ignore", divide="ignore"):
+        ratio = np.where(P > 0, d / np.where(P > 0, P, 1.0), np.inf)
+    with np.errstate(invalid="ignore"):
+        new = np.minimum(bs.Un[t] * ratio, 1.0)
+    new = np.where(d == 0, 0.0, new)
+    new = np.where(np.isinf(d), 1.0, new)
+    bs.Un[t] = new
 
 
 def brute_sweep_symmetric(bs: BruteState) -> None:
@@ -118,15 +136,9 @@ def brute_sweep(bs: BruteState) -> None:
     bs.U0 = bs.U0 * r
     # u_t blocks: u <- min(u ⊙ d ./ P_t(K⊙U), 1)   (eq:sinkhorn_graph_Vineq)
     for t in range(p.T):
-        F = arc_flows(p, bs.tensor())[t]
-        cap = np.asarray(p.cap_t(t), float)
-        with np.errstate(invalid="ignore", divide="ignore"):
-            ratio = np.where(F > 0, cap / np.where(F > 0, F, 1.0), np.inf)
-        with np.errstate(invalid="ignore"):
-            neww = np.minimum(bs.W[t] * ratio, 1.0)
-        neww = np.where(cap == 0, 0.0, neww)
-        neww = np.where(np.isinf(cap), 1.0, neww)
-        bs.W[t] = neww
+        _brute_w_block(bs, t)
+        if bs.Un is not None and t + 1 <= p.T - 1:  # node-capacity block of layer t + 1 (NEXT-3)
+            _brute_node_block(bs, t + 1)
     # U^(0,T) block
     PT = commodity_marginal(bs.tensor(), p.T)
     r = _ratio(p.muT, PT)

@@ -106,6 +106,8 @@ class OracleState:
     lD: Optional[np.ndarray] = None  # [L, N] -c[l, j]/eps, commodity node costs (NEXT-2), or None
     t_in: Optional[np.ndarray] = None   # [L] entry layer of each commodity (NEXT-4 entry/exit times), or None = 0
     t_out: Optional[np.ndarray] = None  # [L] exit layer, or None = T
+    logdn: Optional[np.ndarray] = None  # [T+1, N] log node (state) capacities (NEXT-3), +inf at layers 0 and T; or None
+    nu: Optional[np.ndarray] = None     # [T+1, N] log u_t of the node capacities (0 where free)
 
 
 def _at_layers(arr, layers: np.ndarray) -> np.ndarray:
@@ -121,14 +123,22 @@ def _sink_layer(st) -> np.ndarray:
     return st.t_out if st.t_out is not None else np.full(st.problem.L, st.problem.T, np.int64)
 
 
-def _layer_cost(st: "OracleState", t: int):
-    """log of the commodity node factor D_t[l, j] = exp(-c[l, j]/eps) at layer t (SURVEY §8(f) NEXT-2 in the form of
-    DESIGN.md reading R-N: charged at the intermediate layers 1..T-1 only, so the boundary layers 0 and T carry the
-    marginals alone).  It multiplies every walk through (t, j) of commodity l: the commodity-dependent kernel K_L of
-    eq:K_multicommodity restricted to costs that depend on the arc's head."""
-    if st.lD is None or t < 1 or t > st.problem.T - 1:
+def _layer_cost(st: "OracleState", t: int, nu: bool = True):
+    """log of the node factors of layer t that multiply every walk through (t, j):
+    - the commodity node factor D[l, j] = exp(-c[l, j]/eps) (SURVEY §8(f) NEXT-2 in the form of DESIGN.md reading R-N:
+      charged at the intermediate layers 1..T-1 only, so the boundary layers 0 and T carry the marginals alone; the
+      commodity-dependent kernel K_L of eq:K_multicommodity P:1010-1013 restricted to costs that depend on the head);
+    - (nu) the node-capacity dual u_t[j] = exp(nu_t[j]) (NEXT-3: the capacity of the state marginal P_t(M) <= d_t of
+      eq:multicommodity P:676-683, Algorithm 2's u_t), also at the intermediate layers only."""
+    T = st.problem.T
+    if t < 1 or t > T - 1:
         return 0.0
-    return st.lD
+    out = 0.0
+    if st.lD is not None:
+        out = st.lD
+    if nu and st.nu is not None:
+        out = out + st.nu[t][None, :]
+    return out
 
 
 class _TwoLayers:
@@ -178,6 +188,14 @@ def oracle_init(problem, b_store: Optional[np.ndarray] = None, keep_forward: boo
         in_seg=_segments(p.head.astype(np.int64), N), out_seg=_segments(p.tail.astype(np.int64), N),
         keep_forward=keep_forward,
         lD=None if getattr(p, "node_cost", None) is None else -np.asarray(p.node_cost, np.float64) / float(p.eps))
+    if getattr(p, "node_cap", None) is not None:
+        # NEXT-3 state capacities: d_t[j] on the node marginal at the intermediate layers 1..T-1
+        nc = np.asarray(p.node_cap, np.float64)
+        dn = np.broadcast_to(nc, (T + 1, N)).copy() if nc.ndim == 1 else nc.copy()
+        dn[0] = np.inf
+        dn[T] = np.inf
+        st.logdn = _log(dn)
+        st.nu = np.zeros((T + 1, N))
     if getattr(p, "t_in", None) is not None or getattr(p, "t_out", None) is not None:
         # NEXT-4 entry / exit times (rem:multi_tensor_scheme P:1139-1149): commodity l's transport tensor
         # spans the layers t_in[l] .. t_out[l]; its source scaling sits at layer t_in[l], its sink scaling at t_out[l]
@@ -227,24 +245,24 @@ def capacity_update(logd_t: np.ndarray, log_ks: np.ndarray) -> np.ndarray:
     return om
 
 
-def _enter(st: OracleState, t: int) -> None:
+def _enter(st: OracleState, t: int, nu: bool = True) -> None:
     """Commodities entering at layer t (t_in = t > 0): alpha_t = U0 there (their alpha below t_in is zero, so the
     recursion left -inf in place), times the layer's node factor: a commodity pays its node cost at every
     intermediate layer 1..T-1 of its window, the boundary layers of the window included (reading R-N with times;
     at a boundary layer the factor only rescales U0 / UT, the flows do not depend on it)."""
     if st.t_in is not None and np.any(st.t_in == t):
         sel = st.t_in == t
-        lc = _layer_cost(st, t)
-        st.a[t][sel] = st.lam0[sel] + (lc[sel] if isinstance(lc, np.ndarray) else lc)
+        lc = np.broadcast_to(_layer_cost(st, t, nu), st.lam0.shape)
+        st.a[t][sel] = st.lam0[sel] + lc[sel]
 
 
 def _src_msg(st: OracleState) -> np.ndarray:
     """log beta-hat at each commodity's entry layer: beta_{t_in} times the node factor of that layer (the source
     marginal at t_in is U0 beta-hat; alpha_{t_in} = U0 times the factor, so alpha_{t_in} beta_{t_in} = mu0 after a2)."""
-    b = _at_layers(st.b, st.t_in)
-    if st.lD is not None:
-        mid = (st.t_in >= 1) & (st.t_in <= st.problem.T - 1)
-        b = b + np.where(mid[:, None], st.lD, 0.0)
+    b = _at_layers(st.b, st.t_in).copy()
+    for t in np.unique(st.t_in):
+        sel = st.t_in == t
+        b[sel] = b[sel] + np.broadcast_to(_layer_cost(st, int(t)), b.shape)[sel]
     return b
 
 
@@ -264,6 +282,20 @@ def _mass_now(st: OracleState, t: int, X: Optional[np.ndarray] = None) -> float:
     inside = np.exp(X + st.omega[t][None, :]).sum(axis=1)
     m = np.where(t < tin, pre, np.where(t >= tout, post, inside))
     return float(m.sum())
+
+
+def _node_update(st: OracleState, t: int, on_block: Optional[Callable] = None) -> None:
+    """NEXT-3 node (state) capacity block at layer t (1..T-1), Algorithm 2's u_t update on the node marginal:
+    nu_t = min(log d_t - LSE_l(a_t + b_t), 0) with a_t without the node factor (the current tensor's marginal at layer t
+    up to u_t), the zero conventions of capacity_update; then a_t += nu_t."""
+    if st.nu is None or t < 1 or t > st.problem.T - 1:
+        return
+    X = st.a[t] + st.b[t]
+    st.nu[t] = capacity_update(st.logdn[t], _lse_rows(X))
+    st.a[t] = st.a[t] + st.nu[t][None, :]
+    if on_block is not None:
+        assert st.t_in is None and st.t_out is None
+        on_block("N", t, float(np.exp(X + st.nu[t][None, :]).sum()))
 
 
 def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
@@ -296,8 +328,9 @@ def oracle_sweep(st: OracleState, on_block: Optional[Callable] = None,
             on_block("W", t, float(np.exp(X + st.omega[t][None, :]).sum()) if st.t_in is None and st.t_out is None
                      else _mass_now(st, t, X))
         Y = st.a[t][:, tail_i] + (st.lK[t][oi] + st.omega[t][oi])[None, :]
-        st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1)           # Psi-hat_{t+1}
-        _enter(st, t + 1)
+        st.a[t + 1] = seg_lse(Y, st.in_seg) + _layer_cost(st, t + 1, nu=False)  # Psi-hat_{t+1}
+        _enter(st, t + 1, nu=False)
+        _node_update(st, t + 1, on_block)                                       # u_{t+1} (states)
     # a4: U^(0,T) <- R^(0,T) ./ Psi-hat_T, at each commodity's exit layer
     st.lamT = _boundary(st.log_muT, _at_layers(st.a, tout) if st.t_out is not None else st.a[p.T], "sink")
     if on_block is not None:
@@ -326,6 +359,7 @@ def oracle_sweep_jacobi(st: OracleState, theta: float) -> None:
     p = st.problem
     oi = st.in_seg[0]
     tail_i = p.tail[oi]
+    assert st.nu is None, "node capacities: Gauss-Seidel schedules only"
     tin, tout = _src_layer(st), _sink_layer(st)
     st.lam0 = _boundary(st.log_mu0, _src_msg(st) if st.t_in is not None else st.b[0], "source")
     st.a[0] = st.lam0 if st.t_in is None else np.where((tin == 0)[:, None], st.lam0, NEG_INF)
@@ -457,6 +491,10 @@ def dual_terms(st: OracleState) -> tuple:
     sT = np.where(muT > 0, muT * np.where(np.isfinite(st.lamT), st.lamT, 0.0), 0.0).sum()
     fin = np.isfinite(cap) & (cap > 0)
     sd = (np.where(fin, cap, 0.0) * np.where(fin, st.omega, 0.0)).sum()
+    if st.nu is not None:  # node capacities (NEXT-3): sum_t <d_t, log u_t> over the finite positive ones
+        dn = np.exp(st.logdn)
+        finn = np.isfinite(dn) & (dn > 0)
+        sd = sd + (np.where(finn, dn, 0.0) * np.where(finn, st.nu, 0.0)).sum()
     return s0, sT, sd
 
 

@@ -24,7 +24,7 @@ EXPORTS = ["mmf_create", "mmf_set_graph", "mmf_set_costs", "mmf_set_capacity", "
            "mmf_read_stats", "mmf_read_kernel_stats", "mmf_sweep_bytes", "mmf_destroy", "mmf_last_error",
            "mmf_version", "mmf_solve", "mmf_state_bytes", "mmf_save_state", "mmf_load_state",
            "mmf_read_commodity_flows", "mmf_set_node_costs", "mmf_sweep_group",
-           "mmf_set_commodity_times"]
+           "mmf_set_commodity_times", "mmf_set_node_capacity", "mmf_read_node_duals"]
 
 
 class MMFError(RuntimeError):
@@ -82,6 +82,8 @@ def load(path: str = None):
         "mmf_set_node_costs": ([vp, dp], C.c_int),
         "mmf_sweep_group": ([C.POINTER(vp), i32, i32], C.c_int),
         "mmf_set_commodity_times": ([vp, ip, ip], C.c_int),
+        "mmf_set_node_capacity": ([vp, dp, C.c_int], C.c_int),
+        "mmf_read_node_duals": ([vp, dp], C.c_int),
         "mmf_destroy": ([vp], C.c_int),
         "mmf_last_error": ([vp], C.c_char_p),
         "mmf_version": ([], C.c_char_p),
@@ -169,6 +171,20 @@ def mmf_set_commodity_times(ctx, t_in, t_out):
         return
     t_in, t_out = _i32(t_in), _i32(t_out)
     _check(ctx, load().mmf_set_commodity_times(ctx, _p(t_in, C.c_int32), _p(t_out, C.c_int32)))
+
+
+def mmf_set_node_capacity(ctx, cap, time_varying: bool):
+    if cap is None:
+        _check(ctx, load().mmf_set_node_capacity(ctx, None, 0))
+        return
+    cap = _f64(cap)
+    _check(ctx, load().mmf_set_node_capacity(ctx, _p(cap, C.c_double), int(bool(time_varying))))
+
+
+def mmf_read_node_duals(ctx, T: int, N: int) -> np.ndarray:
+    out = np.empty((T + 1, N), np.float64)
+    _check(ctx, load().mmf_read_node_duals(ctx, _p(out, C.c_double)))
+    return out
 
 
 def mmf_workspace_bytes(ctx) -> int:

@@ -56,6 +56,8 @@ class Solver:
         L.mmf_set_graph(self.ctx, p.N, p.tail, p.head)
         L.mmf_set_costs(self.ctx, p.T, p.eps, p.cost, p.cost.ndim == 2)
         L.mmf_set_capacity(self.ctx, p.cap, p.cap.ndim == 2)
+        if getattr(p, "node_cap", None) is not None:  # SURVEY 8(f) NEXT-3 (state capacities)
+            L.mmf_set_node_capacity(self.ctx, p.node_cap, np.ndim(p.node_cap) == 2)
         sl = slice(l_begin, l_begin + l_count)
         if p.is_point:
             L.mmf_set_point_marginals(self.ctx, p.L, l_begin, p.src[sl], p.dst[sl], p.mass[sl])
@@ -96,6 +98,10 @@ class Solver:
 
     def cap_duals(self) -> np.ndarray:
         return L.mmf_read_cap_duals(self.ctx, self.p.T, self.p.A)
+
+    def node_duals(self) -> np.ndarray:
+        """Node-capacity duals u_t[j], [T+1, N] (NEXT-3)."""
+        return L.mmf_read_node_duals(self.ctx, self.p.T, self.p.N)
 
     def stats(self) -> dict:
         return L.mmf_read_stats(self.ctx)

@@ -63,6 +63,14 @@ struct DevPtrs {
   const void* dnm;
   const void* dne;
   int akeep;  // 1: the alpha store keeps every layer (slot t; symmetric GS), 0: double buffer (slot t & 1)
+  // node (state) capacities: d [TN][N] (M), the duals u [T+1][N] (M significand + int exponent),
+  // and per launch the layer's u applied by the message epilogues (unlm / unle, null when not applied)
+  const void* dnc;
+  int dnc_tv;
+  void* unm;
+  int* une;
+  const void* unlm;
+  const int* unle;
   int diag;  // diagnostics of the pipelined forward (option "dry" >= 2; results invalid), else 0
   float theta;  // Jacobi schedule damping: W <- W^(1 - theta) min(W d / F, 1)^theta
 };
@@ -135,6 +143,15 @@ __device__ __forceinline__ void store_msg(const DevPtrs& p, typename T_::M* pm, 
       m *= M(0.5);
       e += 1;
     }
+  }
+  if (p.unlm && m != M(0)) {  // node-capacity dual of this layer (NEXT-3)
+    m *= ((const M*)p.unlm)[node];
+    e += p.unle[node];
+    if (m >= M(2)) {
+      m *= M(0.5);
+      e += 1;
+    }
+    if (m == M(0)) e = EZERO;
   }
   if (m != M(0) && (e > ELIM || e < -ELIM)) {
     set_error(p, ERR_RANGE, l, node);
@@ -333,6 +350,86 @@ template <class T_> __global__ void k_reduce(DevPtrs p, int t, typename T_::M* o
 }
 
 // capacity-dual update from the all-reduced flows (multi-GPU path)
+// NEXT-3 node-capacity block of layer t (Algorithm 2's u_t, on the states): one CTA per node j,
+//   P = sum_l alpha_t[j,l] beta-hat_t[j,l] / (D[l,j] u_old[j])   (alpha_t written without u_t; beta-hat_t carries the
+//       previous u_t and D: P is the marginal of the current tensor up to u_t),
+//   u_t[j] = min(d_t[j] / P, 1)  (d = inf: 1, d = 0: 0, P = 0: 1), then alpha_t[j, :] *= u_t[j].
+template <class T_> __global__ void __launch_bounds__(256) k_node_cap(DevPtrs p, int t) {
+  typedef typename T_::M M;
+  typedef typename T_::E E;
+  View<T_> v(p);
+  const int j = blockIdx.x;
+  const M d = ((const M*)p.dnc)[(size_t)(p.dnc_tv ? t : 0) * p.N + j];
+  if (isinf(d)) return;
+  M* um = (M*)p.unm + (size_t)t * p.N;
+  int* ue = p.une + (size_t)t * p.N;
+  M* am = v.am(t) + (size_t)j * p.Lp;
+  E* ae = v.ae(t) + (size_t)j * p.Lp;
+  double nm;
+  int ne;
+  if (d == M(0)) {
+    nm = 0.0;
+    ne = EZERO;
+  } else {
+    const M* bm = v.bm(t) + (size_t)j * p.Lp;
+    const E* be = v.be(t) + (size_t)j * p.Lp;
+    XAcc<double> acc;
+    for (int l = threadIdx.x; l < p.L; l += blockDim.x) {
+      double m = (double)am[l] * (double)bm[l];
+      int e = (int)ae[l] + (int)be[l];
+      if (p.dnm) {
+        m /= (double)((const M*)p.dnm)[(size_t)j * p.Lp + l];
+        e -= (int)((const E*)p.dne)[(size_t)j * p.Lp + l];
+      }
+      if (m > 0.0) acc.add(m, e);
+    }
+    // block reduction of (s, E)
+    __shared__ double ss[256];
+    __shared__ int se[256];
+    ss[threadIdx.x] = acc.s;
+    se[threadIdx.x] = acc.E;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) {
+        const int E1 = se[threadIdx.x], E2 = se[threadIdx.x + o], Em = max(E1, E2);
+        ss[threadIdx.x] = ss[threadIdx.x] * pow2_nonpos<double>(E1 - Em) + ss[threadIdx.x + o] * pow2_nonpos<double>(E2 - Em);
+        se[threadIdx.x] = Em;
+      }
+      __syncthreads();
+    }
+    const double s = ss[0];
+    const int E_ = se[0];
+    const double uo = (double)um[j];
+    const int uoe = ue[j];
+    if (!(s > 0.0) || !(uo > 0.0)) {
+      nm = 1.0;
+      ne = 0;
+    } else {
+      // x = d / P = d u_old / (s 2^E)
+      xf_norm<double>((double)d * uo / s, uoe - E_, nm, ne);
+      if (ne >= 0) {
+        nm = 1.0;
+        ne = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    um[j] = (M)nm;
+    ue[j] = ne;
+  }
+  for (int l = threadIdx.x; l < p.Lp; l += blockDim.x) {
+    double m = (double)am[l] * nm;
+    int e = (int)ae[l] + ne;
+    M mm;
+    int ee;
+    xf_norm<M>((M)m, e, mm, ee);
+    if (mm == M(0)) ee = EZERO;
+    am[l] = mm;
+    ae[l] = (E)ee;
+  }
+}
+
 template <class T_> __global__ void k_dual(DevPtrs p, int t) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= p.A) return;

@@ -96,6 +96,8 @@ struct mmf_ctx {
   // a release arc to the source that exists only at step t_in - 1) and a sink holding node (an absorb arc from the sink that exists
   // only at step t_out, and its loop); user arcs keep their positions, readouts cover them only.
   std::vector<int> t_in, t_out;
+  std::vector<double> node_cap;  // NEXT-3 node (state) capacities [N] or [T+1][N] (user node order), empty = none
+  bool node_cap_tv = false;
   bool augmented = false;
   int N_user = 0;
   int64_t A_user = 0;
@@ -864,6 +866,13 @@ void augment_times(mmf_ctx* c) {
       std::copy(c->node_cost.begin() + (size_t)l * c->N, c->node_cost.begin() + (size_t)(l + 1) * c->N, nc.begin() + (size_t)l * N);
     c->node_cost.swap(nc);
   }
+  if (!c->node_cap.empty()) {  // (holding nodes are free)
+    const int TN = c->node_cap_tv ? T + 1 : 1;
+    std::vector<double> dn((size_t)TN * N, INFINITY);
+    for (int t = 0; t < TN; ++t)
+      std::copy(c->node_cap.begin() + (size_t)t * c->N, c->node_cap.begin() + (size_t)(t + 1) * c->N, dn.begin() + (size_t)t * N);
+    c->node_cap.swap(dn);
+  }
   c->N = N;
   c->A = A1;
   c->augmented = true;
@@ -1033,6 +1042,13 @@ size_t layout(mmf_ctx* c, char* base) {
   p.u0e = at(L.take(N * Lp * se));
   p.dnm = c->node_cost.empty() ? nullptr : at(L.take(N * Lp * sm));
   p.dne = c->node_cost.empty() ? nullptr : at(L.take(N * Lp * se));
+  const bool ncap = !c->node_cap.empty();
+  p.dnc = ncap ? at(L.take((c->node_cap_tv ? T + 1 : 1) * N * sm)) : nullptr;
+  p.dnc_tv = c->node_cap_tv ? 1 : 0;
+  p.unm = ncap ? at(L.take((T + 1) * N * sm)) : nullptr;
+  p.une = ncap ? (int*)at(L.take((T + 1) * N * 4)) : nullptr;
+  p.unlm = nullptr;
+  p.unle = nullptr;
   if (!c->point) {
     p.mu0m = at(L.take(N * Lp * sm));
     p.mu0e = at(L.take(N * Lp * se));
@@ -1169,13 +1185,27 @@ template <class T_> struct Eng {
 
   // the device pointers for a launch whose output messages are layer `layer`: the commodity node factor D (NEXT-2,
   // reading R-N) applies at the intermediate layers 1..T-1 only
-  static DevPtrs lay(const mmf_ctx* c, int layer) {
+  // (with_u: the node-capacity dual u_layer (NEXT-3) too — backward and readout launches; the forward sweep's launches
+  // write alpha without it and k_node_cap applies the updated u)
+  static DevPtrs lay(const mmf_ctx* c, int layer, bool with_u = true) {
     DevPtrs d = c->dp;
+    d.unlm = nullptr;
+    d.unle = nullptr;
     if (layer < 1 || layer > c->T - 1) {
       d.dnm = nullptr;
       d.dne = nullptr;
+    } else if (with_u && d.unm) {
+      d.unlm = (const char*)d.unm + (size_t)layer * c->N * c->sm();
+      d.unle = d.une + (size_t)layer * c->N;
     }
     return d;
+  }
+  // NEXT-3 node-capacity block of layer t (1..T-1): u_t from the marginal of alpha_t (written without u_t) and the
+  // stored beta-hat_t, then alpha_t *= u_t
+  static void node_cap(mmf_ctx* c, cudaStream_t s, int t) {
+    if (!c->dp.unm || t < 1 || t > c->T - 1) return;
+    LaunchScope ls(c, K_UPDATE, s);
+    k_node_cap<T_><<<c->N, 256, 0, s>>>(c->dp, t);
   }
 
   static void zero_slot(mmf_ctx* c, cudaStream_t s, void* pm, void* pe) {
@@ -1247,7 +1277,7 @@ template <class T_> struct Eng {
     }
     {
       LaunchScope ls(c, K_UPDATE, s);
-      k_spmm_fwd<T_><<<grid, c->block, 0, s>>>(lay(c, t + 1), t);
+      k_spmm_fwd<T_><<<grid, c->block, 0, s>>>(lay(c, t + 1, readout != 0), t);
     }
     return MMF_OK;
   }
@@ -1255,7 +1285,7 @@ template <class T_> struct Eng {
   // ---------------- node-tile path (opt_kernels == 2)
   template <int CPT, int MODE, int FMODE> static void launch_fwd(mmf_ctx* c, cudaStream_t s, int t, size_t smem) {
     dim3 grid(c->ntiles, c->pc.ngroup);
-    k_fwd_tile<T_, CPT, MODE, FMODE><<<grid, TILE_THREADS, smem, s>>>(lay(c, t), c->tm, c->pc, t);
+    k_fwd_tile<T_, CPT, MODE, FMODE><<<grid, TILE_THREADS, smem, s>>>(lay(c, t, FMODE == 2), c->tm, c->pc, t);
   }
   template <int CPT> static void tiled_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
     const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
@@ -1300,7 +1330,7 @@ template <class T_> struct Eng {
   // ---------------- wide-lane path (opt_kernels == 3)
   template <int CPT, int MODE, int FMODE> static void launch_fwd_wide(mmf_ctx* c, cudaStream_t s, int t) {
     dim3 grid((c->N + c->wc.npc - 1) / c->wc.npc, c->wc.ngroup);
-    k_fwd_wide<T_, CPT, MODE, FMODE><<<grid, WIDE_THREADS, wide_smem<M>(c->wc.max_oa, c->wc.cpcta), s>>>(lay(c, t), c->wc, t);
+    k_fwd_wide<T_, CPT, MODE, FMODE><<<grid, WIDE_THREADS, wide_smem<M>(c->wc.max_oa, c->wc.cpcta), s>>>(lay(c, t, FMODE == 2), c->wc, t);
   }
   template <int CPT> static void wide_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
     const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
@@ -1324,7 +1354,7 @@ template <class T_> struct Eng {
   template <int CPT, int MODE, bool KEEP> static void launch_fwd_head(mmf_ctx* c, cudaStream_t s, int t) {
     const HeadCfg& h = c->hc;
     dim3 grid((c->N + h.npc - 1) / h.npc);
-    k_fwd_head<T_, CPT, MODE, KEEP><<<grid, h.npc * h.wpn * 32, head_smem<M>(h.max_ia, h.nch), s>>>(lay(c, t), h, t);
+    k_fwd_head<T_, CPT, MODE, KEEP><<<grid, h.npc * h.wpn * 32, head_smem<M>(h.max_ia, h.nch), s>>>(lay(c, t, false), h, t);
   }
   template <int CPT> static void head_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
     const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
@@ -1366,7 +1396,7 @@ template <class T_> struct Eng {
     const PipeCfg5& pc = c->pf;
     const unsigned grid = (unsigned)std::min((c->N + NP - 1) / NP, c->sms);
     k_fwd_pipe<CPT, GW, NG, NP, MODE>
-        <<<grid, fwd_threads<GW, NG, NP>(), NP * pfwd_smem(pc.R, pc.D, pc.SW, NG).total, s>>>(lay(c, t), pc, t);
+        <<<grid, fwd_threads<GW, NG, NP>(), NP * pfwd_smem(pc.R, pc.D, pc.SW, NG).total, s>>>(lay(c, t, MODE == 3), pc, t);
   }
   template <int MODE> static void pipe_fwd_mode(mmf_ctx* c, cudaStream_t s, int t) {
     const int SW = c->pf.SW, gw = c->pf_gw, ng = c->pf_ng, np = c->pf_np;
@@ -1506,7 +1536,10 @@ template <class T_> struct Eng {
   // Algorithm 2's sweep (a2, forward with the W updates, a4, and the backward pass a5 when do_bwd)
   static mmf_status gs_sweep(mmf_ctx* c, cudaStream_t s, bool do_bwd) {
     if (c->opt_kernels >= 5 && c->pipe_fwd && !c->comm) {
-      for (int t = 0; t <= c->T; ++t) pipe_fwd(c, s, t);       // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
+      for (int t = 0; t <= c->T; ++t) {
+        pipe_fwd(c, s, t);  // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
+        node_cap(c, s, t);  // (node capacities: u_t, P:1093 on the states)
+      }
       if (do_bwd)
         for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
       return MMF_OK;
@@ -1534,6 +1567,7 @@ template <class T_> struct Eng {
     for (int t = 0; t < c->T; ++t) {
       mmf_status st = fwd_step(c, s, t, 0);  // a3
       if (st != MMF_OK) return st;
+      node_cap(c, s, t + 1);
     }
     boundary(c, s, 1);  // a4
     if (do_bwd) bwd_pass(c, s);  // a5
@@ -2017,6 +2051,34 @@ mmf_status finalize(mmf_ctx* ctx) {
     CU(cudaMemcpyAsync((void*)p.dnm, hDm.data(), hDm.size(), cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync((void*)p.dne, hDe.data(), hDe.size(), cudaMemcpyHostToDevice, s));
   }
+  std::vector<char> hdn;
+  if (p.dnc) {  // node capacities (internal node order); u = 1
+    const int TN = c->node_cap_tv ? c->T + 1 : 1;
+    hdn.assign((size_t)TN * N * sm, 0);
+    for (int t = 0; t < TN; ++t)
+      for (int v = 0; v < N; ++v) {
+        const double d = c->node_cap[(size_t)t * N + v];
+        const size_t k = (size_t)t * N + c->newid[v];
+        if (f32)
+          ((float*)hdn.data())[k] = (float)d;
+        else
+          ((double*)hdn.data())[k] = d;
+      }
+    CU(cudaMemcpyAsync((void*)p.dnc, hdn.data(), hdn.size(), cudaMemcpyHostToDevice, s));
+  }
+  std::vector<char> hum;
+  if (p.unm) {  // u = 1 (significand 1, exponent 0)
+    const size_t n = (size_t)(c->T + 1) * N;
+    hum.assign(n * sm, 0);
+    for (size_t k = 0; k < n; ++k) {
+      if (f32)
+        ((float*)hum.data())[k] = 1.f;
+      else
+        ((double*)hum.data())[k] = 1.0;
+    }
+    CU(cudaMemcpyAsync(p.unm, hum.data(), hum.size(), cudaMemcpyHostToDevice, s));
+    CU(cudaMemsetAsync(p.une, 0, n * 4, s));
+  }
   CU(cudaMemsetAsync(p.err, 0, 8, s));
   CU(cudaMemsetAsync(p.errloc, 0, 8, s));
   // host staging buffers die at return: wait for the copies
@@ -2122,6 +2184,7 @@ static uint64_t problem_hash(const mmf_ctx* c) {
   for (double x : c->cap) f.mixd(x);
   f.mix((uint64_t)c->node_cost.size());
   for (double x : c->node_cost) f.mixd(x);
+  for (double x : c->node_cap) f.mixd(x);
   return f.h;
 }
 // W [T][A] (user arc order), then UT = beta_T and U0 (the last a2's source scaling; readouts before the next sweep
@@ -2401,6 +2464,44 @@ mmf_status mmf_set_node_costs(mmf_ctx* ctx, const double* c) {
   return MMF_OK;
 }
 
+mmf_status mmf_set_node_capacity(mmf_ctx* ctx, const double* cap, int time_varying) {
+  if (!ctx) return MMF_EINVAL;
+  if (ctx->inited || ctx->augmented) return fail(ctx, MMF_ESTATE, "node capacities must be set before the layout");
+  if (!ctx->have_cost) return fail(ctx, MMF_ESTATE, "mmf_set_costs first");
+  if (!cap) {
+    ctx->node_cap.clear();
+    ctx->prepared = false;
+    return MMF_OK;
+  }
+  const size_t n = (size_t)(time_varying ? ctx->T + 1 : 1) * ctx->N;
+  for (size_t k = 0; k < n; ++k)
+    if (!(cap[k] >= 0)) return fail(ctx, MMF_EINVAL, "node capacity < 0 or NaN");
+  ctx->node_cap.assign(cap, cap + n);
+  ctx->node_cap_tv = time_varying != 0;
+  ctx->prepared = false;
+  return MMF_OK;
+}
+
+mmf_status mmf_read_node_duals(mmf_ctx* ctx, double* out) {
+  if (!ctx || !out) return MMF_EINVAL;
+  if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  if (ctx->node_cap.empty()) return fail(ctx, MMF_EINVAL, "no node capacities");
+  mmf_status st = mmf_sync(ctx);
+  if (st != MMF_OK) return st;
+  const size_t n = (size_t)(ctx->T + 1) * ctx->N;
+  std::vector<char> m(n * ctx->sm());
+  std::vector<int> e(n);
+  CU(cudaMemcpy(m.data(), ctx->dp.unm, m.size(), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(e.data(), ctx->dp.une, n * 4, cudaMemcpyDeviceToHost));
+  for (int t = 0; t <= ctx->T; ++t)
+    for (int v = 0; v < ctx->N_user; ++v) {
+      const size_t k = (size_t)t * ctx->N + ctx->newid[v];
+      const double mm = ctx->prec == MMF_FP32 ? (double)((const float*)m.data())[k] : ((const double*)m.data())[k];
+      out[(size_t)t * ctx->N_user + v] = mm == 0.0 ? 0.0 : std::ldexp(mm, e[k]);
+    }
+  return MMF_OK;
+}
+
 mmf_status mmf_set_commodity_times(mmf_ctx* ctx, const int32_t* t_in, const int32_t* t_out) {
   if (!ctx) return MMF_EINVAL;
   if (ctx->inited || ctx->augmented) return fail(ctx, MMF_ESTATE, "commodity times must be set before the layout");
@@ -2491,6 +2592,12 @@ mmf_status mmf_init(mmf_ctx* ctx) {
   CU(cudaSetDevice(ctx->device));
   mmf_status st = finalize(ctx);
   if (st != MMF_OK) return st;
+  if (!ctx->node_cap.empty()) {
+    const bool fam = ctx->opt_kernels == 1 || (ctx->prec == MMF_FP32 && ctx->opt_kernels >= 5 && ctx->pipe_fwd);
+    if (!fam || ctx->opt_schedule == 1 || ctx->comm)
+      return fail(ctx, MMF_EINVAL, "node capacities: the pipelined fp32 path (L >= 256) or kernels = 1, Gauss-Seidel "
+                                   "or symmetric schedule, one rank");
+  }
   st = dispatch(ctx, [&](auto eng) { return decltype(eng)::init_device(ctx, ctx->stream); });
   if (st != MMF_OK) return st;
   CU(cudaGetLastError());
@@ -2661,6 +2768,7 @@ mmf_status mmf_state_bytes(const mmf_ctx* ctx, size_t* bytes) {
 mmf_status mmf_save_state(mmf_ctx* ctx, void* buf, size_t bytes) {
   if (!ctx || !buf) return MMF_EINVAL;
   if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
+  if (!ctx->node_cap.empty()) return fail(ctx, MMF_EINVAL, "checkpoints do not cover node capacities");
   if (bytes < mmf::state_bytes(ctx)) return fail(ctx, MMF_EINVAL, "state buffer too small (mmf_state_bytes)");
   mmf_status st = mmf_sync(ctx);
   if (st != MMF_OK) return st;
@@ -2802,7 +2910,23 @@ mmf_status mmf_read_stats(mmf_ctx* ctx, mmf_stats* out) {
   out->src_mismatch = s[1];
   out->sink_mismatch = s[2];
   out->cap_violation = viol;
-  out->dual = ctx->eps * (-s[0] + s[3] + s[4] + s[5]);
+  double snode = 0.0;  // NEXT-3: sum_t <d_t, log u_t> over finite positive node capacities
+  if (!ctx->node_cap.empty()) {
+    const size_t n = (size_t)(ctx->T + 1) * ctx->N;
+    std::vector<char> m(n * ctx->sm());
+    std::vector<int> e(n);
+    CU(cudaMemcpy(m.data(), ctx->dp.unm, m.size(), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(e.data(), ctx->dp.une, n * 4, cudaMemcpyDeviceToHost));
+    for (int t = 1; t < ctx->T; ++t)
+      for (int v = 0; v < ctx->N; ++v) {
+        const double d = ctx->node_cap[(size_t)(ctx->node_cap_tv ? t : 0) * ctx->N + v];
+        if (!(d > 0) || std::isinf(d)) continue;
+        const size_t k = (size_t)t * ctx->N + ctx->newid[v];
+        const double mm = ctx->prec == MMF_FP32 ? (double)((const float*)m.data())[k] : ((const double*)m.data())[k];
+        snode += d * (std::log(mm) + e[k] * 0.69314718055994530942);
+      }
+  }
+  out->dual = ctx->eps * (-s[0] + s[3] + s[4] + s[5] + snode);
   out->primal = primal;
   return MMF_OK;
 }

@@ -178,6 +178,15 @@ __device__ __forceinline__ void norm_lane(const DevPtrs& p, const typename T_::M
         e += 1;
       }
     }
+    if (p.unlm && m != M(0)) {  // node-capacity dual of this layer (NEXT-3)
+      m *= ((const M*)p.unlm)[node];
+      e += p.unle[node];
+      if (m >= M(2)) {
+        m *= M(0.5);
+        e += 1;
+      }
+      if (m == M(0)) e = EZERO;
+    }
     if (e > ELIM || (m != M(0) && e < -ELIM)) {
       set_error(p, ERR_RANGE, l0 + c, node);
       e = e > 0 ? ELIM : -ELIM;

@@ -742,3 +742,59 @@ def test_symmetric_gs_with_node_costs_and_times():
     p = dataclasses.replace(p, T=10, t_in=t_in, t_out=np.minimum(t_in + 8, 10),
                             node_cost=rng.uniform(0, 0.3, size=(p.L, p.N)))
     assert_parity(p, 3, "fp32", oracle_kw=dict(schedule="sym"), options=dict(schedule=2))
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-3: node (state) capacities and the paper's state spaces on a synthetic street map
+
+def _with_node_caps(p, seed, lo, hi, frac=0.5, tv=False):
+    import dataclasses
+    rng = np.random.default_rng(seed)
+    shape = (p.T + 1, p.N) if tv else (p.N,)
+    d = rng.uniform(lo, hi, size=shape)
+    d[rng.random(shape) > frac] = np.inf
+    return dataclasses.replace(p, node_cap=d)
+
+
+def _node_parity(p, sweeps, prec, opts, oracle_kw=None):
+    from paper_2106_14485_b200 import Solver
+    assert_parity(p, sweeps, prec, oracle_kw=oracle_kw, options=opts)
+    st = oracle_run(p, sweeps, **(oracle_kw or {}))
+    with Solver(p, prec=prec, options=opts) as s:
+        s.sweep(sweeps)
+        U = s.node_duals()
+    assert max_rel_err(U, np.exp(st.nu), W_FLOOR) < TOL[prec]
+    assert np.min(np.exp(st.nu)) < 0.99
+
+
+@pytest.mark.parametrize("prec,L,marg,opts,tv", [("fp32", 1019, "point", {}, False), ("fp64", 20, "point", dict(kernels=1), True),
+                                                 ("fp32", 30, "dense", dict(kernels=1), False),
+                                                 ("fp32", 1019, "point", dict(schedule=2), False)])
+def test_node_caps_parity(prec, L, marg, opts, tv):
+    """Node capacities (Algorithm 2's u_t on the states, k_node_cap after each forward step; pinned against brute-force
+    tensors in tests/test_oracle_pins.py): flows, arc duals, node duals and statistics against the oracle."""
+    sc = L / 64  # (mean node marginal)
+    p = _with_node_caps(grid_problem(8, 8, 7, L, 0.2, seed=52, cap=(5 * sc, 20 * sc), marginals=marg), 3, 0.4 * sc,
+                        1.5 * sc, tv=tv)
+    okw = dict(schedule="sym") if opts.get("schedule") == 2 else None
+    _node_parity(p, 4, prec, opts, okw)
+
+
+def test_node_caps_unsupported_family_is_einval():
+    from paper_2106_14485_b200 import MMFError, Solver
+    p = _with_node_caps(grid_problem(5, 5, 5, 20, 0.2, seed=52), 3, 1.0, 2.0)
+    with pytest.raises(MMFError) as e:
+        Solver(p, prec="fp64")  # (fp64 default: the wide-lane kernels)
+    assert e.value.name == "MMF_EINVAL"
+
+
+@pytest.mark.parametrize("policy,prec,L,opts", [("edges+stay", "fp32", 257, {}), ("vertex_storage", "fp32", 300, {}),
+                                                ("traffic", "fp32", 300, {}), ("traffic", "fp64", 12, dict(kernels=1)),
+                                                ("vertex_storage", "fp64", 12, dict(kernels=1))])
+def test_state_space_problems_parity(policy, prec, L, opts):
+    """The arc-state (edges with staying), vertex-storage and traffic-routing state spaces of P:612, P:704-720 on a
+    synthetic street map of the §5.3 size (57 junctions, 150 directed streets): state capacities (node capacities),
+    commodity state costs C_L (node costs), against the oracle."""
+    from workloads.statespace import state_problem
+    p = state_problem(policy, T=12, eps=0.1, seed=2, L=L, edge_cap=(0.004 * L, 0.012 * L))
+    _node_parity(p, 4, prec, opts)

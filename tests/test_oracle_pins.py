@@ -879,3 +879,83 @@ def test_symmetric_gs_dual_monotone_and_same_optimum():
     Fg, Wg = readout_flows(gs)
     assert max_rel_err(Ws, Wg, 1e-12) < 1e-8 and max_rel_err(Fs, Fg, 1e-12) < 1e-8
     assert np.any(Wg < 0.99)
+
+
+# ---------------------------------------------------------------------------------------------
+# NEXT-3: node (state) capacities, Algorithm 2's u_t on the states (eq:multicommodity P:676-683)
+
+def _node_caps(p, seed, frac=0.5, lo=0.2, hi=0.6, tv=False):
+    import dataclasses
+    rng = np.random.default_rng(seed)
+    shape = (p.T + 1, p.N) if tv else (p.N,)
+    d = rng.uniform(lo, hi, size=shape)
+    d[rng.random(shape) > frac] = np.inf
+    return dataclasses.replace(p, node_cap=d)
+
+
+@pytest.mark.parametrize("kw,tv", [(MICROS[0], False), (MICROS[1], True), (MICROS[4], False), (MICROS[6], False)])
+def test_node_caps_iterates_identical_to_full_tensor(kw, tv):
+    """P1 with node capacities: the GS blocks U0, W_0, u_1, W_1, ..., u_{T-1}, W_{T-1}, UT (prp:sinkhorn with the state
+    marginals' inequality constraints) with every projection a literal sum of the full tensor M = K ⊙ U
+    (U including prod_t u_t[v_t]) equal the oracle's sweeps iterate by iterate."""
+    p = _node_caps(_micro(kw), seed=3, tv=tv)
+    st = oracle_init(p)
+    bs = BruteState(p)
+    for k in range(8):
+        oracle_sweep(st)
+        brute_sweep(bs)
+        assert max_rel_err(np.exp(st.lam0), bs.U0, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.omega), bs.W, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.nu), bs.Un, 1e-300) < 1e-12, k
+        assert max_rel_err(np.exp(st.lamT), bs.UT, 1e-300) < 1e-12, k
+    F, _ = readout_flows(st)
+    assert max_rel_err(F, arc_flows(p, bs.tensor()), 1e-300) < 1e-12
+    assert np.min(np.exp(st.nu)) < 0.99
+
+
+def test_node_cap_on_a_single_in_arc_node_equals_the_arc_capacity():
+    """A node whose only in-arc is a: its marginal at layer t is the flow of a at step t - 1, so a node capacity d on it
+    (layers 1..T-1) is the arc capacity d on a at steps 0..T-2 — the already pinned arc-capacity path: same flows."""
+    import dataclasses
+    from workloads.configs import Problem
+    # 0 -> 1 -> 2 -> 3 and 0 -> 4 -> 3 (loops at 0, 2, 3, 4; node 1's only in-arc is 0 -> 1)
+    tail = np.array([0, 1, 2, 0, 4, 0, 2, 3, 4], np.int32)
+    head = np.array([1, 2, 3, 4, 3, 0, 2, 3, 4], np.int32)
+    T, A = 5, tail.size
+    cost = np.array([0.2, 0.3, 0.1, 0.6, 0.5, 0.05, 0.05, 0.05, 0.05])
+    p = Problem("chain", 5, tail, head, T, 0.3, cost, np.full(A, np.inf), 2, src=np.array([0, 0], np.int32),
+                dst=np.array([3, 3], np.int32), mass=np.array([1.0, 0.7]))
+    dn = np.full(5, np.inf)
+    dn[1] = 0.6
+    q = dataclasses.replace(p, node_cap=dn)
+    cap = np.full((T, A), np.inf)
+    cap[: T - 1, 0] = 0.6
+    r = dataclasses.replace(p, cap=cap)
+    Fq, _ = readout_flows(oracle_run(q, 6))
+    Fr, _ = readout_flows(oracle_run(r, 6))
+    assert max_rel_err(Fq, Fr, 1e-300) < 1e-12
+    assert Fq[: T - 1, 0].max() > 0.3
+
+
+def test_node_caps_dual_monotone_and_strong_duality():
+    """BCA with the node blocks: the dual (now with sum <d_t, log u_t>) never decreases after any block, and
+    at convergence equals the regularised primal of the brute-force tensor (thm:solution P:777-788)."""
+    p = _node_caps(grid_problem(2, 3, 4, 2, 0.5, seed=2, cap=(0.3, 0.6)), seed=5, lo=0.3, hi=0.8, frac=0.6)
+    st = oracle_init(p)
+    vals = []
+    for _ in range(15):
+        oracle_sweep(st, on_block=lambda kind, t, mass: vals.append(dual_objective(st, mass)))
+    v = np.array(vals)
+    assert np.all(np.diff(v) >= -1e-12 * np.abs(v).max())
+    for _ in range(3000):
+        oracle_sweep(st)
+    M = full_tensor(p, np.exp(st.lam0), np.exp(st.omega), np.exp(st.lamT), np.exp(st.nu))
+    C = _cost_tensor(p)
+    pos = M > 0
+    primal = (C[pos] * M[pos]).sum() + p.eps * (M[pos] * np.log(M[pos]) - M[pos]).sum()
+    phi = dual_objective(st, float(np.exp(st.a[p.T] + st.lamT).sum()))
+    assert abs(primal - phi) <= 1e-9 * abs(phi), (primal, phi)
+    assert np.min(np.exp(st.nu)) < 0.99
+    P = np.stack([commodity_marginal(M, t).sum(axis=0) for t in range(p.T + 1)])
+    dn = np.broadcast_to(p.node_cap, P.shape)
+    assert np.all(P[1:p.T] <= dn[1:p.T] * (1 + 1e-8))

@@ -69,6 +69,9 @@ class Problem:
     # P:1139-1149); None = 0 / T
     t_in: Optional[np.ndarray] = None
     t_out: Optional[np.ndarray] = None
+    # node (state) capacities d_t[j] on the node marginal at the intermediate layers ([N] or
+    # [T+1, N]; +inf free, 0 closed; layers 0 and T ignored): the paper's P_t(M) <= d_t of eq:multicommodity
+    node_cap: Optional[np.ndarray] = None
 
     @property
     def A(self) -> int:
