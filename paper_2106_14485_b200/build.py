@@ -31,23 +31,34 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
-        return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", *SOURCES, "-ldl"]
+LIB_DEBUG = os.path.join(HERE, "libmmf_debug.so")  # -DMMF_DEBUG: device-side checks (csrc/xf.cuh MMF_DASSERT)
+
+
+def needs_build_debug() -> bool:
+    if not os.path.exists(LIB_DEBUG):
+        return True
+    t = os.path.getmtime(LIB_DEBUG)
+    return any(os.path.getmtime(p) > t for p in DEPS)
+
+
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    lib = LIB_DEBUG if debug else LIB
+    if not force and not (needs_build_debug() if debug else needs_build()):
+        return lib
+    extra = ["-DMMF_DEBUG"] if debug else []
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp", *SOURCES, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libmmf.so")
-    log = os.path.join(HERE, "build_ptxas.log")
+    log = os.path.join(HERE, "build_ptxas_debug.log" if debug else "build_ptxas.log")
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if verbose:
         sys.stdout.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, debug="--debug" in sys.argv))

@@ -414,6 +414,7 @@ template <class T_> __global__ void __launch_bounds__(256) k_node_cap(DevPtrs p,
     }
   }
   __syncthreads();
+  MMF_DASSERT(nm == 0.0 || (nm >= 1.0 && nm < 2.0 && ne <= 0));  // (u in [0, 1])
   if (threadIdx.x == 0) {
     um[j] = (M)nm;
     ue[j] = ne;

@@ -12,6 +12,7 @@
 #include "reuse.cuh"
 
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>  // (header-only NVTX3: ranges go to a profiler when one is attached, else no-ops)
 #include <cstdlib>
 
 #include <algorithm>
@@ -199,6 +200,12 @@ mmf_status fail(mmf_ctx* c, mmf_status s, const std::string& msg) {
   if (c) c->err = msg;
   return s;
 }
+
+// NVTX range of a host-side scope (sweep, pass, step, readout); under CUDA-graph capture the ranges mark the capture
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 #define CU2(c, call)                                                                               \
   do {                                                                                             \
@@ -1406,6 +1413,7 @@ template <class T_> struct Eng {
 #undef MMF_FWD_COMBO
   }
   static void pipe_fwd(mmf_ctx* c, cudaStream_t s, int t) {
+    Nvtx r(t == 0 ? "a2" : t == c->T ? "a3 + a4 step" : "a3 step");
     if constexpr (sizeof(M) == 4) {
       if (t == 0) {  // a2: elementwise, the head kernel's MODE 0
         head_fwd(c, s, 0);
@@ -1428,6 +1436,7 @@ template <class T_> struct Eng {
     k_bwd_pipe<CPT><<<grid, PIPE_THREADS, pipe_smem(pc.R, pc.SD, pc.D, pc.SW).total, s>>>(lay(c, t), pc, t);
   }
   static void tiled_bwd(mmf_ctx* c, cudaStream_t s, int t) {
+    Nvtx r("a5 step");
     LaunchScope ls(c, K_BWD, s);
     if constexpr (sizeof(M) == 4) {
       if (c->win_bwd) {
@@ -1528,6 +1537,7 @@ template <class T_> struct Eng {
   }
 
   static mmf_status enqueue_sweep(mmf_ctx* c, cudaStream_t s) {
+    Nvtx r("mmf sweep");
     if (c->opt_schedule == 1) return jacobi_sweep(c, s);
     if (c->opt_schedule == 2) return symmetric_sweep(c, s);
     return gs_sweep(c, s, true);
@@ -1536,12 +1546,17 @@ template <class T_> struct Eng {
   // Algorithm 2's sweep (a2, forward with the W updates, a4, and the backward pass a5 when do_bwd)
   static mmf_status gs_sweep(mmf_ctx* c, cudaStream_t s, bool do_bwd) {
     if (c->opt_kernels >= 5 && c->pipe_fwd && !c->comm) {
-      for (int t = 0; t <= c->T; ++t) {
-        pipe_fwd(c, s, t);  // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
-        node_cap(c, s, t);  // (node capacities: u_t, P:1093 on the states)
+      {
+        Nvtx r("forward pass (a2, a3, a4)");
+        for (int t = 0; t <= c->T; ++t) {
+          pipe_fwd(c, s, t);  // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
+          node_cap(c, s, t);  // (node capacities: u_t, P:1093 on the states)
+        }
       }
-      if (do_bwd)
+      if (do_bwd) {
+        Nvtx r("backward pass (a5)");
         for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      }
       return MMF_OK;
     }
     if (c->opt_kernels == 4 && !c->comm) {
@@ -1580,6 +1595,7 @@ template <class T_> struct Eng {
   // flows on the multi-GPU path), the backward step
   static mmf_status symmetric_sweep(mmf_ctx* c, cudaStream_t s) {
     mmf_status st = gs_sweep(c, s, false);
+    Nvtx r("symmetric backward pass");
     if (st != MMF_OK) return st;
     const bool pipe = sizeof(M) == 4 && c->opt_kernels >= 5 && c->pipe_fwd && !c->comm;
     const unsigned ga = (unsigned)((c->A + 255) / 256);
@@ -1746,6 +1762,7 @@ template <class T_> struct Eng {
   // forward pass with the current factors (no dual update): alpha_t of the current state and the flows of every
   // step into Fout (exchanged per step over the ranks if asked)
   static mmf_status forward_flows(mmf_ctx* ctx, cudaStream_t s, bool exchange_each) {
+    Nvtx r("readout forward pass");
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
     if (c->opt_kernels >= 2) {
@@ -2587,6 +2604,7 @@ mmf_status mmf_attach_nccl(mmf_ctx* ctx, const void* unique_id128, int nranks, i
 
 mmf_status mmf_init(mmf_ctx* ctx) {
   if (!ctx) return MMF_EINVAL;
+  Nvtx r("mmf_init");
   if (ctx->inited) return fail(ctx, MMF_ESTATE, "already initialised");
   if (!ready_for_layout(ctx)) return fail(ctx, MMF_ESTATE, "graph, costs, capacity and marginals must be set");
   CU(cudaSetDevice(ctx->device));
@@ -2608,6 +2626,7 @@ mmf_status mmf_init(mmf_ctx* ctx) {
 
 mmf_status mmf_sweep(mmf_ctx* ctx, int32_t n) {
   if (!ctx) return MMF_EINVAL;
+  Nvtx r("mmf_sweep");
   if (!ctx->inited) return fail(ctx, MMF_ESTATE, "mmf_init first");
   if (n < 0) return fail(ctx, MMF_EINVAL, "n < 0");
   if (n == 0) return MMF_OK;

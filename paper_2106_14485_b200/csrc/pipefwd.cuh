@@ -910,6 +910,8 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
       const int ds = k & (FWD_SDF - 1);
       FwdHdr& h = hdr[ds];
       const int rs = __popc(obal & ((1u << lane) - 1u));
+      MMF_DASSERT(rr.rpos >= 0 && rr.rpos + nrow <= R);                 // (items never wrap)
+      MMF_DASSERT(!valid || (r.node >= 0 && r.node < p.N && lane < D));  // (ELL record: a node of the graph)
       if (ok) {
         h.kb[rs] = __float_as_uint(r.km);
         h.k2[rs] = pack2(r.ke);
@@ -975,6 +977,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     mbar_wait(&full[ds], (k / FWD_SDF) & 1);
     const FwdHdr& h = hdr[ds];
     const ArcOps* hops = oring + h.oslot * D;
+    MMF_DASSERT(h.start >= 0 && h.start + h.nr <= R && h.nr <= h.na && h.na <= D && h.oslot < PIPE_RP);
     if (pc.dry == 1) {  // diagnostics: delivery rate of the producer / TMA alone
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[ds]);
@@ -1170,6 +1173,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
       }
       const int ds = k & (FWD_SD - 1);
       const int slot = __popc(bal & ((1u << lane) - 1u));
+      MMF_DASSERT(!ok || (r.node >= 0 && r.node < p.N));
+      MMF_DASSERT(rr.rpos >= 0 && rr.rpos < R && n <= R);
       if (ok) {
         hdr[ds].kb[slot] = __float_as_uint(r.km);
         hdr[ds].k2[slot] = pack2(r.ke);

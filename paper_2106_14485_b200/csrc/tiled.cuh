@@ -191,6 +191,8 @@ __device__ __forceinline__ void norm_lane(const DevPtrs& p, const typename T_::M
       set_error(p, ERR_RANGE, l0 + c, node);
       e = e > 0 ? ELIM : -ELIM;
     }
+    MMF_DASSERT(m == M(0) ? true : (m >= M(1) && m < M(2) && e >= -ELIM && e <= ELIM));
+    MMF_DASSERT(node >= 0 && node < p.N && l0 + c < p.Lp);
     out.m[c] = m;
     out.e[c] = (typename T_::E)e;
   }

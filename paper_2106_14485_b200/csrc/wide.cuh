@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(WIDE_THREADS, MMF_WIDE_MINB) k_fwd_wide(DevPtr
     } else {
       M s[CPT];
       int Ex[CPT];
+      MMF_DASSERT(p.in_ptr[j] >= 0 && p.in_ptr[j] <= p.in_ptr[j + 1] && p.in_ptr[j + 1] <= p.A);  // (CSR row)
       node_sum<T_, CPT>((const ArcKW<M>*)p.inrec + (size_t)(t - 1) * p.A, p.in_ptr[j], p.in_ptr[j + 1], v.am(t - 1),
                         v.ae(t - 1), p.Lp, col, wa, lane, s, Ex, wc.prefetch);
       norm_lane<T_, CPT>(p, s, Ex, a, l0, j);

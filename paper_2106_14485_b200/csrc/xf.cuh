@@ -7,6 +7,7 @@
 // spans of long horizons and small eps (SURVEY §8(d) dynamic-range table).
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace mmf {
@@ -34,6 +35,24 @@ constexpr int ELIM = 16000;
 
 // error bits of the sticky device error word
 constexpr unsigned ERR_INFEASIBLE = 1u, ERR_RANGE = 2u, ERR_NAN = 4u;
+
+// device-side checks of the debug build (-DMMF_DEBUG, libmmf_debug.so: the memory-safety net in place of
+// compute-sanitizer, which this pool does not offer): ring slots, CSR / ELL indices, message exponents; a failed
+// check prints its location and traps (the launch fails with cudaErrorIllegalInstruction -> MMF_ECUDA)
+#ifdef MMF_DEBUG
+#define MMF_DASSERT(c)                                                                          \
+  do {                                                                                          \
+    if (!(c)) {                                                                                 \
+      printf("MMF_DEBUG check failed: %s at %s:%d (block %d thread %d)\n", #c, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define MMF_DASSERT(c) \
+  do {                 \
+  } while (0)
+#endif
 
 // 2^d as M for d <= 0 (0 once below the normal range)
 template <class M> __device__ __forceinline__ M pow2_nonpos(int d) {
