@@ -59,4 +59,7 @@ def combine_stats(problem, pieces: list, omega: np.ndarray, sweeps: int) -> dict
         "cap_violation": float(np.maximum(F - cap, 0.0)[np.isfinite(cap)].max(initial=0.0)),
         "cap_excess": float(np.maximum(F - cap, 0.0)[np.isfinite(cap)].sum()),
         "sweeps": sweeps,
+        # magnitude of the dual's terms (the tolerance scale of a comparison of the dual: a sum of large terms of both
+        # signs): eps (mass + sum over shards of |s0| + |sT| + |sd|)
+        "dual_scale": float(p.eps * (mass + sum(abs(q["s0"]) + abs(q["sT"]) for q in pieces) + abs(sd))),
     }

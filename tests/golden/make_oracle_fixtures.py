@@ -26,6 +26,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import oracle_init, oracle_sweep, readout_flows, stats  # noqa: E402
+from oracle.sweep import dual_terms  # noqa: E402
 from workloads import gen  # noqa: E402
 
 # name: (config, overrides, snapshot sweep counts)   -- SURVEY §8(c) Q21 sweep counts, "lite" L
@@ -41,7 +42,7 @@ JOBS = {
 }
 NSAMPLE = 20000
 NSAMPLE_FULL = 100000
-STAT_KEYS = ("mass", "primal", "dual", "src_mismatch", "sink_mismatch", "cap_violation", "cap_excess")
+STAT_KEYS = ("mass", "primal", "dual", "src_mismatch", "sink_mismatch", "cap_violation", "cap_excess", "dual_scale")
 SCRATCH = os.path.join(ROOT, ".scratch")
 BIG = ("cfg4", "cfg5")
 
@@ -60,7 +61,8 @@ def _record(out, k, F, W, s, idx, rows):
     out[f"Frows_{k}"] = F[out["rows"]]
     out[f"Wrows_{k}"] = W[out["rows"]]
     for key in STAT_KEYS:
-        out[f"{key}_{k}"] = s[key]
+        if key in s:
+            out[f"{key}_{k}"] = s[key]
 
 
 def run(name):
@@ -76,7 +78,9 @@ def run(name):
         print(f"{name}: sweep {k} at {time.time() - t0:.0f}s", flush=True)
         if k in snaps:
             F, W = readout_flows(st)
-            _record(out, k, F, W, stats(st), idx, rows)
+            s = stats(st)
+            s["dual_scale"] = float(p.eps * (s["mass"] + sum(abs(x) for x in dual_terms(st))))
+            _record(out, k, F, W, s, idx, rows)
             np.savez_compressed(os.path.join(os.path.dirname(__file__), f"oracle_{name}.npz"), **out)
     print(f"{name}: done in {time.time() - t0:.0f}s")
 
@@ -150,13 +154,34 @@ def run_sharded(name, world):
     mp.spawn(_rank_main, args=(world, port, name), nprocs=world, join=True)
 
 
+
+def add_dual_scale(name):
+    """Post hoc for fixtures written before dual_scale was recorded: the same quantity from the per-shard pieces the
+    sharded run left in .scratch/ (oracle outputs of the fixture's last snapshot)."""
+    path = os.path.join(os.path.dirname(__file__), f"oracle_{name}.npz")
+    z = dict(np.load(path))
+    k = int(max(z["snaps"]))
+    world = int(z["shards"])
+    pieces = [np.load(os.path.join(SCRATCH, f"{name}_piece_{r}.npz")) for r in range(world)]
+    p = gen(*[JOBS[name][0]], **JOBS[name][1])
+    mass = sum(float(q["mass"]) for q in pieces)
+    assert abs(mass - float(z[f"mass_{k}"])) <= 1e-12 * mass, "pieces of another run"
+    z[f"dual_scale_{k}"] = float(p.eps * (mass + sum(abs(float(q["s0"])) + abs(float(q["sT"])) for q in pieces)
+                                          + abs(float(pieces[0]["sd"]))))
+    np.savez_compressed(path, **z)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--shards", type=int, default=1)
+    ap.add_argument("--add-dual-scale", action="store_true")
     ap.add_argument("names", nargs="+")
     a = ap.parse_args()
     for n in a.names:
-        if a.shards > 1:
+        if a.add_dual_scale:
+            add_dual_scale(n)
+        elif a.shards > 1:
             run_sharded(n, a.shards)
         else:
             run(n)
+
