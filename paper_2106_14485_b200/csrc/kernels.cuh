@@ -72,6 +72,7 @@ struct DevPtrs {
   const void* unlm;
   const int* unle;
   int diag;  // diagnostics of the pipelined forward (option "dry" >= 2; results invalid), else 0
+  int l2hint;  // 1: the pipelined kernels gather message rows with an L2 evict_last policy (option "l2hint")
   float theta;  // Jacobi schedule damping: W <- W^(1 - theta) min(W d / F, 1)^theta
 };
 

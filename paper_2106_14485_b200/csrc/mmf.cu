@@ -121,6 +121,7 @@ struct mmf_ctx {
   int opt_wintma = 1;   // window kernels: 1 = 2-D TMA row-block loads, 0 = per-thread cp.async
   int opt_schedule = 0;      // 0 Gauss-Seidel (Algorithm 2), 1 damped Jacobi
   int opt_theta_milli = 500;  // Jacobi damping theta in 1/1000
+  int opt_l2hint = 0;         // pipelined kernels: L2 evict_last policy on the gathered rows
   int opt_stripw = 0;   // (experiments) restrict the neighbour-overlap order's strip candidates to this width
   int opt_wrap = -1;    // k_bwd_pipe2 ring wrap: -1 auto, 0 items never wrap, 1 items may wrap
   int opt_fgw = 0;      // pipelined forward: warps per consumer group (0 auto, 8, 4, 2)
@@ -1100,6 +1101,7 @@ size_t layout(mmf_ctx* c, char* base) {
     const bool ell = c->pipe_bwd;
     p.Din = ell ? c->ell_din : 0;
     p.diag = c->opt_dry >= 2 ? c->opt_dry : 0;
+    p.l2hint = c->opt_l2hint;
     p.theta = (float)c->opt_theta_milli / 1000.f;
     p.Dout = ell ? c->pb.D : 0;
     p.ell_in = ell ? at(L.take(T * N * (size_t)p.Din * 16)) : nullptr;
@@ -1406,11 +1408,25 @@ template <class T_> struct Eng {
         <<<grid, fwd_threads<GW, NG, NP>(), NP * pfwd_smem(pc.R, pc.D, pc.SW, NG).total, s>>>(lay(c, t, MODE == 3), pc, t);
   }
   template <int MODE> static void pipe_fwd_mode(mmf_ctx* c, cudaStream_t s, int t) {
+    pipe_fwd_mode_launch<MODE>(c, s, t);
+    // (the pipelined epilogues skip the layer's node factors: D here, and u in the readout; the sweep's u is
+    // applied by k_node_cap)
+    if (MODE == 1 || MODE == 3) apply_factors(c, s, t, 0, MODE == 3);
+  }
+  template <int MODE> static void pipe_fwd_mode_launch(mmf_ctx* c, cudaStream_t s, int t) {
     const int SW = c->pf.SW, gw = c->pf_gw, ng = c->pf_ng, np = c->pf_np;
 #define MMF_FWD_COMBO(sw, cpt, g, n, q) \
   if (SW == sw && gw == g && ng == n && np == q) return pipe_fwd_launch<cpt, g, n, q, MODE>(c, s, t);
     MMF_FWD_COMBOS(MMF_FWD_COMBO)
 #undef MMF_FWD_COMBO
+  }
+  // node factors of layer t applied to a stored layer (which = 0 alpha_t, 1 beta_t) after a pipelined launch
+  static void apply_factors(mmf_ctx* c, cudaStream_t s, int t, int which, bool with_u) {
+    if (t < 1 || t > c->T - 1) return;
+    const DevPtrs d = lay(c, t, with_u);
+    if (!d.dnm && !d.unlm) return;
+    LaunchScope ls(c, K_OTHER, s);
+    k_apply_factors<T_><<<grid1d((size_t)c->N * c->Lp, 256), 256, 0, s>>>(d, t, which);
   }
   static void pipe_fwd(mmf_ctx* c, cudaStream_t s, int t) {
     Nvtx r(t == 0 ? "a2" : t == c->T ? "a3 + a4 step" : "a3 step");
@@ -1437,6 +1453,10 @@ template <class T_> struct Eng {
   }
   static void tiled_bwd(mmf_ctx* c, cudaStream_t s, int t) {
     Nvtx r("a5 step");
+    if (tiled_bwd_launch(c, s, t)) apply_factors(c, s, t, 1, true);  // (pipelined epilogues skip the factors)
+  }
+  // returns true for the pipelined families (their epilogues leave the layer's node factors out)
+  static bool tiled_bwd_launch(mmf_ctx* c, cudaStream_t s, int t) {
     LaunchScope ls(c, K_BWD, s);
     if constexpr (sizeof(M) == 4) {
       if (c->win_bwd) {
@@ -1449,7 +1469,7 @@ template <class T_> struct Eng {
           k_bwd_win<2><<<grid, WIN_THREADS, win_smem<2>(w).total, s>>>(lay(c, t), w, c->wdo, c->tmb, tma, t);
         else
           k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(lay(c, t), w, c->wdo, c->tmb, tma, t);
-        return;
+        return true;
       }
       if (c->ru_bwd) {
         const PipeCfg5& pc = c->pr;
@@ -1457,21 +1477,21 @@ template <class T_> struct Eng {
         const size_t sm = RU_NP * ru_smem(pc.R, pc.D, pc.SW).total;
         if (pc.SW == 1024) k_bwd_reuse<4><<<grid, RU_THREADS, sm, s>>>(lay(c, t), pc, t);
         else k_bwd_reuse<2><<<grid, RU_THREADS, sm, s>>>(lay(c, t), pc, t);
-        return;
+        return true;
       }
       if (c->pipe2_bwd) {
         const int cp = c->pb2.SW / 256;
         if (cp == 4) pipe2_bwd_cpt<4>(c, s, t);
         else if (cp == 2) pipe2_bwd_cpt<2>(c, s, t);
         else pipe2_bwd_cpt<1>(c, s, t);
-        return;
+        return true;
       }
       if (c->pipe_bwd) {
         const int cp = c->pb.SW / 256;
         if (cp == 4) pipe_bwd_cpt<4>(c, s, t);
         else if (cp == 2) pipe_bwd_cpt<2>(c, s, t);
         else pipe_bwd_cpt<1>(c, s, t);
-        return;
+        return true;
       }
     }
     if (c->opt_kernels >= 4) {
@@ -1479,18 +1499,19 @@ template <class T_> struct Eng {
       else if (c->CPT == 2 || !is_f32()) head_bwd_cpt<2>(c, s, t);
       else if (c->CPT == 4) head_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
       else head_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
-      return;
+      return false;
     }
     if (c->opt_kernels == 3) {
       if (c->CPT == 1) wide_bwd_cpt<1>(c, s, t);
       else if (c->CPT == 2 || !is_f32()) wide_bwd_cpt<2>(c, s, t);
       else if (c->CPT == 4) wide_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
       else wide_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
-      return;
+      return false;
     }
     if (c->CPT == 1) tiled_bwd_cpt<1>(c, s, t);
     else if (c->CPT == 2) tiled_bwd_cpt<2>(c, s, t);
     else tiled_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
+    return false;
   }
   static mmf_status tiled_attrs(mmf_ctx* ctx) {
     mmf_ctx* c = ctx;
@@ -2271,7 +2292,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -2303,6 +2324,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "wrap must be -1, 0 or 1");
       ctx->opt_wrap = (int)value;
     }
+    if (k == "l2hint") ctx->opt_l2hint = value != 0;
     if (k == "fnp") {
       if (value < 0 || value > 3) return fail(ctx, MMF_EINVAL, "fnp must be in [0, 3]");
       ctx->opt_fnp = (int)value;

@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(PIPE_THREADS, 1) k_bwd_pipe(DevPtrs p, PipeCfg
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
     Lane<M, E, CPT> out;
-    norm_lane<TrF32, CPT>(p, s, Ex, out, it.sl * SW + col, it.node);
+    norm_lane<TrF32, CPT, false>(p, s, Ex, out, it.sl * SW + col, it.node);
     const size_t g = (size_t)it.node * p.Lp + (size_t)(it.sl * SW + col);
     out.store(bmt + g, bet + g);
   }

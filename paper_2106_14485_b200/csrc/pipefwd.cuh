@@ -132,6 +132,29 @@ __host__ __device__ inline PFwdSmem pfwd_smem(int R, int D, int SW, int NG) {
   return m;
 }
 
+// L2 cache policy for the gathered message rows (option "l2hint"): a row of step t's messages is read by every
+// neighbour of its node within a short band of items, while the node's own row and the output rows stream once
+__device__ __forceinline__ unsigned long long l2_policy_keep() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                              unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_h(void* dst, const void* src, unsigned bytes, unsigned long long* bar, bool hint,
+                                           unsigned long long pol) {
+  if (hint)
+    bulk_g2s_hint(dst, src, bytes, bar, pol);
+  else
+    bulk_g2s(dst, src, bytes, bar);
+}
+
 __device__ __forceinline__ void bulk_prefetch_l2(const void* g, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(g), "r"(bytes) : "memory");
 }
@@ -852,6 +875,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     const int* We = v.We(t - 1);
     const M* Km = v.Km(t - 1);
     const int* Ke = v.Ke(t - 1);
+    const unsigned long long pol = l2_policy_keep();
     int pnode = j0, pslot = 0;
     auto prefetch = [&]() {
       if (pnode < p.N && lane < D) {
@@ -944,8 +968,8 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
       if (ok) {
         const size_t g = (size_t)r.node * p.Lp;
         const int q = rr.rpos + rs;
-        bulk_g2s(sig + q * SW, gm + g, SW * 4, &full[ds]);
-        bulk_g2s(sex + q * SW, ge + g, SW * 2, &full[ds]);
+        bulk_g2s_h(sig + q * SW, gm + g, SW * 4, &full[ds], p.l2hint, pol);
+        bulk_g2s_h(sex + q * SW, ge + g, SW * 2, &full[ds], p.l2hint, pol);
       }
       if (!MMF_FWD_OWNG && lane == 31) {  // the node's own beta_t row -> slot nr
         const size_t g = (size_t)j * p.Lp;
@@ -1012,7 +1036,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     const size_t g = (size_t)j * p.Lp + col;
     if constexpr (MODE == 2) {  // a4: UT = muT ./ alpha_T -> beta_T
       Lane<M, E, CPT> a;
-      norm_lane<TrF32, CPT>(p, s, Ex, a, col, j);
+      norm_lane<TrF32, CPT, false>(p, s, Ex, a, col, j);
       a.store(v.am(t) + g, v.ae(t) + g);
       Lane<M, E, CPT> ut;
       boundary_lane<TrF32, CPT>(p, 1, j, col, g, a, ut);
@@ -1021,7 +1045,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
       norm_store_f32<CPT>(p, s, Ex, v.am(t) + g, v.ae(t) + g, col, j);
     } else {
       Lane<M, E, CPT> a;
-      norm_lane<TrF32, CPT>(p, s, Ex, a, col, j);
+      norm_lane<TrF32, CPT, false>(p, s, Ex, a, col, j);
       a.store(v.am(t) + g, v.ae(t) + g);
     }
   }
@@ -1132,6 +1156,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
     ItemIt pf, cur;
     pf.init(item0, step, pc.ns);
     cur = pf;
+    const unsigned long long pol = l2_policy_keep();
     int pslot = 0;
     auto prefetch = [&]() {
       if (pf.node < p.N && lane < D) cp_async16(&ring[pslot * D + lane], ell + (size_t)pf.node * D + lane);
@@ -1191,8 +1216,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
         const size_t g = (size_t)r.node * p.Lp + (size_t)cur.sl * SW;
         int q = rr.rpos + slot;
         if (q >= R) q -= R;
-        bulk_g2s(sig + q * SW, gm + g, SW * 4, &full[ds]);
-        bulk_g2s(sex + q * SW, ge + g, SW * 2, &full[ds]);
+        bulk_g2s_h(sig + q * SW, gm + g, SW * 4, &full[ds], p.l2hint, pol);
+        bulk_g2s_h(sex + q * SW, ge + g, SW * 2, &full[ds], p.l2hint, pol);
       }
       rr.head += (unsigned)n;
       rr.rpos += n;
@@ -1224,7 +1249,7 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
       norm_store_f32<CPT>(p, s, Ex, bmt + g, bet + g, it.sl * SW + col, it.node);
     } else {
       Lane<M, E, CPT> out;
-      norm_lane<TrF32, CPT>(p, s, Ex, out, it.sl * SW + col, it.node);
+      norm_lane<TrF32, CPT, false>(p, s, Ex, out, it.sl * SW + col, it.node);
       out.store(bmt + g, bet + g);
     }
   }

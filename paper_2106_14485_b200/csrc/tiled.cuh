@@ -149,7 +149,10 @@ __device__ __forceinline__ void issue_rows(const M* gm, const E* ge, int Lp, siz
 
 // ------------------------------------------------------------------------------------------------
 
-template <class T_, int CPT>
+// FAC: apply the node factors of the launch's output layer (NEXT-2 commodity node factor D, NEXT-3 node-capacity
+// dual u) here; the pipelined kernels instantiate FAC = false (their launches are followed by k_apply_factors when a
+// problem has such factors): the per-element checks cost their epilogues up to 17 % (measured on [4])
+template <class T_, int CPT, bool FAC = true>
 __device__ __forceinline__ void norm_lane(const DevPtrs& p, const typename T_::M* s, const int* E,
                                           Lane<typename T_::M, typename T_::E, CPT>& out, int l0, int node) {
   typedef typename T_::M M;
@@ -169,23 +172,25 @@ __device__ __forceinline__ void norm_lane(const DevPtrs& p, const typename T_::M
     } else {
       xf_norm<M>(s[c], E[c], m, e);
     }
-    if (p.dnm && m != M(0)) {  // commodity node factor of this layer (NEXT-2)
-      const size_t k = (size_t)node * p.Lp + l0 + c;
-      m *= ((const M*)p.dnm)[k];
-      e += (int)((const typename T_::E*)p.dne)[k];
-      if (m >= M(2)) {
-        m *= M(0.5);
-        e += 1;
+    if constexpr (FAC) {
+      if (p.dnm && m != M(0)) {  // commodity node factor of this layer (NEXT-2)
+        const size_t k = (size_t)node * p.Lp + l0 + c;
+        m *= ((const M*)p.dnm)[k];
+        e += (int)((const typename T_::E*)p.dne)[k];
+        if (m >= M(2)) {
+          m *= M(0.5);
+          e += 1;
+        }
       }
-    }
-    if (p.unlm && m != M(0)) {  // node-capacity dual of this layer (NEXT-3)
-      m *= ((const M*)p.unlm)[node];
-      e += p.unle[node];
-      if (m >= M(2)) {
-        m *= M(0.5);
-        e += 1;
+      if (p.unlm && m != M(0)) {  // node-capacity dual of this layer (NEXT-3)
+        m *= ((const M*)p.unlm)[node];
+        e += p.unle[node];
+        if (m >= M(2)) {
+          m *= M(0.5);
+          e += 1;
+        }
+        if (m == M(0)) e = EZERO;
       }
-      if (m == M(0)) e = EZERO;
     }
     if (e > ELIM || (m != M(0) && e < -ELIM)) {
       set_error(p, ERR_RANGE, l0 + c, node);
@@ -195,6 +200,47 @@ __device__ __forceinline__ void norm_lane(const DevPtrs& p, const typename T_::M
     MMF_DASSERT(node >= 0 && node < p.N && l0 + c < p.Lp);
     out.m[c] = m;
     out.e[c] = (typename T_::E)e;
+  }
+}
+
+// the node factors of layer t applied in place to a stored message layer (after the pipelined kernels, whose
+// epilogues skip them): which = 0 alpha_t, 1 beta_t; the pointers in p are the launch's (lay: D, and u if set)
+template <class T_> __global__ void k_apply_factors(DevPtrs p, int t, int which) {
+  typedef typename T_::M M;
+  typedef typename T_::E E;
+  View<T_> v(p);
+  M* pm = which ? v.bm(t) : v.am(t);
+  E* pe = which ? v.be(t) : v.ae(t);
+  const size_t n = (size_t)p.N * p.Lp;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+    M m = pm[k];
+    if (m == M(0)) continue;
+    int e = (int)pe[k];
+    const int node = (int)(k / p.Lp);
+    if (p.dnm) {
+      m *= ((const M*)p.dnm)[k];
+      e += (int)((const E*)p.dne)[k];
+      if (m >= M(2)) {
+        m *= M(0.5);
+        e += 1;
+      }
+    }
+    if (p.unlm) {
+      m *= ((const M*)p.unlm)[node];
+      e += p.unle[node];
+      if (m >= M(2)) {
+        m *= M(0.5);
+        e += 1;
+      }
+    }
+    if (m == M(0)) {
+      e = EZERO;
+    } else if (e > ELIM || e < -ELIM) {
+      set_error(p, ERR_RANGE, (int)(k % p.Lp), node);
+      e = e > 0 ? ELIM : -ELIM;
+    }
+    pm[k] = m;
+    pe[k] = (E)e;
   }
 }
 

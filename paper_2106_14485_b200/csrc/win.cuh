@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(WIN_THREADS, 1) k_bwd_win(DevPtrs p, WinCfg c,
         continue;
       }
       Lane<float, int16_t, CPT> out;
-      norm_lane<TrF32, CPT>(p, sm, Ex, out, w.col0 + lane * CPT, i);
+      norm_lane<TrF32, CPT, false>(p, sm, Ex, out, w.col0 + lane * CPT, i);
       const size_t gidx = (size_t)i * p.Lp + w.col0 + lane * CPT;
       out.store(bmt + gidx, bet + gidx);
     }
