@@ -168,14 +168,16 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *              pipelines per CTA (0 = default; the compiled combinations are listed in pipefwd.cuh)
  *   "wintma"   window backward row blocks by 2-D tensor TMA (1) or cp.async (0)
  *   "order"    node order: kernels 2..5: 0 input, 1 reverse Cuthill-McKee, 2 BFS tiles (default); kernels 6:
- *              1 RCM, 3 the window kernel's cost model (used with bwd=2), other values: most neighbour overlap
- *              between consecutive nodes (default)
+ *              1 RCM, 3 the window kernel's cost model, 4 most neighbour overlap between consecutive nodes even where
+ *              the pipelined kernels do not apply; default (other values): most neighbour overlap for fp32 with
+ *              L >= 256 (the pipelined kernels), the window cost model otherwise (fp64, L < 256) and with bwd=2
  *   "cpt"      commodities per thread 0 (auto), 1, 2, 4, 8
  *   "tile", "halo", "cpc"  tile sizes of the kernels = 2 family
  *   "wrap"     three-pipeline backward: -1 auto, 0 items never wrap around the ring, 1 items may wrap
  *   "stripw"   (experiments) strip width of the neighbour-overlap node order (0 = chosen by its score)
  *   "dry", "copy"  profiling / diagnostic modes of the pipelined kernels (dry 1: producers only, 2: no flows,
- *              3: no dual update; results invalid; never in production) */
+ *              3: no dual update; results invalid; never in production)
+ *   "l2hint"   pipelined kernels: L2 evict_last policy on the gathered message rows (measured no gain; default 0) */
 mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);
 
 /* W = 1, UT = 1 on supp(muT), one backward pass (Alg. 2 "Initialize").  Async. */

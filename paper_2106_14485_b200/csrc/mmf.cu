@@ -2452,6 +2452,7 @@ mmf_status mmf_set_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_begin, in
   ctx->l_begin = l_begin;
   ctx->L = l_count;
   ctx->point = false;
+  ctx->prepared = false;  // (the node order is chosen from L and the precision)
   if (ctx->node_cost.size() != (size_t)l_count * N) ctx->node_cost.clear();
   ctx->mu0.assign(mu0, mu0 + (size_t)l_count * N);
   ctx->muT.assign(muT, muT + (size_t)l_count * N);
@@ -2474,6 +2475,7 @@ mmf_status mmf_set_point_marginals(mmf_ctx* ctx, int32_t L_global, int32_t l_beg
   ctx->l_begin = l_begin;
   ctx->L = l_count;
   ctx->point = true;
+  ctx->prepared = false;  // (the node order is chosen from L and the precision)
   if (ctx->node_cost.size() != (size_t)l_count * ctx->N) ctx->node_cost.clear();
   ctx->src.assign(src, src + l_count);
   ctx->dst.assign(dst, dst + l_count);
