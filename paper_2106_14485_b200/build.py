@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False, debug: bool = False) -> st
     lib = LIB_DEBUG if debug else LIB
     if not force and not (needs_build_debug() if debug else needs_build()):
         return lib
-    extra = ["-DMMF_DEBUG"] if debug else []
+    extra = (["-DMMF_DEBUG"] if debug else []) + os.environ.get("MMF_NVCC_EXTRA", "").split()  # (experiment builds)
     cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", lib + ".tmp", *SOURCES, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

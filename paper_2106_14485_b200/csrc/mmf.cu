@@ -12,10 +12,13 @@
 #include "reuse.cuh"
 
 #include <dlfcn.h>
+#include <future>
+#include <thread>
 #include <nvtx3/nvToolsExt.h>  // (header-only NVTX3: ranges go to a profiler when one is attached, else no-ops)
 #include <cstdlib>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -192,6 +195,8 @@ struct mmf_ctx {
   size_t sm() const { return prec == MMF_FP32 ? sizeof(float) : sizeof(double); }
   int* d_int_of_arc = nullptr;  // (readouts: user arc -> internal arc, uploaded on first use)
   double* d_export = nullptr;    // (readouts: [T][A] fp64 staging, allocated on first use)
+  void* pinned = nullptr;        // (readouts: pinned bounce buffer of d2h_staged, allocated on first use)
+  cudaEvent_t ev_d2h[2] = {nullptr, nullptr};
   size_t se() const { return prec == MMF_FP32 ? sizeof(int16_t) : sizeof(int32_t); }
 };
 
@@ -201,6 +206,18 @@ mmf_status fail(mmf_ctx* c, mmf_status s, const std::string& msg) {
   if (c) c->err = msg;
   return s;
 }
+
+// host-side phase timer (MMF_VERBOSE: printed to stderr)
+struct HostTimer {
+  const char* name;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  explicit HostTimer(const char* n) : name(n) {}
+  ~HostTimer() {
+    if (getenv("MMF_VERBOSE"))
+      fprintf(stderr, "[mmf] host %s %.1f ms\n", name,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
+};
 
 // NVTX range of a host-side scope (sweep, pass, step, readout); under CUDA-graph capture the ranges mark the capture
 struct Nvtx {
@@ -388,6 +405,7 @@ void make_tiles(int N, const std::vector<int>& tail, const std::vector<int>& hea
 void build_window_tables(mmf_ctx* c);
 
 void derive_shapes(mmf_ctx* c) {
+  HostTimer ht("derive_shapes");
   int cpt_auto = c->prec == MMF_FP32 ? 2 : 1;
   if (c->opt_kernels == 4) {  // register-gather path: 4 fp32 commodities per lane keep 6 rows in registers
     if (c->prec == MMF_FP32)
@@ -625,29 +643,46 @@ double reuse_frac(const mmf_ctx* c, const std::vector<int>& nid, bool in_lists) 
   return A ? (double)hit / (double)A : 0.0;
 }
 void choose_reuse_order(mmf_ctx* c) {
+  HostTimer ht("choose_reuse_order");
   const int N = c->N;
   const size_t A = c->tail.size();
-  std::vector<std::vector<int>> cands;
-  cands.emplace_back(N);
-  std::iota(cands[0].begin(), cands[0].end(), 0);
-  cands.push_back(rcm_newid(N, c->tail, c->head));
+  std::vector<int> id(N);
+  std::iota(id.begin(), id.end(), 0);
+  std::vector<int> rcm = rcm_newid(N, c->tail, c->head);
+  // candidates: input, RCM, and strip versions of both; built and scored on host threads (one per candidate)
+  struct Cand {
+    int base, w;
+  };
+  std::vector<Cand> spec = {{0, 0}, {1, 0}};
+  const std::vector<int>* bases[2] = {&id, &rcm};
   for (int base = 0; base < 2; ++base) {
     std::vector<int> d;
+    const std::vector<int>& b = *bases[base];
     for (size_t a = 0; a < A; ++a)
-      if (c->tail[a] != c->head[a]) d.push_back(std::abs(cands[base][c->tail[a]] - cands[base][c->head[a]]));
+      if (c->tail[a] != c->head[a]) d.push_back(std::abs(b[c->tail[a]] - b[c->head[a]]));
     if (d.empty()) continue;
     std::nth_element(d.begin(), d.begin() + (size_t)(0.90 * (d.size() - 1)), d.end());
     const int b90 = d[(size_t)(0.90 * (d.size() - 1))];
     for (int w : {2, 4, 8, 16, 32})
-      if (b90 > 2 * w && (!c->opt_stripw || c->opt_stripw == w)) cands.push_back(strip_newid(cands[base], b90, w));
+      if (b90 > 2 * w && (!c->opt_stripw || c->opt_stripw == w)) spec.push_back({base, w * 1000000 + b90});
   }
+  const size_t first = (c->opt_stripw && spec.size() > 2) ? 2 : 0;
+  std::vector<std::vector<int>> cands(spec.size());
+  std::vector<double> score(spec.size(), -1.0);
+  std::vector<std::future<void>> jobs;
+  for (size_t ci = first; ci < spec.size(); ++ci)
+    jobs.push_back(std::async(std::launch::async, [&, ci]() {
+      const Cand& k = spec[ci];
+      cands[ci] = k.w == 0 ? *bases[k.base] : strip_newid(*bases[k.base], k.w % 1000000, k.w / 1000000);
+      score[ci] = reuse_frac(c, cands[ci], true) + reuse_frac(c, cands[ci], false);
+    }));
+  for (auto& j : jobs) j.get();
   double best = -1.0;
-  size_t bi = 0;
-  for (size_t ci = (c->opt_stripw && cands.size() > 2) ? 2 : 0; ci < cands.size(); ++ci) {
-    const double f = reuse_frac(c, cands[ci], true) + reuse_frac(c, cands[ci], false);
-    if (getenv("MMF_VERBOSE")) fprintf(stderr, "[mmf] reuse order cand %zu: %.3f\n", ci, 0.5 * f);
-    if (f > best + 1e-9) {
-      best = f;
+  size_t bi = first;
+  for (size_t ci = first; ci < spec.size(); ++ci) {  // (same choice as a serial scan: first of the best)
+    if (getenv("MMF_VERBOSE")) fprintf(stderr, "[mmf] reuse order cand %zu: %.3f\n", ci, 0.5 * score[ci]);
+    if (score[ci] > best + 1e-9) {
+      best = score[ci];
       bi = ci;
     }
   }
@@ -744,6 +779,7 @@ void choose_window_order(mmf_ctx* c) {
 
 // window tables of the out-direction (backward gathers): per out-CSR record the window slot or far index
 void build_window_tables(mmf_ctx* c) {
+  HostTimer ht("build_window_tables");
   const int N = c->N, Wb = c->win_Wb, RBa = 2 * Wb + 1 + WIN_PD;
   const int nblk = (N + WIN_BR - 1) / WIN_BR;
   const int64_t A = c->A;
@@ -888,6 +924,7 @@ void augment_times(mmf_ctx* c) {
 
 void prepare(mmf_ctx* c) {
   if (c->prepared) return;
+  HostTimer ht("prepare");
   augment_times(c);
   const int N = c->N;
   const int64_t A = c->A;
@@ -938,14 +975,24 @@ void prepare(mmf_ctx* c) {
   c->tileB = 0;
   for (int k = 0; k < c->ntiles; ++k) c->tileB = std::max(c->tileB, c->h_tile_ptr[k + 1] - c->h_tile_ptr[k]);
 
+  HostTimer ht1("prepare: csr");
   std::vector<int> it(A), ih(A);
   for (int64_t a = 0; a < A; ++a) {
     it[a] = c->newid[c->tail[a]];
     ih[a] = c->newid[c->head[a]];
   }
+  // arcs sorted by (head, tail): two stable counting sorts (by tail, then by head); the pairs are unique, so this is
+  // the order of a lexicographic comparison sort
+  auto counting_sort = [N](const std::vector<int64_t>& in, const std::vector<int>& key) {
+    std::vector<int64_t> cnt(N + 1, 0), out(in.size());
+    for (int64_t x : in) cnt[key[x] + 1]++;
+    for (int v = 0; v < N; ++v) cnt[v + 1] += cnt[v];
+    for (int64_t x : in) out[cnt[key[x]]++] = x;
+    return out;
+  };
   std::vector<int64_t> ord(A);
   std::iota(ord.begin(), ord.end(), 0);
-  std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) { return ih[x] != ih[y] ? ih[x] < ih[y] : it[x] < it[y]; });
+  ord = counting_sort(counting_sort(ord, it), ih);
   c->int_of_arc.assign(A, 0);
   c->h_tail.assign(A, 0);
   c->h_head.assign(A, 0);
@@ -963,10 +1010,8 @@ void prepare(mmf_ctx* c) {
   c->maxdeg_in = 0;
   for (int v = 0; v < N; ++v) c->maxdeg_in = std::max(c->maxdeg_in, c->h_inptr[v + 1] - c->h_inptr[v]);
   std::vector<int64_t> ordo(A);
-  std::iota(ordo.begin(), ordo.end(), 0);
-  std::sort(ordo.begin(), ordo.end(), [&](int64_t x, int64_t y) {
-    return c->h_tail[x] != c->h_tail[y] ? c->h_tail[x] < c->h_tail[y] : c->h_head[x] < c->h_head[y];
-  });
+  std::iota(ordo.begin(), ordo.end(), 0);  // (already sorted by head: one stable pass by tail gives (tail, head))
+  ordo = counting_sort(ordo, c->h_tail);
   for (int64_t k = 0; k < A; ++k) {
     c->h_outarc[k] = (int)ordo[k];
     c->h_outhead[k] = c->h_head[ordo[k]];
@@ -981,7 +1026,20 @@ void prepare(mmf_ctx* c) {
   }
   c->ell_din = din;
 
-  // halos
+  // halos (node-tile kernels only, kernels = 2; the other families get empty tables of the right sizes)
+  if (c->opt_kernels != 2) {
+    const size_t nt = (size_t)c->ntiles;
+    c->h_hin_ptr.assign(nt + 1, 0);
+    c->h_hout_ptr.assign(nt + 1, 0);
+    c->h_hin_node.clear();
+    c->h_hout_node.clear();
+    c->h_in_hidx.assign(A, 0);
+    c->h_out_hidx.assign(A, 0);
+    c->max_hin = c->max_hout = c->max_ia = c->max_oa = 0;
+    c->prepared = true;
+    return;
+  }
+  HostTimer ht2("prepare: halos");
   std::vector<int> tile_of(N);
   for (int k = 0; k < c->ntiles; ++k)
     for (int v = c->h_tile_ptr[k]; v < c->h_tile_ptr[k + 1]; ++v) tile_of[v] = k;
@@ -1919,6 +1977,7 @@ mmf_status collect_profile(mmf_ctx* ctx) {
 
 // build internal structures and upload (called by mmf_init)
 mmf_status finalize(mmf_ctx* ctx) {
+  HostTimer ht("finalize");
   mmf_ctx* c = ctx;
   const int N = c->N;
   const int64_t A = c->A;
@@ -2149,6 +2208,56 @@ __global__ void k_export_duals(const M* __restrict__ wm, const int* __restrict__
     out[k] = m == 0.0 ? 0.0 : ldexp(m, we[i]);  // (values below 2^-1074 read 0)
   }
 }
+// device -> pageable host copy of a readout through a pinned bounce buffer (two halves: the DMA of one chunk
+// overlaps the host threads' copy of the other into the caller's buffer); a plain pageable cudaMemcpy runs at a few
+// GB/s on the [T][A] fp64 readouts (305 MB on [4])
+static cudaError_t d2h_staged(mmf_ctx* ctx, void* out, const void* dev, size_t bytes) {
+  constexpr size_t CH = 16u << 20;  // bytes per half
+  if (bytes < 2 * CH) {
+    cudaError_t e = cudaMemcpyAsync(out, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+    return e == cudaSuccess ? cudaStreamSynchronize(ctx->stream) : e;
+  }
+  if (!ctx->pinned) {
+    cudaError_t e = cudaMallocHost(&ctx->pinned, 2 * CH);
+    if (e != cudaSuccess) {
+      ctx->pinned = nullptr;
+      cudaGetLastError();
+      e = cudaMemcpyAsync(out, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream);
+      return e == cudaSuccess ? cudaStreamSynchronize(ctx->stream) : e;
+    }
+    if (!ctx->ev_d2h[0]) {
+      cudaEventCreateWithFlags(&ctx->ev_d2h[0], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&ctx->ev_d2h[1], cudaEventDisableTiming);
+    }
+  }
+  char* pin = (char*)ctx->pinned;
+  const char* src = (const char*)dev;
+  char* dst = (char*)out;
+  const size_t nch = (bytes + CH - 1) / CH;
+  auto issue = [&](size_t k) {
+    const size_t off = k * CH, len = std::min(CH, bytes - off);
+    cudaError_t e = cudaMemcpyAsync(pin + (k & 1) * CH, src + off, len, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ctx->ev_d2h[k & 1], ctx->stream);
+    return e;
+  };
+  cudaError_t e = issue(0);
+  for (size_t k = 0; k < nch && e == cudaSuccess; ++k) {
+    e = cudaEventSynchronize(ctx->ev_d2h[k & 1]);
+    if (e != cudaSuccess) break;
+    if (k + 1 < nch) e = issue(k + 1);  // (the other half is free: its copy-out finished last iteration)
+    const size_t off = k * CH, len = std::min(CH, bytes - off);
+    const int nt = 4;
+    std::vector<std::thread> th;
+    for (int i = 0; i < nt; ++i)
+      th.emplace_back([&, i]() {
+        const size_t a = len * i / nt, b = len * (i + 1) / nt;
+        memcpy(dst + off + a, pin + (k & 1) * CH + a, b - a);
+      });
+    for (auto& x : th) x.join();
+  }
+  return e;
+}
+
 // what: 0 edge flows (one readout pass first), 1 capacity duals
 static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
   if (!ctx || !out) return MMF_EINVAL;
@@ -2176,8 +2285,7 @@ static mmf_status read_export(mmf_ctx* ctx, double* out, int what) {
     else k_export_duals<double><<<grid, 256, 0, ctx->stream>>>((const double*)ctx->dp.Wm, ctx->dp.We, ctx->d_int_of_arc, d, A, Au, n);
   }
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e == cudaSuccess) e = d2h_staged(ctx, out, d, (size_t)n * sizeof(double));
   if (e != cudaSuccess) return fail(ctx, MMF_ECUDA, std::string("readout: ") + cudaGetErrorString(e));
   return MMF_OK;
 }
@@ -3038,6 +3146,9 @@ mmf_status mmf_destroy(mmf_ctx* ctx) {
   if (ctx->ws_owned) cudaFree(ctx->ws);
   if (ctx->d_int_of_arc) cudaFree(ctx->d_int_of_arc);
   if (ctx->d_export) cudaFree(ctx->d_export);
+  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (auto e : ctx->ev_d2h)
+    if (e) cudaEventDestroy(e);
   if (ctx->priv) cudaStreamDestroy(ctx->priv);
   delete ctx;
   return MMF_OK;

@@ -24,8 +24,14 @@ namespace mmf {
 constexpr int PIPE_NWC = 8;                                  // consumer warps per group (one group = one item)
 constexpr int PIPE_NG = 2;                                   // consumer groups (alternate items)
 constexpr int PIPE_THREADS = (PIPE_NWC * PIPE_NG + 1) * 32;  // + one producer warp
-constexpr int PIPE_P = 12;                                   // record prefetch distance (items)
-constexpr int PIPE_RP = 16;                                  // record ring slots (> PIPE_P)
+#ifndef MMF_PIPE_P
+#define MMF_PIPE_P 12
+#endif
+#ifndef MMF_PIPE_RP
+#define MMF_PIPE_RP 16
+#endif
+constexpr int PIPE_P = MMF_PIPE_P;                           // record prefetch distance (items)
+constexpr int PIPE_RP = MMF_PIPE_RP;                         // record ring slots (> PIPE_P)
 constexpr int PIPE_NR = 8;                                   // rows a consumer holds in registers (fast path)
 constexpr int PIPE_SD = 16;                                  // item descriptors (power of two)
 

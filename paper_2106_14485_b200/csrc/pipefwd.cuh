@@ -36,7 +36,10 @@ constexpr int FWD_NP = 2;  // (pipelines per CTA of the backward's structure)
 constexpr int FWD_PW = PIPE_NWC + 1;  // warps per pipeline of the backward (8 consumers + producer)
 constexpr int FWD_SD = 8;             // item descriptors per pipeline of the backward (power of two)
 constexpr int FWD_SDF = 4;            // item descriptors per pipeline of the forward (power of two)
-constexpr int FWD_P = 8;              // record prefetch distance of the forward (items; PIPE_RP > FWD_P + FWD_SDF)
+#ifndef MMF_FWD_P
+#define MMF_FWD_P 8
+#endif
+constexpr int FWD_P = MMF_FWD_P;      // record prefetch distance of the forward (items; PIPE_RP > FWD_P + FWD_SDF)
 static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the consumers until released");
 #ifndef MMF_NORM_PACKED
 #define MMF_NORM_PACKED 0  // packed normalise-and-store of the pipelined kernels' output rows (measured: no gain)
