@@ -43,7 +43,9 @@ struct DevPtrs {
   const int* pdst;
   const double* pmass;
   void* part;           // [G][A] partial flows (M)
-  void* Fsum;           // [A] reduced flows (M)
+  void* Fsum;           // [Ecap] the multi-GPU exchange buffer: flows of the capacitated arcs only (M)
+  const int* fpos;      // [A] internal arc -> its position in Fsum (-1: uncapacitated at every step)
+  int Ecap;             // capacitated arcs (Fsum length; the all-reduce moves Ecap values, not A)
   void* Fout;           // [T][A] readout flows (M)
   unsigned* err;        // sticky error word
   unsigned long long* errloc;  // first error (commodity << 32 | node)
@@ -346,6 +348,8 @@ template <class T_> __global__ void k_reduce(DevPtrs p, int t, typename T_::M* o
   if (!(s == s) || isinf(s)) set_error(p, ERR_NAN, -1, a);
   if (mode == 2)
     dual_update<T_>(p, t, a, (double)s);
+  else if (mode == 1)
+    out[p.fpos[a]] = s;  // (finite capacity at t: fpos >= 0)
   else
     out[a] = s;
 }
@@ -432,10 +436,17 @@ template <class T_> __global__ void __launch_bounds__(256) k_node_cap(DevPtrs p,
   }
 }
 
-template <class T_> __global__ void k_dual(DevPtrs p, int t) {
+// compact = 1: F from the exchange buffer Fsum[fpos[a]]; 0: from an arc-indexed array (Fsum = a step of Fout)
+template <class T_> __global__ void k_dual(DevPtrs p, int t, int compact) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= p.A) return;
-  dual_update<T_>(p, t, a, (double)((const typename T_::M*)p.Fsum)[a]);
+  typedef typename T_::M M;
+  if (compact) {
+    const int f = p.fpos[a];
+    if (f >= 0) dual_update<T_>(p, t, a, (double)((const M*)p.Fsum)[f]);  // (uncapacitated: nothing to update)
+  } else {
+    dual_update<T_>(p, t, a, (double)((const M*)p.Fsum)[a]);
+  }
 }
 
 // a3(iv) SpMM^T: alpha_{t+1}[j,l] = sum_{a -> j} alpha_t[i_a,l] K_t[a] W_t[a]   (eq:psi_hat P:1031-1036)

@@ -144,6 +144,9 @@ struct mmf_ctx {
   std::vector<int> int_of_arc;  // user arc -> internal arc
   bool prepared = false;        // host graph structures below are valid
   std::vector<int> h_tail, h_head, h_inptr, h_outptr, h_outarc, h_outhead;
+  std::vector<int> h_fpos;  // internal arc -> position in the exchange buffer (capacitated at some step), else -1
+  int64_t Ecap = 0;
+  bool fpos_ok = false;
   int ntiles = 0, tileB = 0, max_hin = 0, max_hout = 0, max_ia = 0, max_oa = 0;
   std::vector<int> h_tile_ptr, h_hin_ptr, h_hin_node, h_hout_ptr, h_hout_node, h_in_hidx, h_out_hidx;
   TileMeta tm{};
@@ -925,6 +928,7 @@ void augment_times(mmf_ctx* c) {
 void prepare(mmf_ctx* c) {
   if (c->prepared) return;
   HostTimer ht("prepare");
+  c->fpos_ok = false;  // (int_of_arc follows the node order)
   augment_times(c);
   const int N = c->N;
   const int64_t A = c->A;
@@ -1080,7 +1084,25 @@ void prepare(mmf_ctx* c) {
 }
 
 // walk the workspace layout; assign pointers when base != nullptr
+// the multi-GPU exchange buffer holds the flows of the arcs with a finite capacity at some step only (SURVEY 8(e)
+// mitigation 2: the all-reduce of a step moves |E| values, not |A|; [4]: 150,444 of 190,444)
+static void build_fpos(mmf_ctx* c) {
+  const int64_t A = c->A;
+  const int TC = c->cap_tv ? c->T : 1;
+  std::vector<char> capd(A, 0);
+  for (int t = 0; t < TC; ++t)
+    for (int64_t a = 0; a < A; ++a)
+      if (std::isfinite(c->cap[(size_t)t * A + a])) capd[c->int_of_arc[a]] = 1;
+  c->h_fpos.assign(A, -1);
+  int64_t e = 0;
+  for (int64_t k = 0; k < A; ++k)
+    if (capd[k]) c->h_fpos[k] = (int)e++;
+  c->Ecap = e;
+  c->fpos_ok = true;
+}
+
 size_t layout(mmf_ctx* c, char* base) {
+  if (!c->fpos_ok) build_fpos(c);
   Layout L;
   const size_t A = (size_t)c->A, N = (size_t)c->N, T = (size_t)c->T, Lp = (size_t)c->Lp;
   const size_t TK = c->cost_tv ? T : 1, TC = c->cap_tv ? T : 1;
@@ -1129,7 +1151,9 @@ size_t layout(mmf_ctx* c, char* base) {
     p.pmass = (const double*)at(L.take((size_t)c->L * 8));
   }
   p.part = at(L.take((size_t)c->G * A * sm));
-  p.Fsum = at(L.take(A * sm));
+  p.Fsum = at(L.take(std::max<int64_t>(c->Ecap, 1) * sm));
+  p.fpos = (const int*)at(L.take(A * 4));
+  p.Ecap = (int)c->Ecap;
   p.Fout = at(L.take(T * A * sm));
   p.err = (unsigned*)at(L.take(8));
   p.errloc = (unsigned long long*)at(L.take(8));
@@ -1333,11 +1357,11 @@ template <class T_> struct Eng {
         LaunchScope ls(c, K_REDUCE, s);
         k_reduce<T_><<<ga, 256, 0, s>>>(p, t, (M*)p.Fsum, 1);
       }
-      int r = nccl_api().AllReduce(p.Fsum, p.Fsum, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
+      int r = nccl_api().AllReduce(p.Fsum, p.Fsum, (size_t)c->Ecap, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
                                    NCCL_SUM, c->comm, s);
       if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
       LaunchScope ls(c, K_REDUCE, s);
-      k_dual<T_><<<ga, 256, 0, s>>>(p, t);
+      k_dual<T_><<<ga, 256, 0, s>>>(p, t, 1);
     } else {
       LaunchScope ls(c, K_REDUCE, s);
       k_reduce<T_><<<ga, 256, 0, s>>>(p, t, nullptr, 2);
@@ -1581,11 +1605,11 @@ template <class T_> struct Eng {
   // the multi-GPU exchange of one forward step: all-reduce the rank-partial F_t, then W_t update
   static mmf_status exchange(mmf_ctx* c, cudaStream_t s, int t) {
     const DevPtrs& p = c->dp;
-    int r = nccl_api().AllReduce(p.Fsum, p.Fsum, (size_t)c->A, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
-                                 NCCL_SUM, c->comm, s);
+    int r = nccl_api().AllReduce(p.Fsum, p.Fsum, (size_t)c->Ecap, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
+                                 NCCL_SUM, c->comm, s);  // (capacitated arcs only, SURVEY 8(e) mitigation 2)
     if (r != 0) return fail(c, MMF_ENCCL, "ncclAllReduce failed");
     LaunchScope ls(c, K_REDUCE, s);
-    k_dual<T_><<<(unsigned)((c->A + 255) / 256), 256, 0, s>>>(p, t);
+    k_dual<T_><<<(unsigned)((c->A + 255) / 256), 256, 0, s>>>(p, t, 1);
     return MMF_OK;
   }
 
@@ -1602,11 +1626,11 @@ template <class T_> struct Eng {
       if (t < c0->T) {
         {
           LaunchScope ls(c0, K_REDUCE, s);
-          k_vsum<M><<<ga, 256, 0, s>>>(vs, G, c0->A);
+          k_vsum<M><<<ga, 256, 0, s>>>(vs, G, c0->Ecap);
         }
         for (int g = 0; g < G; ++g) {
           LaunchScope ls(cs[g], K_REDUCE, s);
-          k_dual<T_><<<ga, 256, 0, s>>>(cs[g]->dp, t);
+          k_dual<T_><<<ga, 256, 0, s>>>(cs[g]->dp, t, 1);
         }
       }
     }
@@ -1700,7 +1724,7 @@ template <class T_> struct Eng {
         DevPtrs d = c->dp;
         d.Fsum = Ft;
         LaunchScope ls(c, K_UPDATE, s);
-        k_dual<T_><<<ga, 256, 0, s>>>(d, t);
+        k_dual<T_><<<ga, 256, 0, s>>>(d, t, 0);
       }
       if (c->opt_kernels >= 2) {
         tiled_bwd(c, s, t);
@@ -2078,6 +2102,8 @@ mmf_status finalize(mmf_ctx* ctx) {
   CU(cudaMemcpyAsync((void*)p.Km, hKm.data(), hKm.size(), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync((void*)p.Ke, hKe.data(), hKe.size() * 4, cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync((void*)p.dcap, hdc.data(), hdc.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync((void*)p.fpos, c->h_fpos.data(), (size_t)A * 4, cudaMemcpyHostToDevice, s));
+  CU(cudaMemsetAsync(p.Fsum, 0, (size_t)std::max<int64_t>(c->Ecap, 1) * sm, s));
 
   // marginals
   std::vector<char> h0, h0e, hT, hTe;
@@ -2524,6 +2550,7 @@ mmf_status mmf_set_capacity(mmf_ctx* ctx, const double* cap, int time_varying) {
     if (!(cap[k] >= 0)) return fail(ctx, MMF_EINVAL, "capacity < 0 or NaN");
   ctx->cap.assign(cap, cap + n);
   ctx->cap_tv = time_varying != 0;
+  ctx->fpos_ok = false;
   ctx->have_cap = true;
   return MMF_OK;
 }

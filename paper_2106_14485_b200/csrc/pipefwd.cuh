@@ -35,9 +35,12 @@ namespace mmf {
 constexpr int FWD_NP = 2;  // (pipelines per CTA of the backward's structure)
 constexpr int FWD_PW = PIPE_NWC + 1;  // warps per pipeline of the backward (8 consumers + producer)
 constexpr int FWD_SD = 8;             // item descriptors per pipeline of the backward (power of two)
-constexpr int FWD_SDF = 4;            // item descriptors per pipeline of the forward (power of two)
+#ifndef MMF_FWD_SDF
+#define MMF_FWD_SDF 8  // (4: [3] forward 8 % slower, [4] 2 %)
+#endif
+constexpr int FWD_SDF = MMF_FWD_SDF;  // item descriptors per pipeline of the forward (power of two)
 #ifndef MMF_FWD_P
-#define MMF_FWD_P 8
+#define MMF_FWD_P 6
 #endif
 constexpr int FWD_P = MMF_FWD_P;      // record prefetch distance of the forward (items; PIPE_RP > FWD_P + FWD_SDF)
 static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the consumers until released");
@@ -949,14 +952,9 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
         h.aux[lane] = r.aux;
         h.rtail[lane] = r.node;
       }
+      // capmask over rows (row order = lane order of the nonzero-factor arcs)
+      const unsigned cm = __reduce_or_sync(0xffffffffu, ok && ((cbal >> lane) & 1u) ? 1u << rs : 0u);
       if (lane == 0) {
-        // capmask over rows (row order = lane order of the nonzero-factor arcs)
-        unsigned cm = 0u, ob = obal;
-        for (int q = 0; ob; ++q) {
-          const int l = __ffs(ob) - 1;
-          if ((cbal >> l) & 1u) cm |= 1u << q;
-          ob &= ob - 1u;
-        }
         h.capmask = cm;
         h.nr = nr;
         h.na = na;

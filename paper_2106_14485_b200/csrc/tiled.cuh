@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(TILE_THREADS, 2) k_fwd_tile(DevPtrs p, TileMet
     if (FMODE == 0)
       dual_update<T_>(p, t, arc, (double)s);
     else if (FMODE == 1)
-      ((M*)p.Fsum)[arc] = s;
+      ((M*)p.Fsum)[p.fpos[arc]] = s;  // (finite capacity at t: fpos >= 0)
     else
       ((M*)p.Fout)[(size_t)t * p.A + arc] = s;
   }
