@@ -50,42 +50,6 @@ template <class M> __host__ __device__ inline size_t head_smem(int max_ia, int n
   return ((size_t)max_ia * nch * sizeof(M) + 15) / 16 * 16 + (size_t)max_ia * sizeof(KwEnt<M>) + 16;
 }
 
-// one lane's CPT consecutive commodities of a row; fp32 exponents kept packed two per word
-template <class T_, int CPT> struct Row {
-  typedef typename T_::M M;
-  typedef typename T_::E E;
-  static constexpr bool PACKED = sizeof(M) == 4 && sizeof(E) == 2 && CPT % 2 == 0;
-  static constexpr int NW = PACKED ? CPT / 2 : CPT;
-  M m[CPT];
-  int w[NW];  // PACKED: int16x2 words; else one exponent per commodity
-  __device__ __forceinline__ void load(const M* pm, const E* pe) {
-    typedef typename VecM<M, CPT>::T VM;
-    VM vm = *reinterpret_cast<const VM*>(pm);
-    const M* sm = reinterpret_cast<const M*>(&vm);
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) m[c] = sm[c];
-    if constexpr (PACKED) {
-      typedef typename VecE<int16_t, CPT>::T VE;
-      VE ve = *reinterpret_cast<const VE*>(pe);
-      const int* sw = reinterpret_cast<const int*>(&ve);
-#pragma unroll
-      for (int k = 0; k < NW; ++k) w[k] = sw[k];
-    } else {
-      typedef typename VecE<E, CPT>::T VE;
-      VE ve = *reinterpret_cast<const VE*>(pe);
-      const E* se = reinterpret_cast<const E*>(&ve);
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) w[c] = (int)se[c];
-    }
-  }
-  __device__ __forceinline__ int e(int c) const {
-    if constexpr (PACKED)
-      return (c & 1) ? (w[c >> 1] >> 16) : (int)(short)(w[c >> 1] & 0xffff);
-    else
-      return w[c];
-  }
-};
-
 // 16-bit-exponent-safe max-plus state (fp32 packed path) or plain ints
 template <class T_, int CPT> struct RowMax {
   typedef Row<T_, CPT> R;

@@ -131,104 +131,6 @@ struct ItemIt {
   }
 };
 
-// ------------------------------------------------------------------------------------------------
-// Extended-range arithmetic on a lane's CPT commodities (fp32 significand, int16 exponent).
-// Exponents are handled two per 32-bit word (CPT even): the max of (row exponent + arc exponent) by one
-// VIADDMNMX.S16x2 per pair (exact: |e| <= 16384, |ke| <= 16000); the scale 2^d, d = max(max(e + ke,
-// E - 32512) - E, -126) (no 16-bit wrap) by two more; then K W 2^d by an integer add into the float's
-// exponent field — mod 2^32 the low / high half of d << 23 equals d2 << 23 / (d2 >> 16) << 23 (SHF + LEA).
-
-#ifndef MMF_HI_SHF
-#define MMF_HI_SHF 1
-#endif
-#if MMF_HI_SHF
-#define MMF_HI23(d2) (((d2) >> 16) << 23)
-#else
-#define MMF_HI23(d2) (((d2)&0xffff0000u) << 7)
-#endif
-template <int CPT> struct XPre {  // per-item constants of a lane: -E and the low clamp E - 32512, packed
-  unsigned nE2[CPT / 2 > 0 ? CPT / 2 : 1], Lo2[CPT / 2 > 0 ? CPT / 2 : 1], Ep2[CPT / 2 > 0 ? CPT / 2 : 1];
-  int nE[CPT];
-  int E[CPT];
-  __device__ __forceinline__ void set(const unsigned* E2) {
-    if constexpr (CPT % 2 == 0) {
-#pragma unroll
-      for (int w = 0; w < CPT / 2; ++w) {
-        nE2[w] = __vneg2(E2[w]);
-        Lo2[w] = __vsubss2(E2[w], 0x7f007f00u);
-        Ep2[w] = __vaddss2(E2[w], 0x007f007fu);  // E + 127 (float exponent bias), saturated
-        E[2 * w] = (int)(short)(E2[w] & 0xffffu);
-        E[2 * w + 1] = (int)E2[w] >> 16;
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) E[c] = (int)E2[c];
-    }
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) nE[c] = -E[c];
-  }
-};
-
-template <int CPT> __device__ __forceinline__ void xmax_init(unsigned* E2) {
-  if constexpr (CPT % 2 == 0) {
-#pragma unroll
-    for (int w = 0; w < CPT / 2; ++w) E2[w] = 0x80008000u;
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) E2[c] = (unsigned)(EZERO - 4 * ELIM);
-  }
-}
-template <int CPT>
-__device__ __forceinline__ void xmax_add(unsigned* E2, const Row<TrF32, CPT>& x, unsigned k2, int ke) {
-  if constexpr (CPT % 2 == 0) {
-#pragma unroll
-    for (int w = 0; w < CPT / 2; ++w) E2[w] = __viaddmax_s16x2((unsigned)x.w[w], k2, E2[w]);
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) E2[c] = (unsigned)max((int)E2[c], x.e(c) + ke);
-  }
-}
-// t[c] = x.m[c] * K W * 2^(x.e[c] + ke - E[c]) (flushed below 2^-126 of the maximum)
-template <int CPT>
-__device__ __forceinline__ void xterms(const Row<TrF32, CPT>& x, unsigned kb, unsigned k2, int ke,
-                                       const XPre<CPT>& P, float* tq) {
-  if constexpr (CPT % 2 == 0) {
-#pragma unroll
-    for (int w = 0; w < CPT / 2; ++w) {
-      const unsigned u = __viaddmax_s16x2((unsigned)x.w[w], k2, P.Lo2[w]);
-      const unsigned d2 = __viaddmax_s16x2(u, P.nE2[w], 0xff82ff82u);
-      tq[2 * w] = x.m[2 * w] * __uint_as_float(kb + (d2 << 23));
-      tq[2 * w + 1] = x.m[2 * w + 1] * __uint_as_float(kb + MMF_HI23(d2));
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const int d = max(x.e(c) + ke + P.nE[c], -126);
-      tq[c] = x.m[c] * __uint_as_float(kb + ((unsigned)d << 23));
-    }
-  }
-}
-template <int CPT>
-__device__ __forceinline__ void xacc(const Row<TrF32, CPT>& x, unsigned kb, unsigned k2, int ke, const XPre<CPT>& P,
-                                     float* acc) {
-  if constexpr (CPT % 2 == 0) {
-#pragma unroll
-    for (int w = 0; w < CPT / 2; ++w) {
-      const unsigned u = __viaddmax_s16x2((unsigned)x.w[w], k2, P.Lo2[w]);
-      const unsigned d2 = __viaddmax_s16x2(u, P.nE2[w], 0xff82ff82u);
-      acc[2 * w] = fmaf(x.m[2 * w], __uint_as_float(kb + (d2 << 23)), acc[2 * w]);
-      acc[2 * w + 1] = fmaf(x.m[2 * w + 1], __uint_as_float(kb + MMF_HI23(d2)), acc[2 * w + 1]);
-    }
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      const int d = max(x.e(c) + ke + P.nE[c], -126);
-      acc[c] = fmaf(x.m[c], __uint_as_float(kb + ((unsigned)d << 23)), acc[c]);
-    }
-  }
-}
-__device__ __forceinline__ int k2_to_ke(unsigned k2) { return (int)(short)(k2 & 0xffffu); }
-
 // normalise a lane's sums (s[c] * 2^Ex[c], s[c] = 0 or a normal float) into [1, 2) significands and int16
 // exponents two at a time, and store them (norm_lane's semantics: zero -> (0, EZERO); an exponent outside
 // [-ELIM, ELIM] is clamped and raises the sticky ERR_RANGE — checked once per lane)

@@ -59,6 +59,17 @@ static_assert(PIPE_RP > FWD_P + FWD_SDF, "record-ring slots are read by the cons
 #ifndef MMF_FWD_LEAN_UPDATE
 #define MMF_FWD_LEAN_UPDATE 1  // branch-light dual update in the pipelined forward
 #endif
+#ifndef MMF_L2PF
+#define MMF_L2PF 0  // producers prefetch into L2 the gathered row of the node this many positions ahead (0: off)
+#endif
+#ifndef MMF_FWD_BPRE
+#define MMF_FWD_BPRE 0  // (measured: no gain on [4], 4 % slower on [3]) consumers load the own row beta_t[j] of their next item one item ahead (registers)
+#endif
+#ifndef MMF_ALT_ORDER
+#define MMF_ALT_ORDER 0  // odd steps visit the nodes in reverse order (the rows written last by the previous launch
+                         // are still in L2 when the next launch starts)
+#endif
+__device__ __forceinline__ int alt_node(int x, int N, int t) { return (MMF_ALT_ORDER && (t & 1)) ? N - 1 - x : x; }
 #ifndef MMF_FWD_OWNG
 #define MMF_FWD_OWNG 1  // 1: the node's own row beta_t[j] is loaded by the consumers from global memory (L2-
                         // prefetched by the producer) instead of staged in the ring
@@ -451,8 +462,8 @@ __device__ __forceinline__ void beta_lin(const Row<TrF32, CPT>& b, const XPre<CP
 #pragma unroll
     for (int w = 0; w < CPT / 2; ++w) {
       const unsigned es = __vmins2(__vmaxs2(__vaddss2((unsigned)b.w[w], P.Ep2[w]), 0u), 0x00fe00feu);
-      bl[2 * w] = b.m[2 * w] * __uint_as_float(es << 23);
-      bl[2 * w + 1] = b.m[2 * w + 1] * __uint_as_float((es >> 16) << 23);
+      mul2(bl[2 * w], bl[2 * w + 1], b.m[2 * w], b.m[2 * w + 1], __uint_as_float(es << 23),
+           __uint_as_float((es >> 16) << 23));
     }
   } else {
 #pragma unroll
@@ -603,8 +614,8 @@ __device__ __forceinline__ void xterms_w(const int* w, float* m, unsigned kb, un
   for (int k = 0; k < CPT / 2; ++k) {
     const unsigned u = __viaddmax_s16x2((unsigned)w[k], k2, P.Lo2[k]);
     const unsigned d2 = __viaddmax_s16x2(u, P.nE2[k], 0xff82ff82u);
-    m[2 * k] *= __uint_as_float(kb + (d2 << 23));
-    m[2 * k + 1] *= __uint_as_float(kb + MMF_HI23(d2));
+    mul2(m[2 * k], m[2 * k + 1], m[2 * k], m[2 * k + 1], __uint_as_float(kb + (d2 << 23)),
+         __uint_as_float(kb + MMF_HI23(d2)));
   }
 }
 
@@ -687,9 +698,17 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
 #pragma unroll
     for (int q = 0; q < NF; ++q) {
       f[q] = 0.f;
-      if (q < N)
+      if (q < N) {
+#if MMF_F2
+        float f0 = 0.f, f1 = 0.f;  // (pairs of commodities: two partial sums)
+#pragma unroll
+        for (int c = 0; c < CPT; c += 2) fma2(f0, f1, tq[q < N ? q : 0][c], tq[q < N ? q : 0][c + 1], bl[c], bl[c + 1]);
+        f[q] = f0 + f1;
+#else
 #pragma unroll
         for (int c = 0; c < CPT; ++c) f[q] = fmaf(tq[q < N ? q : 0][c], bl[c], f[q]);
+#endif
+      }
     }
     if constexpr (NF == 4) {
       const float r = bfly4(f, lane);
@@ -780,7 +799,7 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
     for (int q = 0; q < N; ++q) {
       const float r = u.rq(h.rarc[q]);
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) s[c] = fmaf(r, tq[q][c], s[c]);
+      for (int c = 0; c < CPT; c += 2) fma2(s[c], s[c + 1], r, r, tq[q][c], tq[q][c + 1]);
     }
 #endif
   } else {  // large ratios: recompute from shared memory with the new factors
@@ -884,14 +903,15 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     const unsigned long long pol = l2_policy_keep();
     int pnode = j0, pslot = 0;
     auto prefetch = [&]() {
+      const int pn = alt_node(pnode, p.N, t);
       if (pnode < p.N && lane < D) {
-        cp_async16(&ring[pslot * D + lane], ell + (size_t)pnode * D + lane);
-        const ArcOps* go = (const ArcOps*)p.ell_ops + (size_t)(t - 1) * p.N * D + (size_t)pnode * D + lane;
+        cp_async16(&ring[pslot * D + lane], ell + (size_t)pn * D + lane);
+        const ArcOps* go = (const ArcOps*)p.ell_ops + (size_t)(t - 1) * p.N * D + (size_t)pn * D + lane;
         cp_async16(&oring[pslot * D + lane], go);
         cp_async16((char*)&oring[pslot * D + lane] + 16, (const char*)go + 16);
       }
       if (MMF_FWD_OWNG && pnode < p.N && lane >= 30) {  // the item's own row beta_t[j] -> L2 (read at its start)
-        const size_t g = (size_t)pnode * p.Lp;
+        const size_t g = (size_t)pn * p.Lp;
         if (lane == 30) bulk_prefetch_l2(bm + g, SW * 4);
         else bulk_prefetch_l2(be + g, SW * 2);
       }
@@ -909,7 +929,8 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
       ++rr.kold;
     };
     int k = 0, cslot = 0;
-    for (int j = j0; j < p.N; j += jstep, ++k) {
+    for (int jpos = j0; jpos < p.N; jpos += jstep, ++k) {
+      const int j = alt_node(jpos, p.N, t);
       cp_async_wait<FWD_P - 1>();
       __syncwarp();
       ArcKW<M> r;
@@ -978,6 +999,11 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
         bulk_g2s(sig + q * SW, bm + g, SW * 4, &full[ds]);
         bulk_g2s(sex + q * SW, be + g, SW * 2, &full[ds]);
       }
+      if (MMF_L2PF > 0 && lane >= 28 && lane < 30 && j + MMF_L2PF < p.N) {  // first touch of an upcoming row
+        const size_t g = (size_t)(j + MMF_L2PF) * p.Lp;
+        if (lane == 28) bulk_prefetch_l2(gm + g, SW * 4);
+        else bulk_prefetch_l2(ge + g, SW * 2);
+      }
       rr.head += (unsigned)nrow;
       rr.rpos += nrow;
       if (rr.rpos >= R) rr.rpos = 0;
@@ -992,14 +1018,26 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
   const int col = wg * 32 * CPT + lane * CPT;
   const int bar_id = 1 + pl * NG + grp;
   int k = grp;
-  for (int j = j0 + grp * jstep; j < p.N; j += NG * jstep, k += NG) {
+  Row<TrF32, CPT> bnext;  // (MMF_FWD_BPRE) own row of the group's next item, loaded one item ahead
+  if (MMF_FWD_OWNG && MMF_FWD_BPRE && j0 + grp * jstep < p.N) {
+    const size_t g = (size_t)alt_node(j0 + grp * jstep, p.N, t) * p.Lp + col;
+    bnext.load(v.bm(t) + g, v.be(t) + g);
+  }
+  for (int jpos = j0 + grp * jstep; jpos < p.N; jpos += NG * jstep, k += NG) {
+    const int j = alt_node(jpos, p.N, t);
     const int ds = k & (FWD_SDF - 1);
     Row<TrF32, CPT> bown;  // own row beta_t[j] (global; its latency overlaps the wait and the row math)
-    if constexpr (MMF_FWD_OWNG) {
+    if constexpr (MMF_FWD_OWNG && MMF_FWD_BPRE) {
+      bown = bnext;
+      if (jpos + NG * jstep < p.N) {
+        const size_t g = (size_t)alt_node(jpos + NG * jstep, p.N, t) * p.Lp + col;
+        bnext.load(v.bm(t) + g, v.be(t) + g);
+      }
+    } else if constexpr (MMF_FWD_OWNG) {
       const size_t g = (size_t)j * p.Lp + col;
       bown.load(v.bm(t) + g, v.be(t) + g);
     }
-    mbar_wait(&full[ds], (k / FWD_SDF) & 1);
+    mbar_wait_sleep(&full[ds], (k / FWD_SDF) & 1);
     const FwdHdr& h = hdr[ds];
     const ArcOps* hops = oring + h.oslot * D;
     MMF_DASSERT(h.start >= 0 && h.start + h.nr <= R && h.nr <= h.na && h.na <= D && h.oslot < PIPE_RP);
@@ -1160,7 +1198,8 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
     const unsigned long long pol = l2_policy_keep();
     int pslot = 0;
     auto prefetch = [&]() {
-      if (pf.node < p.N && lane < D) cp_async16(&ring[pslot * D + lane], ell + (size_t)pf.node * D + lane);
+      if (pf.node < p.N && lane < D)
+        cp_async16(&ring[pslot * D + lane], ell + (size_t)alt_node(pf.node, p.N, t) * D + lane);
       cp_async_commit();
       pf.next();
       pslot = pslot + 1 == PIPE_RP ? 0 : pslot + 1;
@@ -1220,6 +1259,11 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
         bulk_g2s_h(sig + q * SW, gm + g, SW * 4, &full[ds], p.l2hint, pol);
         bulk_g2s_h(sex + q * SW, ge + g, SW * 2, &full[ds], p.l2hint, pol);
       }
+      if (MMF_L2PF > 0 && lane >= 28 && lane < 30 && cur.node + MMF_L2PF < p.N) {  // first touch of an upcoming row
+        const size_t g = (size_t)(cur.node + MMF_L2PF) * p.Lp + (size_t)cur.sl * SW;
+        if (lane == 28) bulk_prefetch_l2(gm + g, SW * 4);
+        else bulk_prefetch_l2(ge + g, SW * 2);
+      }
       rr.head += (unsigned)n;
       rr.rpos += n;
       if (rr.rpos >= R) rr.rpos -= R;
@@ -1236,7 +1280,12 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
   E* const bet = v.be(t);
   for (int k = 0; it.node < p.N; ++k, it.next()) {
     const int ds = k & (FWD_SD - 1);
-    mbar_wait(&full[ds], (k / FWD_SD) & 1);
+    mbar_wait_sleep(&full[ds], (k / FWD_SD) & 1);
+    if (pc.dry == 1) {  // diagnostics: delivery rate of the producer / TMA alone
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[ds]);
+      continue;
+    }
     const PipeHdr& h = hdr[ds];
     const RingRows rw0{sig, sex, h.start, R, col, SW};
     M s[CPT];
@@ -1245,12 +1294,13 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) k_bwd_pipe2(DevPtrs p, PipeCfg
     else ring_sum<CPT>(RingRowsF<SW>(rw0), h, h.n, s, Ex);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[ds]);
-    const size_t g = (size_t)it.node * p.Lp + (size_t)(it.sl * SW + col);
+    const int node = alt_node(it.node, p.N, t);
+    const size_t g = (size_t)node * p.Lp + (size_t)(it.sl * SW + col);
     if constexpr (CPT % 2 == 0 && MMF_NORM_PACKED) {
-      norm_store_f32<CPT>(p, s, Ex, bmt + g, bet + g, it.sl * SW + col, it.node);
+      norm_store_f32<CPT>(p, s, Ex, bmt + g, bet + g, it.sl * SW + col, node);
     } else {
       Lane<M, E, CPT> out;
-      norm_lane<TrF32, CPT, false>(p, s, Ex, out, it.sl * SW + col, it.node);
+      norm_lane<TrF32, CPT, false>(p, s, Ex, out, it.sl * SW + col, node);
       out.store(bmt + g, bet + g);
     }
   }

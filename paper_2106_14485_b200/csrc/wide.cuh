@@ -19,6 +19,7 @@
 // integer add into the float's exponent field, acc = fma(x, scale, acc).
 #pragma once
 #include "tiled.cuh"
+#include "xpack.cuh"
 
 namespace mmf {
 
@@ -124,31 +125,23 @@ __device__ __forceinline__ void gather_sum(const typename T_::M* gm, const typen
 #pragma unroll
       for (int j = 0; j < NP; ++j) E2[j] = __viaddmax_s16x2(ew[j], k2, E2[j]);
     }
-    int nE[CPT];
+    XPre<CPT> P;
+    P.set(E2);
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
-      E[2 * j] = (int)(short)(E2[j] & 0xffffu);
-      E[2 * j + 1] = (int)E2[j] >> 16;
-      nE[2 * j] = -E[2 * j];
-      nE[2 * j + 1] = -E[2 * j + 1];
-    }
+    for (int c = 0; c < CPT; ++c) E[c] = P.E[c];
     float acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.f;
-    // pass 2: sum x * K W 2^(e - E)
+    // pass 2: sum x * K W 2^(e - E) (packed: the scale of a commodity pair by two 16x2 max-plus operations,
+    // the products by FFMA2; same arithmetic as the pipelined kernels' xacc)
 #pragma unroll kUnroll2
     for (int q = 0; q < n; ++q) {
       const unsigned kb = __float_as_uint((float)w.km[q]);
-      const int ke = w.ke[q];
+      const unsigned k2 = pack2(w.ke[q]);
       const size_t g = (size_t)w.node[q] * Lp + col;
-      Lane<float, int16_t, CPT> x;
+      Row<TrF32, CPT> x;
       x.load(gm + g, ge + g);
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        const int d = max((int)x.e[c] + ke + nE[c], -126);
-        const float sc = __uint_as_float(kb + ((unsigned)d << 23));
-        acc[c] = fmaf(x.m[c], sc, acc[c]);
-      }
+      xacc<CPT>(x, kb, k2, w.ke[q], P, acc);
     }
 #pragma unroll
     for (int c = 0; c < CPT; ++c) s[c] = acc[c];
@@ -256,15 +249,27 @@ __global__ void __launch_bounds__(WIDE_THREADS, MMF_WIDE_MINB) k_fwd_wide(DevPtr
     } else {
       // flow contributions of j's (capacitated, nonzero) out-arcs for this chunk
       const int k0 = p.out_ptr[j], k1 = p.out_ptr[j + 1];
+      unsigned aw[CPT / 2 > 0 ? CPT / 2 : 1];  // (fp32: the own row's exponents packed 16x2 for flow_terms_f2)
+      if constexpr (sizeof(M) == 4 && CPT % 2 == 0) {
+#pragma unroll
+        for (int k = 0; k < CPT / 2; ++k) aw[k] = pack_e2((int)a.e[2 * k], (int)a.e[2 * k + 1]);
+      }
       __syncwarp();
       for (int b = k0; b < k1; b += WARP_ARCS) {
         const int n = warp_arcs<M>((const ArcKW<M>*)p.outrec + (size_t)t * p.A, b, min(WARP_ARCS, k1 - b), oq0, wa,
                                    lane, FMODE != 2);
         for (int q = 0; q < n; ++q) {
           const size_t gg = (size_t)wa.node[q] * p.Lp + col;
-          Lane<M, E, CPT> bb;
-          bb.load(v.bm(t + 1) + gg, v.be(t + 1) + gg);
-          M f = flow_terms<T_, CPT>(a, bb, wa.km[q], wa.ke[q]);
+          M f;
+          if constexpr (sizeof(M) == 4 && CPT % 2 == 0) {
+            Row<TrF32, CPT> bb;
+            bb.load((const float*)(v.bm(t + 1) + gg), v.be(t + 1) + gg);
+            f = flow_terms_f2<CPT>((const float*)a.m, aw, bb, (float)wa.km[q], wa.ke[q]);
+          } else {
+            Lane<M, E, CPT> bb;
+            bb.load(v.bm(t + 1) + gg, v.be(t + 1) + gg);
+            f = flow_terms<T_, CPT>(a, bb, wa.km[q], wa.ke[q]);
+          }
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
           if (lane == 0) fpart[wa.pos[q] * wc.cpcta + cloc] = f;
