@@ -177,7 +177,10 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "stripw"   (experiments) strip width of the neighbour-overlap node order (0 = chosen by its score)
  *   "dry", "copy"  profiling / diagnostic modes of the pipelined kernels (dry 1: producers only, 2: no flows,
  *              3: no dual update; results invalid; never in production)
- *   "l2hint"   pipelined kernels: L2 evict_last policy on the gathered message rows (measured no gain; default 0) */
+ *   "l2hint"   pipelined kernels: L2 evict_last policy on the gathered message rows (measured no gain; default 0)
+ *   "pexch"    multi-GPU / virtual-rank Gauss-Seidel exchange (rem:multi_tensor_scheme P:1139-1147) on the pipelined
+ *              forward split around the all-reduce (flows-only launch, dual update, alpha-only launch): 1 on, 0 off
+ *              (wide-lane two-pass kernels), -1 auto (default: on for 1024-commodity slices) */
 mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);
 
 /* W = 1, UT = 1 on supp(muT), one backward pass (Alg. 2 "Initialize").  Async. */

@@ -129,7 +129,10 @@ struct mmf_ctx {
   int opt_wrap = -1;    // k_bwd_pipe2 ring wrap: -1 auto, 0 items never wrap, 1 items may wrap
   int opt_fgw = 0;      // pipelined forward: warps per consumer group (0 auto, 8, 4, 2)
   int opt_fng = 0;      // pipelined forward: consumer groups per pipeline (0 auto, 1 .. 6)
-  int opt_fnp = 0;      // pipelined forward: pipelines per CTA (0 auto, 1, 2)
+  int opt_fnp = 0;
+  int opt_pexch = -1;   // multi-GPU / virtual-rank Gauss-Seidel exchange on the pipelined kernels: 1 on, 0 off (wide-lane
+                        // two-pass), -1 auto = 1024-commodity slices (measured on [4]: 92 vs 115 ms/sweep at L = 1024, but
+                        // 74 vs 66 at 512 and 64 vs 57 at 256)      // pipelined forward: pipelines per CTA (0 auto, 1, 2)
   int opt_bwd = 0;      // backward kernel: 0 = auto (two-pipeline TMA kernel where it applies, else the window
                         // kernel), 1 = two-pipeline TMA kernel, 2 = window kernel, 3 = pipe (1 pipeline)
   PipeCfg5 pb2{};       // two-pipeline backward configuration
@@ -1493,7 +1496,7 @@ template <class T_> struct Eng {
     pipe_fwd_mode_launch<MODE>(c, s, t);
     // (the pipelined epilogues skip the layer's node factors: D here, and u in the readout; the sweep's u is
     // applied by k_node_cap)
-    if (MODE == 1 || MODE == 3) apply_factors(c, s, t, 0, MODE == 3);
+    if (MODE == 1 || MODE == 3 || MODE == 5) apply_factors(c, s, t, 0, MODE == 3);
   }
   template <int MODE> static void pipe_fwd_mode_launch(mmf_ctx* c, cudaStream_t s, int t) {
     const int SW = c->pf.SW, gw = c->pf_gw, ng = c->pf_ng, np = c->pf_np;
@@ -1603,6 +1606,11 @@ template <class T_> struct Eng {
     return MMF_OK;
   }
   // the multi-GPU exchange of one forward step: all-reduce the rank-partial F_t, then W_t update
+  // the exchange path runs on the pipelined kernels (fp32, one slice per node) unless option pexch = 0
+  static bool pipe_exchange(const mmf_ctx* c) {
+    return sizeof(M) == 4 && c->opt_kernels >= 5 && c->pipe_fwd && c->comm && pexch_on(c);
+  }
+  static bool pexch_on(const mmf_ctx* c) { return c->opt_pexch > 0 || (c->opt_pexch < 0 && c->pf.SW >= 1024); }
   static mmf_status exchange(mmf_ctx* c, cudaStream_t s, int t) {
     const DevPtrs& p = c->dp;
     int r = nccl_api().AllReduce(p.Fsum, p.Fsum, (size_t)c->Ecap, c->prec == MMF_FP32 ? NCCL_FLOAT32 : NCCL_FLOAT64,
@@ -1621,6 +1629,33 @@ template <class T_> struct Eng {
     VSum vs{};
     for (int g = 0; g < G; ++g) vs.f[g] = cs[g]->dp.Fsum;
     const unsigned ga = (unsigned)((c0->A + 255) / 256);
+    bool pipe = true;
+    for (int g = 0; g < G; ++g) pipe = pipe && sizeof(M) == 4 && cs[g]->opt_kernels >= 5 && cs[g]->pipe_fwd && pexch_on(cs[g]);
+    if (pipe) {  // the pipelined exchange path (as pipe_exchange): MODE 4 partials, device sum, dual, MODE 5 / 6
+      for (int g = 0; g < G; ++g) pipe_fwd(cs[g], s, 0);  // a2
+      for (int t = 1; t <= c0->T; ++t) {
+        for (int g = 0; g < G; ++g) {
+          LaunchScope ls(cs[g], K_FUSED, s);
+          pipe_fwd_mode<4>(cs[g], s, t);
+        }
+        {
+          LaunchScope ls(c0, K_REDUCE, s);
+          k_vsum<M><<<ga, 256, 0, s>>>(vs, G, c0->Ecap);
+        }
+        for (int g = 0; g < G; ++g) {
+          LaunchScope ls(cs[g], K_REDUCE, s);
+          k_dual<T_><<<ga, 256, 0, s>>>(cs[g]->dp, t - 1, 1);
+        }
+        for (int g = 0; g < G; ++g) {
+          LaunchScope ls(cs[g], K_FUSED, s);
+          if (t == c0->T) pipe_fwd_mode<6>(cs[g], s, t);
+          else pipe_fwd_mode<5>(cs[g], s, t);
+        }
+      }
+      for (int g = 0; g < G; ++g)
+        for (int t = c0->T - 1; t >= 0; --t) tiled_bwd(cs[g], s, t);  // a5
+      return MMF_OK;
+    }
     for (int t = 0; t <= c0->T; ++t) {
       for (int g = 0; g < G; ++g) tiled_fwd(cs[g], s, t, 1);  // alpha_t of the shard; its partial F_t -> Fsum
       if (t < c0->T) {
@@ -1654,6 +1689,28 @@ template <class T_> struct Eng {
         for (int t = 0; t <= c->T; ++t) {
           pipe_fwd(c, s, t);  // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
           node_cap(c, s, t);  // (node capacities: u_t, P:1093 on the states)
+        }
+      }
+      if (do_bwd) {
+        Nvtx r("backward pass (a5)");
+        for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      }
+      return MMF_OK;
+    }
+    if (pipe_exchange(c)) {  // multi-GPU Gauss-Seidel on the pipelined kernels: each step split around the exchange
+      {
+        Nvtx r("forward pass (a2, a3 + exchange, a4)");
+        pipe_fwd(c, s, 0);  // a2
+        for (int t = 1; t <= c->T; ++t) {
+          {
+            LaunchScope ls(c, K_FUSED, s);
+            pipe_fwd_mode<4>(c, s, t);  // rank-partial F_{t-1} -> Fsum
+          }
+          mmf_status st = exchange(c, s, t - 1);  // all-reduce, W_{t-1} update
+          if (st != MMF_OK) return st;
+          LaunchScope ls(c, K_FUSED, s);
+          if (t == c->T) pipe_fwd_mode<6>(c, s, t);  // alpha_T, a4
+          else pipe_fwd_mode<5>(c, s, t);  // alpha_t with the updated W_{t-1}
         }
       }
       if (do_bwd) {
@@ -1785,6 +1842,9 @@ template <class T_> struct Eng {
     CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
     CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
     CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+    CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+    CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
+    CU(cudaFuncSetAttribute(k_fwd_pipe<cpt, g, n, q, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm)); \
   }
         MMF_FWD_COMBOS(MMF_FWD_COMBO)
 #undef MMF_FWD_COMBO
@@ -2426,7 +2486,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order" || k == "pexch") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -2459,6 +2519,10 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_wrap = (int)value;
     }
     if (k == "l2hint") ctx->opt_l2hint = value != 0;
+    if (k == "pexch") {
+      if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "pexch must be -1 (auto), 0 or 1");
+      ctx->opt_pexch = (int)value;
+    }
     if (k == "fnp") {
       if (value < 0 || value > 3) return fail(ctx, MMF_EINVAL, "fnp must be in [0, 3]");
       ctx->opt_fnp = (int)value;

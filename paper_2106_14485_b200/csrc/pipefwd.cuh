@@ -7,6 +7,11 @@
 //   (ii)  W_{t-1}[a] <- min(W_{t-1}[a] d[a] / F_{t-1}[a], 1)                         (eq:sinkhorn_graph_Vineq P:861)
 //   (iii) alpha_t[j] = sum_{a -> j} alpha_{t-1}[i_a] K W_{t-1}[a] with the updated W    (eq:psi_hat P:1031-1036)
 // MODE 1: (i)-(iii); MODE 2: also a4 (t = T); MODE 3 (readout, Jacobi pass): (i) into Fout for every arc and
+// (iii) with the current factors, no update.  The multi-GPU Gauss-Seidel exchange (rem:multi_tensor_scheme
+// P:1139-1147) splits a step in two launches around the all-reduce of the rank-partial flows: MODE 4 computes
+// (i) over the rank's commodities into the compact exchange buffer Fsum (capacitated arcs), k_dual applies (ii)
+// to the all-reduced sums, then MODE 5 computes (iii) with the updated factors (MODE 6: also a4).
+// (earlier note:)
 // (iii) with the current factors, no update.
 //
 // Each CTA runs NP pipelines; a pipeline is one producer warp and NG consumer groups of GW warps (default 2 x
@@ -538,6 +543,23 @@ __device__ __forceinline__ UpdView fwd_update_phase(const DevPtrs& p, const FwdH
   return v;
 }
 
+template <int MODE> constexpr bool fwd_has_flows() { return MODE <= 4; }   // (MODE 5, 6: alpha only)
+template <int MODE> constexpr bool fwd_alpha_only() { return MODE == 5 || MODE == 6; }
+// exchange mode (MODE 4): the rank-partial flow of every capacitated in-arc (0 for zero-factor arcs) -> Fsum[fpos]
+template <int GW>
+__device__ __forceinline__ void fwd_exchange_store(const DevPtrs& p, const FwdHdr& h, const float (*fp)[PIPE_NWC],
+                                                   int lane, int wg) {
+  if (wg != 0 || lane >= h.na) return;
+  const int aux = h.aux[lane];
+  if (aux < 0) return;  // (uncapacitated at this step: not exchanged)
+  const int row = h.rowof[lane];
+  float F = 0.f;
+  if (row >= 0)
+#pragma unroll
+    for (int w = 0; w < GW; ++w) F += fp[row][w];
+  ((float*)p.Fsum)[p.fpos[aux]] = F;
+}
+
 // readout mode (MODE 3): the flow of every in-arc of the item (0 for zero-factor arcs) -> Fout[t - 1][arc], by
 // warp 0; the dual update is skipped and alpha uses the current factors
 template <int GW>
@@ -670,7 +692,8 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
     for (int q = 0; q < N; ++q) xterms_w<CPT>(xw[q], tq[q], h.kb[q], h.k2[q], P);
   }
   float bl[CPT];
-  if constexpr (MMF_FWD_OWNG) {
+  if constexpr (!fwd_has_flows<MODE>()) {
+  } else if constexpr (MMF_FWD_OWNG) {
     beta_lin<CPT>(bown, P, bl);
   } else {
     R_ b;
@@ -692,7 +715,7 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
       for (int c = 0; c < CPT; ++c) s[c] += tq[q][c] * bl[c];
     return;
   }
-  if (N > 0 && cap != 0u) {
+  if (fwd_has_flows<MODE>() && N > 0 && cap != 0u) {
     constexpr int NF = N <= 4 ? 4 : 8;
     float f[NF];
 #pragma unroll
@@ -731,9 +754,13 @@ __device__ __forceinline__ void fwd_body(const DevPtrs& p, const RingRows& rw0, 
 #pragma unroll
     for (int c = 0; c < CPT; ++c) sp[c] += tq[q][c];
 #endif
-  named_bar(bar_id, GW * 32);
-  if constexpr (MODE == 3) {  // readout: flows out, alpha with the current factors
-    fwd_readout_store<GW>(p, h, fp, t, lane, wg);
+  if constexpr (fwd_has_flows<MODE>()) named_bar(bar_id, GW * 32);
+  if constexpr (MODE == 4) {  // exchange: the rank-partial flows out, no alpha
+    fwd_exchange_store<GW>(p, h, fp, lane, wg);
+    return;
+  }
+  if constexpr (MODE == 3 || fwd_alpha_only<MODE>()) {  // readout: flows out, alpha with the current factors
+    if constexpr (MODE == 3) fwd_readout_store<GW>(p, h, fp, t, lane, wg);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       s[c] = 0.f;
@@ -826,7 +853,10 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& r
   XPre<CPT> P;
   P.set(E2);
   float bl[CPT];
-  if constexpr (MMF_FWD_OWNG) {
+  if constexpr (!fwd_has_flows<MODE>()) {
+    fwd_alpha_new<CPT>(rw, h, fwd_old_view(h, lane), nr, s, Ex);  // (alpha only: the current factors)
+    return;
+  } else if constexpr (MMF_FWD_OWNG) {
     beta_lin<CPT>(bown, P, bl);
   } else {
     R_ b;
@@ -847,6 +877,10 @@ __device__ __forceinline__ void fwd_body_any(const DevPtrs& p, const RingRows& r
     if (lane == 0) fp[q][wg] = f;
   }
   named_bar(bar_id, GW * 32);
+  if constexpr (MODE == 4) {
+    fwd_exchange_store<GW>(p, h, fp, lane, wg);
+    return;
+  }
   if constexpr (MODE == 3) {
     fwd_readout_store<GW>(p, h, fp, t, lane, wg);
     fwd_alpha_new<CPT>(rw, h, fwd_old_view(h, lane), nr, s, Ex);
@@ -910,7 +944,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
         cp_async16(&oring[pslot * D + lane], go);
         cp_async16((char*)&oring[pslot * D + lane] + 16, (const char*)go + 16);
       }
-      if (MMF_FWD_OWNG && pnode < p.N && lane >= 30) {  // the item's own row beta_t[j] -> L2 (read at its start)
+      if (MMF_FWD_OWNG && fwd_has_flows<MODE>() && pnode < p.N && lane >= 30) {  // the item's own row beta_t[j] -> L2 (read at its start)
         const size_t g = (size_t)pn * p.Lp;
         if (lane == 30) bulk_prefetch_l2(bm + g, SW * 4);
         else bulk_prefetch_l2(be + g, SW * 2);
@@ -1033,7 +1067,7 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
         const size_t g = (size_t)alt_node(jpos + NG * jstep, p.N, t) * p.Lp + col;
         bnext.load(v.bm(t) + g, v.be(t) + g);
       }
-    } else if constexpr (MMF_FWD_OWNG) {
+    } else if constexpr (MMF_FWD_OWNG && fwd_has_flows<MODE>()) {
       const size_t g = (size_t)j * p.Lp + col;
       bown.load(v.bm(t) + g, v.be(t) + g);
     }
@@ -1073,7 +1107,8 @@ __global__ void __launch_bounds__(fwd_threads<GW, NG, NP>(), 1) k_fwd_pipe(DevPt
     if (lane == 0) mbar_arrive(&empty[ds]);
     // s is 0 or a normal float (ratios are within 2^+-40 of the previous terms): bit-level normalisation
     const size_t g = (size_t)j * p.Lp + col;
-    if constexpr (MODE == 2) {  // a4: UT = muT ./ alpha_T -> beta_T
+    if constexpr (MODE == 4) {  // (exchange: flows only)
+    } else if constexpr (MODE == 2 || MODE == 6) {  // a4: UT = muT ./ alpha_T -> beta_T
       Lane<M, E, CPT> a;
       norm_lane<TrF32, CPT, false>(p, s, Ex, a, col, j);
       a.store(v.am(t) + g, v.ae(t) + g);

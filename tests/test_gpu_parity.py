@@ -809,3 +809,48 @@ def test_state_space_problems_parity(policy, prec, L, opts):
     from workloads.statespace import state_problem
     p = state_problem(policy, T=12, eps=0.1, seed=2, L=L, edge_cap=(0.004 * L, 0.012 * L))
     _node_parity(p, 4, prec, opts)
+
+
+# ---------------------------------------------------------------------------------------------
+# the multi-GPU Gauss-Seidel exchange on the pipelined kernels (flows-only launch -> all-reduce -> dual update ->
+# alpha-only launch; rem:multi_tensor_scheme P:1139-1147)
+
+@pytest.mark.parametrize("opts", [dict(), dict(pexch=0), dict(pexch=1)])
+def test_nccl_exchange_path_pipelined_one_rank(opts):
+    """The per-step exchange of the commodity-sharded sweep with the pipelined forward split around the all-reduce
+    (MODE 4 rank-partial flows of the capacitated arcs, k_dual on the sums, MODE 5 / 6 alpha with the updated W) on a
+    one-rank NCCL communicator, fp32 and L >= 256, against the oracle; pexch=0 runs the wide-lane two-pass kernels."""
+    import torch
+    torch.cuda.nccl.version()
+    from paper_2106_14485_b200 import _lib
+    p = grid_problem(12, 12, 8, 1019, 0.1, seed=33, cap=(0.3, 1.5))
+    assert_parity(p, 4, "fp32", nccl_uid=_lib.mmf_nccl_unique_id(), nranks=1, rank=0, options=opts)
+
+
+@pytest.mark.parametrize("L,G,marg,opts", [(2040, 2, "point", {}), (1019, 3, "point", dict(pexch=1)), (600, 2, "dense", dict(pexch=1))])
+def test_virtual_ranks_pipelined_exchange(L, G, marg, opts):
+    """Virtual ranks (mmf_sweep_group) with the default kernels: every shard has L / G >= 256 commodities, so the
+    sweep runs the pipelined exchange path (flows-only launches, device-side sum, dual update, alpha-only launches);
+    the shards' duals agree, the summed flows equal the unsharded run and the oracle (fp32 tolerance)."""
+    from paper_2106_14485_b200 import Solver, _lib
+    sc = L / 100 if marg == "point" else 0.2
+    p = grid_problem(9, 9, 7, L, 0.1, seed=52, cap=(0.3 * sc, 1.0 * sc), marginals=marg)
+    per = (L + G - 1) // G
+    bounds = [(min(g * per, L), min((g + 1) * per, L)) for g in range(G)]
+    shards = [Solver(p, prec="fp32", l_begin=a, l_count=b - a, options=opts) for a, b in bounds]
+    try:
+        _lib.mmf_sweep_group([s.ctx for s in shards], 4)
+        for s in shards:
+            s.sync()
+        F = sum(s.edge_flows() for s in shards)
+        Ws = [s.cap_duals() for s in shards]
+    finally:
+        for s in shards:
+            s.close()
+    for W in Ws[1:]:
+        assert np.array_equal(W, Ws[0])
+    Fu, Wu, _ = run_gpu(p, 4, "fp32")
+    assert max_rel_err(F, Fu, flow_floor(p)) < TOL["fp32"] and max_rel_err(Ws[0], Wu, W_FLOOR) < TOL["fp32"]
+    Fo, Wo, _ = run_oracle(p, 4)
+    assert max_rel_err(F, Fo, flow_floor(p)) < TOL["fp32"] and max_rel_err(Ws[0], Wo, W_FLOOR) < TOL["fp32"]
+    assert np.min(Wo) < 0.99

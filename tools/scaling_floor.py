@@ -2,7 +2,8 @@
 on ONE GPU, a rank's share L/G of [4] through the multi-GPU exchange path (one-rank NCCL communicator: partial flows ->
 ncclAllReduce -> dual update per step, the same kernels and calls as G ranks make), for G = 1, 2, 4, 8, next to the
 single-GPU path.  The G-GPU sweep cannot be faster than this per-rank time (+ the cross-GPU all-reduce latency, which a
-one-rank communicator does not pay).   usage: python tools/scaling_floor.py > out.json"""
+one-rank communicator does not pay).   usage: python tools/scaling_floor.py [--config 4|5] > out.json"""
+import argparse
 import json
 import os
 import sys
@@ -16,7 +17,11 @@ torch.cuda.nccl.version()
 from paper_2106_14485_b200 import Solver, _lib  # noqa: E402
 from workloads import gen  # noqa: E402
 
-p = gen(4)
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--sweeps", type=int, default=5)
+a = ap.parse_args()
+p = gen(a.config)
 out = {"workload": p.name, "L": p.L, "rows": []}
 for G in (1, 2, 4, 8):
     per = p.L // G
@@ -26,11 +31,11 @@ for G in (1, 2, 4, 8):
             s.sync()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            s.sweep(5)
+            s.sweep(a.sweeps)
             e1.record()
             s.sync()
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / 5
+            ms = e0.elapsed_time(e1) / a.sweeps
         row = {"G": G, "L_rank": per, "path": name, "ms_per_sweep": ms}
         out["rows"].append(row)
         print(row, file=sys.stderr, flush=True)
