@@ -156,8 +156,7 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "kernels"  kernel family 1..6 (default 6 = TMA-pipelined forward (2 pipelines / CTA) and
  *              backward (3 pipelines / CTA); 5 single-pipeline; 4 register head-flow; 3 wide-lane;
  *              2 smem node tiles; 1 per-node reference kernels)
- *   "bwd"      backward kernel with kernels >= 5: 0 auto, 1 three-pipeline, 2 sliding window, 3 single,
- *              4 row-reuse rings (contiguous node blocks, resident rows referenced instead of reloaded)
+ *   "bwd"      backward kernel with kernels >= 5: 0 auto, 1 three-pipeline, 2 sliding window, 3 single
  *   "schedule" 0 = Gauss-Seidel (Algorithm 2, default), 1 = damped Jacobi (every W_t from
  *              one alpha/beta pair, W <- W^(1-theta) min(W d / F, 1)^theta; one all-reduce of the T x n_arcs
  *              flows per sweep on the multi-GPU path)

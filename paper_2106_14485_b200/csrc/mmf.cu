@@ -9,7 +9,6 @@
 #include "kernels.cuh"
 #include "tiled.cuh"
 #include "win.cuh"
-#include "reuse.cuh"
 
 #include <dlfcn.h>
 #include <future>
@@ -137,8 +136,6 @@ struct mmf_ctx {
                         // kernel), 1 = two-pipeline TMA kernel, 2 = window kernel, 3 = pipe (1 pipeline)
   PipeCfg5 pb2{};       // two-pipeline backward configuration
   bool pipe2_bwd = false;
-  bool ru_bwd = false;  // row-reuse backward (reuse.cuh)
-  PipeCfg5 pr{};
 
   // ---- derived
   int Lp = 0, G = 0, block = 0, maxdeg_in = 0;
@@ -426,7 +423,6 @@ void derive_shapes(mmf_ctx* c) {
   }
   c->CPT = c->opt_cpt ? c->opt_cpt : cpt_auto;
   if (c->prec == MMF_FP64) c->CPT = std::min(c->CPT, 2);   // fp64 lanes: at most 2 (16-byte loads)
-  if (c->opt_kernels == 2) c->CPT = std::min(c->CPT, 4);   // tile kernels: instantiated for 1, 2, 4
   c->LC = 32 * c->CPT;
   c->Lp = ((c->L + c->LC - 1) / c->LC) * c->LC;
   // pipelined backward (fp32, ELL width <= 32): slice width SW = 256 * cp commodities, S stages of
@@ -505,22 +501,6 @@ void derive_shapes(mmf_ctx* c) {
     }
   }
   if (c->opt_bwd == 3) c->win_bwd = false;
-  // row-reuse backward: contiguous node blocks per pipeline, resident rows referenced instead of reloaded
-  c->ru_bwd = false;
-  // (option only: measured slower than the three-pipeline kernel on [4] and [5])
-  if (c->pipe_bwd && c->pb.SW >= 512 && c->opt_bwd == 4 && c->pb.D < 32) {
-    const size_t budget = 226 * 1024 / RU_NP;
-    int R = 0;
-    while (ru_smem(R + 1, c->pb.D, c->pb.SW).total <= budget) ++R;
-    if (R >= c->pb.D) {
-      c->ru_bwd = true;
-      c->pr = c->pb;
-      c->pr.R = R;
-      c->pr.ns = c->Lp / c->pb.SW;
-      c->pr.nitems = c->N * c->pr.ns;
-      c->win_bwd = false;
-    }
-  }
   // pipelined forward: one item per node (all Lp commodities in one slice of the backward's width), NG
   // consumer groups of GW warps per pipeline (a warp owns 32 CPT = SW / GW commodities)
   c->pipe_fwd = false;
@@ -1376,50 +1356,6 @@ template <class T_> struct Eng {
     return MMF_OK;
   }
 
-  // ---------------- node-tile path (opt_kernels == 2)
-  template <int CPT, int MODE, int FMODE> static void launch_fwd(mmf_ctx* c, cudaStream_t s, int t, size_t smem) {
-    dim3 grid(c->ntiles, c->pc.ngroup);
-    k_fwd_tile<T_, CPT, MODE, FMODE><<<grid, TILE_THREADS, smem, s>>>(lay(c, t, FMODE == 2), c->tm, c->pc, t);
-  }
-  template <int CPT> static void tiled_fwd_cpt(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
-    const int mode = t == 0 ? 0 : (t == c->T ? 2 : 1);
-    const size_t smem = FwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_hin, c->max_ia, c->max_oa);
-    switch (mode * 3 + fmode) {
-      case 0: launch_fwd<CPT, 0, 0>(c, s, t, smem); break;
-      case 1: launch_fwd<CPT, 0, 1>(c, s, t, smem); break;
-      case 2: launch_fwd<CPT, 0, 2>(c, s, t, smem); break;
-      case 3: launch_fwd<CPT, 1, 0>(c, s, t, smem); break;
-      case 4: launch_fwd<CPT, 1, 1>(c, s, t, smem); break;
-      case 5: launch_fwd<CPT, 1, 2>(c, s, t, smem); break;
-      case 6: launch_fwd<CPT, 2, 0>(c, s, t, smem); break;
-      case 7: launch_fwd<CPT, 2, 1>(c, s, t, smem); break;
-      default: launch_fwd<CPT, 2, 2>(c, s, t, smem); break;
-    }
-  }
-  template <int CPT> static void tiled_bwd_cpt(mmf_ctx* c, cudaStream_t s, int t) {
-    dim3 grid(c->ntiles, c->pc.ngroup);
-    k_bwd_tile<T_, CPT><<<grid, TILE_THREADS, BwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_oa), s>>>(
-        lay(c, t), c->tm, c->pc, t);
-  }
-  template <int CPT> static cudaError_t tiled_attrs_cpt(mmf_ctx* c) {
-    const int fwd = (int)FwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_hin, c->max_ia, c->max_oa);
-    const int bwd = (int)BwdSmem<T_, CPT>::bytes(c->max_hout, c->tileB, c->max_oa);
-    cudaError_t e = cudaSuccess;
-#define MMF_ATTR(K, B) \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, B);
-    MMF_ATTR((k_fwd_tile<T_, CPT, 0, 0>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 0, 1>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 0, 2>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 1, 0>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 1, 1>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 1, 2>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 2, 0>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 2, 1>), fwd)
-    MMF_ATTR((k_fwd_tile<T_, CPT, 2, 2>), fwd)
-    MMF_ATTR((k_bwd_tile<T_, CPT>), bwd)
-#undef MMF_ATTR
-    return e;
-  }
   static constexpr bool is_f32() { return sizeof(M) == 4; }
   // ---------------- wide-lane path (opt_kernels == 3)
   template <int CPT, int MODE, int FMODE> static void launch_fwd_wide(mmf_ctx* c, cudaStream_t s, int t) {
@@ -1474,17 +1410,11 @@ template <class T_> struct Eng {
     k_bwd_head<T_, CPT><<<(unsigned)((warps + HF_WARPS - 1) / HF_WARPS), HF_WARPS * 32, 0, s>>>(lay(c, t), c->hc, t);
   }
   static void tiled_fwd(mmf_ctx* c, cudaStream_t s, int t, int fmode) {
-    LaunchScope ls(c, K_FUSED, s);
-    if (c->opt_kernels >= 3) {
-      if (c->CPT == 1) wide_fwd_cpt<1>(c, s, t, fmode);
-      else if (c->CPT == 2 || !is_f32()) wide_fwd_cpt<2>(c, s, t, fmode);
-      else if (c->CPT == 4) wide_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
-      else wide_fwd_cpt<is_f32() ? 8 : 2>(c, s, t, fmode);
-      return;
-    }
-    if (c->CPT == 1) tiled_fwd_cpt<1>(c, s, t, fmode);
-    else if (c->CPT == 2) tiled_fwd_cpt<2>(c, s, t, fmode);
-    else tiled_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
+    LaunchScope ls(c, K_FUSED, s);  // (kernels >= 3: the wide-lane forward)
+    if (c->CPT == 1) wide_fwd_cpt<1>(c, s, t, fmode);
+    else if (c->CPT == 2 || !is_f32()) wide_fwd_cpt<2>(c, s, t, fmode);
+    else if (c->CPT == 4) wide_fwd_cpt<is_f32() ? 4 : 2>(c, s, t, fmode);
+    else wide_fwd_cpt<is_f32() ? 8 : 2>(c, s, t, fmode);
   }
   template <int CPT, int GW, int NG, int NP, int MODE> static void pipe_fwd_launch(mmf_ctx* c, cudaStream_t s, int t) {
     const PipeCfg5& pc = c->pf;
@@ -1556,14 +1486,6 @@ template <class T_> struct Eng {
           k_bwd_win<1><<<grid, WIN_THREADS, win_smem<1>(w).total, s>>>(lay(c, t), w, c->wdo, c->tmb, tma, t);
         return true;
       }
-      if (c->ru_bwd) {
-        const PipeCfg5& pc = c->pr;
-        const unsigned grid = (unsigned)std::min((c->N + RU_NP - 1) / RU_NP, c->sms);
-        const size_t sm = RU_NP * ru_smem(pc.R, pc.D, pc.SW).total;
-        if (pc.SW == 1024) k_bwd_reuse<4><<<grid, RU_THREADS, sm, s>>>(lay(c, t), pc, t);
-        else k_bwd_reuse<2><<<grid, RU_THREADS, sm, s>>>(lay(c, t), pc, t);
-        return true;
-      }
       if (c->pipe2_bwd) {
         const int cp = c->pb2.SW / 256;
         if (cp == 4) pipe2_bwd_cpt<4>(c, s, t);
@@ -1586,24 +1508,11 @@ template <class T_> struct Eng {
       else head_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
       return false;
     }
-    if (c->opt_kernels == 3) {
-      if (c->CPT == 1) wide_bwd_cpt<1>(c, s, t);
-      else if (c->CPT == 2 || !is_f32()) wide_bwd_cpt<2>(c, s, t);
-      else if (c->CPT == 4) wide_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
-      else wide_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
-      return false;
-    }
-    if (c->CPT == 1) tiled_bwd_cpt<1>(c, s, t);
-    else if (c->CPT == 2) tiled_bwd_cpt<2>(c, s, t);
-    else tiled_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
+    if (c->CPT == 1) wide_bwd_cpt<1>(c, s, t);  // (kernels == 3)
+    else if (c->CPT == 2 || !is_f32()) wide_bwd_cpt<2>(c, s, t);
+    else if (c->CPT == 4) wide_bwd_cpt<is_f32() ? 4 : 2>(c, s, t);
+    else wide_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
     return false;
-  }
-  static mmf_status tiled_attrs(mmf_ctx* ctx) {
-    mmf_ctx* c = ctx;
-    if (c->CPT == 1) CU(tiled_attrs_cpt<1>(c));
-    else if (c->CPT == 2) CU(tiled_attrs_cpt<2>(c));
-    else CU(tiled_attrs_cpt<is_f32() ? 4 : 2>(c));
-    return MMF_OK;
   }
   // the multi-GPU exchange of one forward step: all-reduce the rank-partial F_t, then W_t update
   // the exchange path runs on the pipelined kernels (fp32, one slice per node) unless option pexch = 0
@@ -1796,10 +1705,6 @@ template <class T_> struct Eng {
   static mmf_status init_device(mmf_ctx* ctx, cudaStream_t s) {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
-    if (c->opt_kernels == 2) {
-      mmf_status st = tiled_attrs(c);
-      if (st != MMF_OK) return st;
-    }
     if constexpr (sizeof(M) == 4) {
       if (c->pipe_bwd) {
         const int sm = (int)pipe_smem(c->pb.R, c->pb.SD, c->pb.D, c->pb.SW).total;
@@ -1821,12 +1726,6 @@ template <class T_> struct Eng {
           fprintf(stderr, "[mmf] window bwd: cpt %d Wb %d RBa %d ns %d nseg %d segB %d farmax %d maxrec %d smem %zu\n",
                   c->win_cpt, c->wcb.Wb, c->wcb.RBa, c->wcb.ns, c->wcb.nseg, c->wcb.segB, c->wcb.farmax,
                   c->wcb.maxrec, c->win_cpt == 4 ? win_smem<4>(c->wcb).total : c->win_cpt == 2 ? win_smem<2>(c->wcb).total : win_smem<1>(c->wcb).total);
-      }
-      if (c->ru_bwd) {
-        const int sm = RU_NP * (int)ru_smem(c->pr.R, c->pr.D, c->pr.SW).total;
-        CU(cudaFuncSetAttribute(k_bwd_reuse<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        CU(cudaFuncSetAttribute(k_bwd_reuse<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
-        if (getenv("MMF_VERBOSE")) fprintf(stderr, "[mmf] reuse bwd: SW %d R %d D %d smem %d\n", c->pr.SW, c->pr.R, c->pr.D, sm);
       }
       if (c->pipe2_bwd) {
         const int sm = BWD_NP * (int)((pipe_smem(c->pb2.R, FWD_SD, c->pb2.D, c->pb2.SW).total + 127) / 128 * 128);
@@ -2492,7 +2391,10 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
     if (k == "dry") ctx->opt_dry = (int)value;
     if (k == "copy") ctx->opt_copy = (int)value;
     if (k == "wintma") ctx->opt_wintma = (int)value;
-    if (k == "bwd") ctx->opt_bwd = (int)value;
+    if (k == "bwd") {
+      if (value < 0 || value > 3) return fail(ctx, MMF_EINVAL, "bwd must be 0 .. 3");
+      ctx->opt_bwd = (int)value;
+    }
     if (k == "fgw") {
       if (value != 0 && value != 2 && value != 4 && value != 8) return fail(ctx, MMF_EINVAL, "fgw must be 0, 2, 4 or 8");
       ctx->opt_fgw = (int)value;
@@ -2528,7 +2430,8 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_fnp = (int)value;
     }
     if (k == "kernels") {
-      if (value < 1 || value > 6) return fail(ctx, MMF_EINVAL, "kernels must be 1 .. 6");
+      if (value < 1 || value > 6 || value == 2)
+        return fail(ctx, MMF_EINVAL, "kernels must be 1 or 3 .. 6 (the node-tile family 2 was removed)");
       ctx->opt_kernels = (int)value;
     }
     if (k == "tile") {
