@@ -179,7 +179,11 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "l2hint"   pipelined kernels: L2 evict_last policy on the gathered message rows (measured no gain; default 0)
  *   "pexch"    multi-GPU / virtual-rank Gauss-Seidel exchange (rem:multi_tensor_scheme P:1139-1147) on the pipelined
  *              forward split around the all-reduce (flows-only launch, dual update, alpha-only launch): 1 on, 0 off
- *              (wide-lane two-pass kernels), -1 auto (default: on for 1024-commodity slices) */
+ *              (wide-lane two-pass kernels), -1 auto (default: on for 1024-commodity slices)
+ *   "tbwd"     backward on node tiles (BFS blobs of "tile" nodes whose out-halo stays within "halo" rows; the halo
+ *              rows of a (tile, commodity chunk) staged once by TMA, the tile's nodes computed from shared memory):
+ *              1 on, 0 off, -1 auto (default: fp32, L >= 256 and mean degree >= 7, e.g. BJ [3] and [5]); it sets
+ *              the node order to the tile order */
 mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);
 
 /* W = 1, UT = 1 on supp(muT), one backward pass (Alg. 2 "Initialize").  Async. */

@@ -9,6 +9,7 @@
 #include "kernels.cuh"
 #include "tiled.cuh"
 #include "win.cuh"
+#include "tilebwd.cuh"
 
 #include <dlfcn.h>
 #include <future>
@@ -129,6 +130,12 @@ struct mmf_ctx {
   int opt_fgw = 0;      // pipelined forward: warps per consumer group (0 auto, 8, 4, 2)
   int opt_fng = 0;      // pipelined forward: consumer groups per pipeline (0 auto, 1 .. 6)
   int opt_fnp = 0;
+  int opt_tbwd = -1;    // backward: 1 = node tiles with staged out-halos (tilebwd.cuh; nodes ordered into tiles), 0 off,
+                        // -1 auto: fp32, L >= 256 and mean degree >= 7 (measured: [5] 34.4 vs 40.0 ms/sweep, [3] 5.4 vs
+                        // 7.7; [4], degree 4.8, 71 vs 31)
+  bool tile_bwd = false;
+  TileCfg tbc{};
+  int tb_cpt = 4;
   int opt_pexch = -1;   // multi-GPU / virtual-rank Gauss-Seidel exchange on the pipelined kernels: 1 on, 0 off (wide-lane
                         // two-pass), -1 auto = 1024-commodity slices (measured on [4]: 92 vs 115 ms/sweep at L = 1024, but
                         // 74 vs 66 at 512 and 64 vs 57 at 256)      // pipelined forward: pipelines per CTA (0 auto, 1, 2)
@@ -148,6 +155,9 @@ struct mmf_ctx {
   int64_t Ecap = 0;
   bool fpos_ok = false;
   int ntiles = 0, tileB = 0, max_hin = 0, max_hout = 0, max_ia = 0, max_oa = 0;
+  std::vector<int> h_tb_desc, h_tb_meta;  // tile backward: per-tile descriptors (8 ints) and 16-B aligned static metadata
+  const int* d_tb_desc = nullptr;
+  const int* d_tb_meta = nullptr;
   std::vector<int> h_tile_ptr, h_hin_ptr, h_hin_node, h_hout_ptr, h_hout_node, h_in_hidx, h_out_hidx;
   TileMeta tm{};
   PipeCfg pc{1, 1};
@@ -406,6 +416,7 @@ void make_tiles(int N, const std::vector<int>& tail, const std::vector<int>& hea
 }
 
 void build_window_tables(mmf_ctx* c);
+bool tbwd_wanted(const mmf_ctx* c);
 
 void derive_shapes(mmf_ctx* c) {
   HostTimer ht("derive_shapes");
@@ -530,6 +541,28 @@ void derive_shapes(mmf_ctx* c) {
       c->pf_gw = gw;
       c->pf_ng = ng;
       c->pf_np = np;
+    }
+  }
+  // tile backward (option tbwd): stages of the largest out-halo x SW commodities; SW = 256 when two stages fit
+  c->tile_bwd = false;
+  if (tbwd_wanted(c) && c->max_hout > 0) {
+    const size_t budget = 226 * 1024;
+    const int MA = c->max_oa;
+    int MB = 0;  // (largest static metadata block, ints)
+    for (int k = 0; k < c->ntiles; ++k) MB = std::max(MB, c->h_tb_desc[(size_t)k * 8 + 7]);
+    int cpt = (c->Lp % 256 == 0 && tb_smem(2, c->max_hout, 256, MA, MB) <= budget) ? 8 : 4;
+    const int SW = 32 * cpt;
+    int nst = 1;
+    while (nst < 6 && tb_smem(nst + 1, c->max_hout, SW, MA, MB) <= budget) ++nst;
+    if (c->Lp % SW == 0 && nst >= 2) {
+      c->tile_bwd = true;
+      c->tb_cpt = cpt;
+      c->tbc.nst = nst;
+      c->tbc.H = c->max_hout;
+      c->tbc.MA = MA;
+      c->tbc.MB = MB;
+      c->tbc.nch = c->Lp / SW;
+      c->tbc.nitems = c->ntiles * c->tbc.nch;
     }
   }
   c->nch = c->Lp / c->LC;
@@ -908,6 +941,13 @@ void augment_times(mmf_ctx* c) {
   c->augmented = true;
 }
 
+// the tile backward applies (option tbwd; decided before the node order, which it dictates)
+bool tbwd_wanted(const mmf_ctx* c) {
+  if (c->prec != MMF_FP32 || c->opt_kernels != 6 || c->opt_tbwd == 0) return false;
+  if (c->opt_tbwd > 0) return true;
+  return c->L >= 256 && c->A >= 7 * (int64_t)c->N && c->opt_bwd == 0;
+}
+
 void prepare(mmf_ctx* c) {
   if (c->prepared) return;
   HostTimer ht("prepare");
@@ -917,7 +957,15 @@ void prepare(mmf_ctx* c) {
   const int64_t A = c->A;
   std::vector<int> order;
   const int B = c->opt_kernels >= 2 ? c->opt_tile : std::max(N, 1);
-  if (c->opt_kernels == 6 && c->opt_reorder) {
+  if (tbwd_wanted(c)) {
+    // node tiles for the tile backward: BFS-grown blobs of at most `tile` nodes whose halos stay within `halo`
+    const int Bt = c->opt_tile;
+    make_tiles(N, c->tail, c->head, Bt, c->opt_halo > 0 ? c->opt_halo : 2 * Bt, c->opt_reorder, order, c->h_tile_ptr);
+    c->newid.assign(N, 0);
+    for (int k = 0; k < N; ++k) c->newid[order[k]] = k;
+    c->win_Wb = 0;
+    c->win_cpt = 4;
+  } else if (c->opt_kernels == 6 && c->opt_reorder) {
     // node order: the window kernel's cost model for the window backward (bwd=2) and for the other kernel
     // families (measured better for them on [2]), plain RCM on request (order=1), else the order with the most
     // neighbour overlap between consecutive nodes (measured best for the pipelined kernels: [4] 85.4 vs 87.1
@@ -1013,8 +1061,8 @@ void prepare(mmf_ctx* c) {
   }
   c->ell_din = din;
 
-  // halos (node-tile kernels only, kernels = 2; the other families get empty tables of the right sizes)
-  if (c->opt_kernels != 2) {
+  // halos (tile backward only; the other families get empty tables of the right sizes)
+  if (!tbwd_wanted(c)) {
     const size_t nt = (size_t)c->ntiles;
     c->h_hin_ptr.assign(nt + 1, 0);
     c->h_hout_ptr.assign(nt + 1, 0);
@@ -1023,6 +1071,8 @@ void prepare(mmf_ctx* c) {
     c->h_in_hidx.assign(A, 0);
     c->h_out_hidx.assign(A, 0);
     c->max_hin = c->max_hout = c->max_ia = c->max_oa = 0;
+    c->h_tb_desc.clear();
+    c->h_tb_meta.clear();
     c->prepared = true;
     return;
   }
@@ -1062,6 +1112,29 @@ void prepare(mmf_ctx* c) {
     for (int q = c->h_outptr[v0]; q < c->h_outptr[v1]; ++q)
       c->h_out_hidx[q] = (int)(std::lower_bound(c->h_hout_node.begin() + base_out, c->h_hout_node.end(), c->h_outhead[q]) -
                                (c->h_hout_node.begin() + base_out));
+  }
+  // tile backward: per tile {v0, nv, q0, na, h0, nh, meta offset (ints, multiple of 4), meta ints (multiple of 4)} and
+  // the static metadata [nv + 1 local out-CSR offsets | pad | na halo indices | pad] at 16-byte aligned offsets, so
+  // that the producer stages a tile with one descriptor load and bulk copies only
+  c->h_tb_desc.assign((size_t)c->ntiles * 8, 0);
+  c->h_tb_meta.clear();
+  for (int k = 0; k < c->ntiles; ++k) {
+    const int v0 = c->h_tile_ptr[k], v1 = c->h_tile_ptr[k + 1];
+    const int q0 = c->h_outptr[v0], q1 = c->h_outptr[v1];
+    const int off = (int)c->h_tb_meta.size();
+    for (int v = v0; v <= v1; ++v) c->h_tb_meta.push_back(c->h_outptr[v] - q0);
+    while (c->h_tb_meta.size() % 4) c->h_tb_meta.push_back(0);
+    for (int q = q0; q < q1; ++q) c->h_tb_meta.push_back(c->h_out_hidx[q]);
+    while (c->h_tb_meta.size() % 4) c->h_tb_meta.push_back(0);
+    int* d = &c->h_tb_desc[(size_t)k * 8];
+    d[0] = v0;
+    d[1] = v1 - v0;
+    d[2] = q0;
+    d[3] = q1 - q0;
+    d[4] = c->h_hout_ptr[k];
+    d[5] = c->h_hout_ptr[k + 1] - c->h_hout_ptr[k];
+    d[6] = off;
+    d[7] = (int)c->h_tb_meta.size() - off;
   }
   c->prepared = true;
 }
@@ -1149,6 +1222,8 @@ size_t layout(mmf_ctx* c, char* base) {
   tm.hout_node = (const int*)at(L.take(c->h_hout_node.size() * 4 + 4));
   tm.in_hidx = (const int*)at(L.take(A * 4));
   tm.out_hidx = (const int*)at(L.take(A * 4));
+  c->d_tb_desc = (const int*)at(L.take(c->h_tb_desc.size() * 4 + 16));
+  c->d_tb_meta = (const int*)at(L.take(c->h_tb_meta.size() * 4 + 16));
   tm.cnt = (int*)at(L.take(nt * 4));
   c->wc.cnt = (int*)at(L.take(((size_t)c->N + 1) * 4));
   tm.part = at(L.take(A * (size_t)c->nch * sm));
@@ -1474,6 +1549,21 @@ template <class T_> struct Eng {
   static bool tiled_bwd_launch(mmf_ctx* c, cudaStream_t s, int t) {
     LaunchScope ls(c, K_BWD, s);
     if constexpr (sizeof(M) == 4) {
+      if (c->tile_bwd) {
+        TileCfg tc = c->tbc;
+        tc.tile_ptr = c->tm.tile_ptr;
+        tc.hout_ptr = c->tm.hout_ptr;
+        tc.hout_node = c->tm.hout_node;
+        tc.out_hidx = c->tm.out_hidx;
+        tc.desc = c->d_tb_desc;
+        tc.meta = c->d_tb_meta;
+        const int SW = 32 * c->tb_cpt;
+        const unsigned grid = (unsigned)std::min(tc.nitems, c->sms);
+        const size_t sm = tb_smem(tc.nst, tc.H, SW, tc.MA, tc.MB);
+        if (c->tb_cpt == 8) k_bwd_tile2<8><<<grid, TB_THREADS, sm, s>>>(lay(c, t), tc, t);
+        else k_bwd_tile2<4><<<grid, TB_THREADS, sm, s>>>(lay(c, t), tc, t);
+        return true;
+      }
       if (c->win_bwd) {
         const WinCfg& w = c->wcb;
         const unsigned grid = (unsigned)(w.ns * w.nseg);
@@ -1706,6 +1796,14 @@ template <class T_> struct Eng {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
     if constexpr (sizeof(M) == 4) {
+      if (c->tile_bwd) {
+        const int sm = (int)tb_smem(c->tbc.nst, c->tbc.H, 32 * c->tb_cpt, c->tbc.MA, c->tbc.MB);
+        CU(cudaFuncSetAttribute(k_bwd_tile2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        CU(cudaFuncSetAttribute(k_bwd_tile2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        if (getenv("MMF_VERBOSE"))
+          fprintf(stderr, "[mmf] tile bwd: cpt %d stages %d H %d tiles %d items %d smem %d\n", c->tb_cpt, c->tbc.nst,
+                  c->tbc.H, c->ntiles, c->tbc.nitems, sm);
+      }
       if (c->pipe_bwd) {
         const int sm = (int)pipe_smem(c->pb.R, c->pb.SD, c->pb.D, c->pb.SW).total;
         CU(cudaFuncSetAttribute(k_bwd_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -2026,6 +2124,10 @@ mmf_status finalize(mmf_ctx* ctx) {
       CU(cudaMemcpyAsync((void*)tm.hout_node, c->h_hout_node.data(), c->h_hout_node.size() * 4, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync((void*)tm.in_hidx, c->h_in_hidx.data(), A * 4, cudaMemcpyHostToDevice, s));
     CU(cudaMemcpyAsync((void*)tm.out_hidx, c->h_out_hidx.data(), A * 4, cudaMemcpyHostToDevice, s));
+    if (!c->h_tb_desc.empty())
+      CU(cudaMemcpyAsync((void*)c->d_tb_desc, c->h_tb_desc.data(), c->h_tb_desc.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!c->h_tb_meta.empty())
+      CU(cudaMemcpyAsync((void*)c->d_tb_meta, c->h_tb_meta.data(), c->h_tb_meta.size() * 4, cudaMemcpyHostToDevice, s));
     CU(cudaMemsetAsync(tm.cnt, 0, nt * 4, s));
     CU(cudaMemsetAsync(c->wc.cnt, 0, ((size_t)c->N + 1) * 4, s));
   }
@@ -2385,7 +2487,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order" || k == "pexch") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order" || k == "pexch" || k == "tbwd") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -2421,6 +2523,10 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_wrap = (int)value;
     }
     if (k == "l2hint") ctx->opt_l2hint = value != 0;
+    if (k == "tbwd") {
+      if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "tbwd must be -1 (auto), 0 or 1");
+      ctx->opt_tbwd = (int)value;
+    }
     if (k == "pexch") {
       if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "pexch must be -1 (auto), 0 or 1");
       ctx->opt_pexch = (int)value;

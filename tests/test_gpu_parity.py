@@ -857,3 +857,16 @@ def test_virtual_ranks_pipelined_exchange(L, G, marg, opts):
     Fo, Wo, _ = run_oracle(p, 4)
     assert max_rel_err(F, Fo, flow_floor(p)) < TOL["fp32"] and max_rel_err(Ws[0], Wo, W_FLOOR) < TOL["fp32"]
     assert np.min(Wo) < 0.99
+
+
+# ---------------------------------------------------------------------------------------------
+# node-tile backward with staged out-halos (option tbwd)
+
+@pytest.mark.parametrize("L,opts", [(1019, dict(tbwd=1)), (1019, dict(tbwd=1, tile=64)), (300, dict(tbwd=1)),
+                                    (2051, dict(tbwd=1, tile=16))])
+def test_tile_backward_parity(L, opts):
+    """The tile backward (BFS node tiles, out-halo rows staged per (tile, chunk) by TMA, consumers from shared
+    memory) against the live oracle, with the hub / empty-item graph (high out-degree: arc batches of 32)."""
+    assert_parity(_hub_problem(L, 22), 3, "fp32", options=opts)
+    p = grid_problem(14, 14, 8, L, 0.1, seed=61, cap=(0.3 * L / 100, 1.2 * L / 100))
+    assert_parity(p, 3, "fp32", options=opts)
