@@ -183,7 +183,11 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "tbwd"     backward on node tiles (BFS blobs of "tile" nodes whose out-halo stays within "halo" rows; the halo
  *              rows of a (tile, commodity chunk) staged once by TMA, the tile's nodes computed from shared memory):
  *              1 on, 0 off, -1 auto (default: fp32, L >= 256 and mean degree >= 7, e.g. BJ [3] and [5]); it sets
- *              the node order to the tile order */
+ *              the node order to the tile order
+ *   "tfwd"     forward on the same node tiles (alpha_t and the flow partials of step t per (tile, 128-commodity chunk)
+ *              from staged in- and out-halo rows, then a fixed-order chunk sum and the dual update): 1 on, 0 off
+ *              (default; measured slower than the wide-lane forward on [5]), -1 where the pipelined forward does not
+ *              apply; single rank, no node capacities */
 mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value);
 
 /* W = 1, UT = 1 on supp(muT), one backward pass (Alg. 2 "Initialize").  Async. */

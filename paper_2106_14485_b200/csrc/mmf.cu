@@ -135,6 +135,15 @@ struct mmf_ctx {
                         // 7.7; [4], degree 4.8, 71 vs 31)
   bool tile_bwd = false;
   TileCfg tbc{};
+  int opt_tfwd = 0;     // forward on node tiles (k_fwd_tile2 + k_tile_dual, with the tile backward's tiles): 1 on, 0 off
+                        // (default: measured slower than the wide-lane forward on [5], 77.5 vs 67.2 ms/sweep), -1 where
+                        // the tile backward runs and the pipelined forward does not apply
+  bool tile_fwd = false;
+  TileCfgF tfc{};
+  std::vector<int> h_tf_desc, h_tf_meta;
+  const int* d_tf_desc = nullptr;
+  const int* d_tf_meta = nullptr;
+  float* d_tf_part = nullptr;
   int tb_cpt = 4;
   int opt_pexch = -1;   // multi-GPU / virtual-rank Gauss-Seidel exchange on the pipelined kernels: 1 on, 0 off (wide-lane
                         // two-pass), -1 auto = 1024-commodity slices (measured on [4]: 92 vs 115 ms/sweep at L = 1024, but
@@ -563,6 +572,29 @@ void derive_shapes(mmf_ctx* c) {
       c->tbc.MB = MB;
       c->tbc.nch = c->Lp / SW;
       c->tbc.nitems = c->ntiles * c->tbc.nch;
+    }
+  }
+  // tile forward (option tfwd): stages of the in- and out-halo rows x 128 commodities + records + metadata
+  c->tile_fwd = false;
+  if (c->tile_bwd && c->opt_tfwd != 0 && (c->opt_tfwd > 0 || !c->pipe_fwd) && c->node_cap.empty() && c->Lp % 128 == 0) {
+    const size_t budget = 226 * 1024;
+    int MM = 0, MAi = 0;
+    for (int k = 0; k < c->ntiles; ++k) {
+      MM = std::max(MM, c->h_tf_desc[(size_t)k * 16 + 11]);
+      MAi = std::max(MAi, c->h_tf_desc[(size_t)k * 16 + 3]);
+    }
+    int nst = 1;
+    while (nst < 4 && tf_smem(nst + 1, c->max_hin, c->max_hout, 128, MAi, c->max_oa, MM) <= budget) ++nst;
+    if (nst >= 2) {
+      c->tile_fwd = true;
+      c->tfc.nst = nst;
+      c->tfc.Hin = c->max_hin;
+      c->tfc.Hout = c->max_hout;
+      c->tfc.MAi = MAi;
+      c->tfc.MAo = c->max_oa;
+      c->tfc.MM = MM;
+      c->tfc.nch = c->Lp / 128;
+      c->tfc.nitems = c->ntiles * c->tfc.nch;
     }
   }
   c->nch = c->Lp / c->LC;
@@ -1073,6 +1105,8 @@ void prepare(mmf_ctx* c) {
     c->max_hin = c->max_hout = c->max_ia = c->max_oa = 0;
     c->h_tb_desc.clear();
     c->h_tb_meta.clear();
+    c->h_tf_desc.clear();
+    c->h_tf_meta.clear();
     c->prepared = true;
     return;
   }
@@ -1135,6 +1169,32 @@ void prepare(mmf_ctx* c) {
     d[5] = c->h_hout_ptr[k + 1] - c->h_hout_ptr[k];
     d[6] = off;
     d[7] = (int)c->h_tb_meta.size() - off;
+  }
+  // tile forward: per tile 16 ints {v0, nv, qi0, nai, qo0, nao, hin0, nhin, hout0, nhout, moff, mn, o_inidx, o_outptr,
+  // o_outidx, 0} and the block [nv + 1 in offsets | in-halo indices | nv + 1 out offsets | out-halo indices]
+  c->h_tf_desc.assign((size_t)c->ntiles * 16, 0);
+  c->h_tf_meta.clear();
+  auto pad4 = [&]() { while (c->h_tf_meta.size() % 4) c->h_tf_meta.push_back(0); };
+  for (int k = 0; k < c->ntiles; ++k) {
+    const int v0 = c->h_tile_ptr[k], v1 = c->h_tile_ptr[k + 1];
+    const int qi0 = c->h_inptr[v0], qi1 = c->h_inptr[v1], qo0 = c->h_outptr[v0], qo1 = c->h_outptr[v1];
+    const int off = (int)c->h_tf_meta.size();
+    for (int v = v0; v <= v1; ++v) c->h_tf_meta.push_back(c->h_inptr[v] - qi0);
+    pad4();
+    const int o_inidx = (int)c->h_tf_meta.size() - off;
+    for (int q = qi0; q < qi1; ++q) c->h_tf_meta.push_back(c->h_in_hidx[q]);
+    pad4();
+    const int o_outptr = (int)c->h_tf_meta.size() - off;
+    for (int v = v0; v <= v1; ++v) c->h_tf_meta.push_back(c->h_outptr[v] - qo0);
+    pad4();
+    const int o_outidx = (int)c->h_tf_meta.size() - off;
+    for (int q = qo0; q < qo1; ++q) c->h_tf_meta.push_back(c->h_out_hidx[q]);
+    pad4();
+    int* d = &c->h_tf_desc[(size_t)k * 16];
+    const int dv[16] = {v0, v1 - v0, qi0, qi1 - qi0, qo0, qo1 - qo0, c->h_hin_ptr[k], c->h_hin_ptr[k + 1] - c->h_hin_ptr[k],
+                        c->h_hout_ptr[k], c->h_hout_ptr[k + 1] - c->h_hout_ptr[k], off, (int)c->h_tf_meta.size() - off,
+                        o_inidx, o_outptr, o_outidx, 0};
+    std::copy(dv, dv + 16, d);
   }
   c->prepared = true;
 }
@@ -1224,6 +1284,9 @@ size_t layout(mmf_ctx* c, char* base) {
   tm.out_hidx = (const int*)at(L.take(A * 4));
   c->d_tb_desc = (const int*)at(L.take(c->h_tb_desc.size() * 4 + 16));
   c->d_tb_meta = (const int*)at(L.take(c->h_tb_meta.size() * 4 + 16));
+  c->d_tf_desc = (const int*)at(L.take(c->h_tf_desc.size() * 4 + 16));
+  c->d_tf_meta = (const int*)at(L.take(c->h_tf_meta.size() * 4 + 16));
+  c->d_tf_part = c->tile_fwd ? (float*)at(L.take((size_t)A * c->tfc.nch * 4)) : nullptr;
   tm.cnt = (int*)at(L.take(nt * 4));
   c->wc.cnt = (int*)at(L.take(((size_t)c->N + 1) * 4));
   tm.part = at(L.take(A * (size_t)c->nch * sm));
@@ -1604,6 +1667,27 @@ template <class T_> struct Eng {
     else wide_bwd_cpt<is_f32() ? 8 : 2>(c, s, t);
     return false;
   }
+  // node-tile forward launch t (alpha_t, flow partials of step t or a4) and, t < T, the dual update of step t
+  static void tile_fwd_step(mmf_ctx* c, cudaStream_t s, int t) {
+    if constexpr (sizeof(M) == 4) {
+      TileCfgF tc = c->tfc;
+      tc.desc = c->d_tf_desc;
+      tc.meta = c->d_tf_meta;
+      tc.hin_node = c->tm.hin_node;
+      tc.hout_node = c->tm.hout_node;
+      tc.part = c->d_tf_part;
+      {
+        LaunchScope ls(c, K_FUSED, s);
+        const unsigned grid = (unsigned)std::min(tc.nitems, c->sms);
+        k_fwd_tile2<4><<<grid, TB_THREADS, tf_smem(tc.nst, tc.Hin, tc.Hout, 128, tc.MAi, tc.MAo, tc.MM), s>>>(
+            lay(c, t), tc, t);
+      }
+      if (t < c->T) {
+        LaunchScope ls(c, K_UPDATE, s);
+        k_tile_dual<<<(unsigned)((c->A + 255) / 256), 256, 0, s>>>(c->dp, tc.part, tc.nch, t);
+      }
+    }
+  }
   // the multi-GPU exchange of one forward step: all-reduce the rank-partial F_t, then W_t update
   // the exchange path runs on the pipelined kernels (fp32, one slice per node) unless option pexch = 0
   static bool pipe_exchange(const mmf_ctx* c) {
@@ -1688,6 +1772,21 @@ template <class T_> struct Eng {
         for (int t = 0; t <= c->T; ++t) {
           pipe_fwd(c, s, t);  // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
           node_cap(c, s, t);  // (node capacities: u_t, P:1093 on the states)
+        }
+      }
+      if (do_bwd) {
+        Nvtx r("backward pass (a5)");
+        for (int t = c->T - 1; t >= 0; --t) tiled_bwd(c, s, t);  // a5
+      }
+      return MMF_OK;
+    }
+    if (c->tile_fwd && !c->comm) {  // node-tile forward: launch t = alpha_t + flow partials of step t, then its dual
+      {
+        Nvtx r("forward pass (a2, a3 on node tiles, a4)");
+        tiled_fwd(c, s, 0, 0);  // a2 + flows + dual update of step 0 (wide-lane launch)
+        for (int t = 1; t <= c->T; ++t) {
+          tile_fwd_step(c, s, t);
+          node_cap(c, s, t);
         }
       }
       if (do_bwd) {
@@ -1796,6 +1895,13 @@ template <class T_> struct Eng {
     mmf_ctx* c = ctx;
     const DevPtrs& p = c->dp;
     if constexpr (sizeof(M) == 4) {
+      if (c->tile_fwd) {
+        const int sm = (int)tf_smem(c->tfc.nst, c->tfc.Hin, c->tfc.Hout, 128, c->tfc.MAi, c->tfc.MAo, c->tfc.MM);
+        CU(cudaFuncSetAttribute(k_fwd_tile2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        if (getenv("MMF_VERBOSE"))
+          fprintf(stderr, "[mmf] tile fwd: stages %d Hin %d Hout %d items %d smem %d\n", c->tfc.nst, c->tfc.Hin,
+                  c->tfc.Hout, c->tfc.nitems, sm);
+      }
       if (c->tile_bwd) {
         const int sm = (int)tb_smem(c->tbc.nst, c->tbc.H, 32 * c->tb_cpt, c->tbc.MA, c->tbc.MB);
         CU(cudaFuncSetAttribute(k_bwd_tile2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
@@ -2128,6 +2234,10 @@ mmf_status finalize(mmf_ctx* ctx) {
       CU(cudaMemcpyAsync((void*)c->d_tb_desc, c->h_tb_desc.data(), c->h_tb_desc.size() * 4, cudaMemcpyHostToDevice, s));
     if (!c->h_tb_meta.empty())
       CU(cudaMemcpyAsync((void*)c->d_tb_meta, c->h_tb_meta.data(), c->h_tb_meta.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!c->h_tf_desc.empty())
+      CU(cudaMemcpyAsync((void*)c->d_tf_desc, c->h_tf_desc.data(), c->h_tf_desc.size() * 4, cudaMemcpyHostToDevice, s));
+    if (!c->h_tf_meta.empty())
+      CU(cudaMemcpyAsync((void*)c->d_tf_meta, c->h_tf_meta.data(), c->h_tf_meta.size() * 4, cudaMemcpyHostToDevice, s));
     CU(cudaMemsetAsync(tm.cnt, 0, nt * 4, s));
     CU(cudaMemsetAsync(c->wc.cnt, 0, ((size_t)c->N + 1) * 4, s));
   }
@@ -2487,7 +2597,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order" || k == "pexch" || k == "tbwd") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order" || k == "pexch" || k == "tbwd" || k == "tfwd") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -2523,6 +2633,10 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_wrap = (int)value;
     }
     if (k == "l2hint") ctx->opt_l2hint = value != 0;
+    if (k == "tfwd") {
+      if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "tfwd must be -1 (auto), 0 or 1");
+      ctx->opt_tfwd = (int)value;
+    }
     if (k == "tbwd") {
       if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "tbwd must be -1 (auto), 0 or 1");
       ctx->opt_tbwd = (int)value;

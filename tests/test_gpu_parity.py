@@ -870,3 +870,15 @@ def test_tile_backward_parity(L, opts):
     assert_parity(_hub_problem(L, 22), 3, "fp32", options=opts)
     p = grid_problem(14, 14, 8, L, 0.1, seed=61, cap=(0.3 * L / 100, 1.2 * L / 100))
     assert_parity(p, 3, "fp32", options=opts)
+
+
+@pytest.mark.parametrize("L,opts", [(2051, dict(tbwd=1, tfwd=1)), (1019, dict(tbwd=1, tfwd=1)),
+                                    (600, dict(tbwd=1, tfwd=1, tile=16))])
+def test_tile_forward_parity(L, opts):
+    """The node-tile forward (alpha_t and the flow partials of step t per (tile, 128-commodity chunk) from staged in-
+    and out-halo rows, fixed-order chunk sum and dual update per step) against the live oracle: a grid with a ragged
+    commodity tail, the hub / empty-item graph, and commodity node costs (the layer factor applied before the flows)."""
+    p = grid_problem(14, 14, 8, L, 0.1, seed=63, cap=(0.3 * L / 100, 1.2 * L / 100))
+    assert_parity(p, 3, "fp32", options=opts)
+    assert_parity(_hub_problem(L, 22), 3, "fp32", options=opts)
+    assert_parity(_node_cost(p, 0.05, seed=7), 3, "fp32", options=opts)
