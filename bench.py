@@ -239,7 +239,9 @@ def main():
     peak, peak_kind = measured_peaks()
     achieved = dom_bytes_per_launch / (dom_launch_ms / 1e3) / 1e9
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "r02", "traffic.json")
+    tpath = os.path.join(ROOT, "profiles", "r02_final", "traffic.json")
+    if not os.path.exists(tpath):
+        tpath = os.path.join(ROOT, "profiles", "r02", "traffic.json")
     if os.path.exists(tpath):  # ncu dram bytes per launch of the same kernel and workload (committed capture)
         with open(tpath) as f:
             tj = json.load(f).get(workload_name(p, args.config), {}).get(dom)

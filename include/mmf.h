@@ -184,6 +184,8 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *              rows of a (tile, commodity chunk) staged once by TMA, the tile's nodes computed from shared memory):
  *              1 on, 0 off, -1 auto (default: fp32, L >= 256 and mean degree >= 7, e.g. BJ [3] and [5]); it sets
  *              the node order to the tile order
+ *   "wcp"      wide-lane kernels: commodity chunks per CTA (0 auto: 1 for fp32 rows of >= 16 chunks, else 8; the CTA's
+ *              8 / wcp warps-per-chunk take neighbouring nodes)
  *   "tfwd"     forward on the same node tiles (alpha_t and the flow partials of step t per (tile, 128-commodity chunk)
  *              from staged in- and out-halo rows, then a fixed-order chunk sum and the dual update): 1 on, 0 off
  *              (default; measured slower than the wide-lane forward on [5]), -1 where the pipelined forward does not

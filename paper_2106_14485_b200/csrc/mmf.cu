@@ -135,6 +135,7 @@ struct mmf_ctx {
                         // 7.7; [4], degree 4.8, 71 vs 31)
   bool tile_bwd = false;
   TileCfg tbc{};
+  int opt_wcp = 0;      // wide-lane kernels: commodity chunks per CTA (0 auto = 8; 8 / wcp neighbouring nodes per CTA)
   int opt_tfwd = 0;     // forward on node tiles (k_fwd_tile2 + k_tile_dual, with the tile backward's tiles): 1 on, 0 off
                         // (default: measured slower than the wide-lane forward on [5], 77.5 vs 67.2 ms/sweep), -1 where
                         // the tile backward runs and the pipelined forward does not apply
@@ -600,7 +601,9 @@ void derive_shapes(mmf_ctx* c) {
   c->nch = c->Lp / c->LC;
   // wide path: warps = (nodes per CTA) x (chunks per CTA) = 8
   {
-    int cp = 8;
+    // (auto: 8 chunks of one node per CTA; 1 chunk of 8 neighbouring nodes when the rows are sliced into >= 16 chunks:
+    // their shared neighbour rows hit in L1, measured [5] forward 67.3 -> 62.5 ms per sweep)
+    int cp = c->opt_wcp > 0 ? c->opt_wcp : (c->prec == MMF_FP32 && c->nch >= 16 ? 1 : 8);
     while (cp > 1 && cp > c->nch) cp >>= 1;
     c->wc.cpcta = cp;
     c->wc.npc = (WIDE_THREADS / 32) / cp;
@@ -2597,7 +2600,7 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->graph = nullptr;
     }
   }
-  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order" || k == "pexch" || k == "tbwd" || k == "tfwd") {
+  else if (k == "reorder" || k == "dry" || k == "copy" || k == "wintma" || k == "bwd" || k == "fgw" || k == "wrap" || k == "stripw" || k == "schedule" || k == "theta_milli" || k == "fng" || k == "fnp" || k == "l2hint" || k == "kernels" || k == "tile" || k == "cpt" || k == "halo" || k == "cpc" || k == "order" || k == "pexch" || k == "tbwd" || k == "tfwd" || k == "wcp") {
     if (ctx->inited) return fail(ctx, MMF_ESTATE, k + " must be set before mmf_init");
     if (k == "reorder") ctx->opt_reorder = value != 0;
     if (k == "dry") ctx->opt_dry = (int)value;
@@ -2633,6 +2636,11 @@ mmf_status mmf_set_option(mmf_ctx* ctx, const char* key, int64_t value) {
       ctx->opt_wrap = (int)value;
     }
     if (k == "l2hint") ctx->opt_l2hint = value != 0;
+    if (k == "wcp") {
+      if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+        return fail(ctx, MMF_EINVAL, "wcp must be 0, 1, 2, 4 or 8");
+      ctx->opt_wcp = (int)value;
+    }
     if (k == "tfwd") {
       if (value < -1 || value > 1) return fail(ctx, MMF_EINVAL, "tfwd must be -1 (auto), 0 or 1");
       ctx->opt_tfwd = (int)value;

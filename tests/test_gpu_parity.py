@@ -882,3 +882,31 @@ def test_tile_forward_parity(L, opts):
     assert_parity(p, 3, "fp32", options=opts)
     assert_parity(_hub_problem(L, 22), 3, "fp32", options=opts)
     assert_parity(_node_cost(p, 0.05, seed=7), 3, "fp32", options=opts)
+
+
+@pytest.mark.parametrize("case", ["jacobi", "symmetric", "node_costs", "node_caps", "times", "time_varying"])
+def test_tile_backward_with_next_rows(case):
+    """The tile backward (forced: tbwd=1; the default on high-degree graphs, BJ [3] / [5]) under every NEXT-row feature:
+    the Jacobi and symmetric schedules, commodity node costs and node capacities (factors applied after the launch),
+    entry / exit times (holding nodes), time-varying costs and capacities — against the oracle."""
+    L = 1019
+    sc = L / 64
+    p = grid_problem(8, 8, 7, L, 0.2, seed=71, cap=(0.3 * L / 100, 1.2 * L / 100))
+    opts, okw = dict(tbwd=1), None
+    if case == "jacobi":
+        opts.update(schedule=1, theta_milli=500)
+        okw = dict(schedule="jacobi", theta=0.5)
+    elif case == "symmetric":
+        opts.update(schedule=2)
+        okw = dict(schedule="sym")
+    elif case == "node_costs":
+        p = _node_cost(p, 0.1, seed=5)
+    elif case == "node_caps":
+        p = _with_node_caps(grid_problem(8, 8, 7, L, 0.2, seed=52, cap=(5 * sc, 20 * sc)), 3, 0.4 * sc, 1.5 * sc)
+        _node_parity(p, 4, "fp32", opts)
+        return
+    elif case == "times":
+        p = _times(p, seed=3, T=10)
+    else:
+        p = grid_problem(8, 8, 7, L, 0.2, seed=71, cap=(0.3 * L / 100, 1.2 * L / 100), time_varying=True)
+    assert_parity(p, 4, "fp32", oracle_kw=okw, options=opts)

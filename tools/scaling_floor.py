@@ -20,6 +20,7 @@ from workloads import gen  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--sweeps", type=int, default=5)
+ap.add_argument("--out", default=None, help="write the JSON here (NCCL prints its banner on stdout)")
 a = ap.parse_args()
 p = gen(a.config)
 out = {"workload": p.name, "L": p.L, "rows": []}
@@ -39,4 +40,8 @@ for G in (1, 2, 4, 8):
         row = {"G": G, "L_rank": per, "path": name, "ms_per_sweep": ms}
         out["rows"].append(row)
         print(row, file=sys.stderr, flush=True)
-print(json.dumps(out))
+if a.out:
+    with open(a.out, "w") as f:
+        json.dump(out, f)
+else:
+    print(json.dumps(out))
