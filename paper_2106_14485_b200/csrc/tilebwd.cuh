@@ -22,7 +22,10 @@
 
 namespace mmf {
 
-constexpr int TB_NWC = 16;                     // consumer warps per CTA
+#ifndef MMF_TB_NWC
+#define MMF_TB_NWC 16
+#endif
+constexpr int TB_NWC = MMF_TB_NWC;             // consumer warps per CTA
 constexpr int TB_THREADS = (TB_NWC + 1) * 32;  // + one producer warp
 
 struct TileCfg {
