@@ -153,9 +153,10 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "profile"  1 = per-kernel CUDA-event timing for mmf_read_kernel_stats (any time)
  *   "prefetch" 1 = L2 prefetch hints in the wide-lane kernels (any time; recaptures the graph)
  *   "reorder"  1 = locality node reordering (default 1)
- *   "kernels"  kernel family 1..6 (default 6 = TMA-pipelined forward (2 pipelines / CTA) and
- *              backward (3 pipelines / CTA); 5 single-pipeline; 4 register head-flow; 3 wide-lane;
- *              2 smem node tiles; 1 per-node reference kernels)
+ *   "kernels"  kernel family 1, 3..6 (default 6 = TMA-pipelined forward (2 pipelines / CTA) and
+ *              backward (3 pipelines / CTA), node-tile backward on high-degree graphs ("tbwd"); 5 single-pipeline;
+ *              4 register head-flow; 3 wide-lane; 1 per-node reference kernels; 2 (the round-1 node tiles) was
+ *              removed -> MMF_EINVAL)
  *   "bwd"      backward kernel with kernels >= 5: 0 auto, 1 three-pipeline, 2 sliding window, 3 single
  *   "schedule" 0 = Gauss-Seidel (Algorithm 2, default), 1 = damped Jacobi (every W_t from
  *              one alpha/beta pair, W <- W^(1-theta) min(W d / F, 1)^theta; one all-reduce of the T x n_arcs
@@ -166,7 +167,7 @@ mmf_status mmf_nccl_unique_id(void* out128);
  *   "fgw", "fng", "fnp"  pipelined forward: warps per consumer group (8, 4, 2), groups per pipeline,
  *              pipelines per CTA (0 = default; the compiled combinations are listed in pipefwd.cuh)
  *   "wintma"   window backward row blocks by 2-D tensor TMA (1) or cp.async (0)
- *   "order"    node order: kernels 2..5: 0 input, 1 reverse Cuthill-McKee, 2 BFS tiles (default); kernels 6:
+ *   "order"    node order: kernels 3..5: 0 input, 1 reverse Cuthill-McKee, 2 BFS tiles (default); kernels 6:
  *              1 RCM, 3 the window kernel's cost model, 4 most neighbour overlap between consecutive nodes even where
  *              the pipelined kernels do not apply; default (other values): most neighbour overlap for fp32 with
  *              L >= 256 (the pipelined kernels), the window cost model otherwise (fp64, L < 256) and with bwd=2
