@@ -34,7 +34,10 @@ struct WideCfg {
   int prefetch;  // 1: pass 1 also prefetches the significand rows into L1
 };
 
-constexpr int WIDE_THREADS = 256;
+#ifndef MMF_WIDE_THREADS
+#define MMF_WIDE_THREADS 256
+#endif
+constexpr int WIDE_THREADS = MMF_WIDE_THREADS;  // (warps per CTA = nodes x chunks per CTA)
 constexpr int WARP_ARCS = 64;  // arcs per warp scratch batch
 #ifndef MMF_U1
 #define MMF_U1 4  // unroll of the exponent pass (loads in flight per warp)
