@@ -1769,12 +1769,13 @@ template <class T_> struct Eng {
 
   // Algorithm 2's sweep (a2, forward with the W updates, a4, and the backward pass a5 when do_bwd)
   static mmf_status gs_sweep(mmf_ctx* c, cudaStream_t s, bool do_bwd) {
-    if (c->opt_kernels >= 5 && c->pipe_fwd && !c->comm) {
+    if (c->tile_fwd && !c->comm) {  // node-tile forward: launch t = alpha_t + flow partials of step t, then its dual
       {
-        Nvtx r("forward pass (a2, a3, a4)");
-        for (int t = 0; t <= c->T; ++t) {
-          pipe_fwd(c, s, t);  // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
-          node_cap(c, s, t);  // (node capacities: u_t, P:1093 on the states)
+        Nvtx r("forward pass (a2, a3 on node tiles, a4)");
+        tiled_fwd(c, s, 0, 0);  // a2 + flows + dual update of step 0 (wide-lane launch)
+        for (int t = 1; t <= c->T; ++t) {
+          tile_fwd_step(c, s, t);
+          node_cap(c, s, t);
         }
       }
       if (do_bwd) {
@@ -1783,13 +1784,12 @@ template <class T_> struct Eng {
       }
       return MMF_OK;
     }
-    if (c->tile_fwd && !c->comm) {  // node-tile forward: launch t = alpha_t + flow partials of step t, then its dual
+    if (c->opt_kernels >= 5 && c->pipe_fwd && !c->comm) {
       {
-        Nvtx r("forward pass (a2, a3 on node tiles, a4)");
-        tiled_fwd(c, s, 0, 0);  // a2 + flows + dual update of step 0 (wide-lane launch)
-        for (int t = 1; t <= c->T; ++t) {
-          tile_fwd_step(c, s, t);
-          node_cap(c, s, t);
+        Nvtx r("forward pass (a2, a3, a4)");
+        for (int t = 0; t <= c->T; ++t) {
+          pipe_fwd(c, s, t);  // a2 in t = 0; a3 (W_{t-1}, alpha_t); a4 in t = T
+          node_cap(c, s, t);  // (node capacities: u_t, P:1093 on the states)
         }
       }
       if (do_bwd) {
