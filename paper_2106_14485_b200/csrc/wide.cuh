@@ -50,6 +50,13 @@ constexpr int kUnroll2 = MMF_U2;
 #ifndef MMF_WIDE_MINB
 #define MMF_WIDE_MINB 3  // CTAs per SM the register budget is sized for
 #endif
+#ifndef MMF_WIDE_MINB_F32X8
+#define MMF_WIDE_MINB_F32X8 4  // ... for the fp32, 8-commodity-per-lane forward ([5]): 64 registers, 32 warps per SM
+                               // (measured 62.5 -> 58.1 ms per sweep on [5]; the latency-bound gathers want warps)
+#endif
+template <class T_, int CPT> constexpr int wide_fwd_minb() {
+  return sizeof(typename T_::M) == 4 && CPT == 8 ? MMF_WIDE_MINB_F32X8 : MMF_WIDE_MINB;
+}
 
 // compacted per-warp arc list: gathered node, K W factor, position of the arc (flow slot)
 template <class M> struct WarpArcs {
@@ -199,7 +206,7 @@ __device__ __forceinline__ void node_sum(const ArcKW<typename T_::M>* rec, int k
 // MODE 0: t = 0 (a2 fused, or U0 reload in readout); MODE 1: 0 < t < T; MODE 2: t = T (a4 fused)
 // FMODE: 0 dual update in place, 1 write Fsum (multi-GPU), 2 readout (Fout[t], all arcs)
 template <class T_, int CPT, int MODE, int FMODE>
-__global__ void __launch_bounds__(WIDE_THREADS, MMF_WIDE_MINB) k_fwd_wide(DevPtrs p, WideCfg wc, int t) {
+__global__ void __launch_bounds__(WIDE_THREADS, wide_fwd_minb<T_, CPT>()) k_fwd_wide(DevPtrs p, WideCfg wc, int t) {
   typedef typename T_::M M;
   typedef typename T_::E E;
   constexpr int LC = 32 * CPT;
