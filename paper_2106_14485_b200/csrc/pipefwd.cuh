@@ -466,7 +466,11 @@ __device__ __forceinline__ void beta_lin(const Row<TrF32, CPT>& b, const XPre<CP
   if constexpr (CPT % 2 == 0) {  // two at a time: biased exponent e + E + 127 clamped to [0, 254] (0: flushed)
 #pragma unroll
     for (int w = 0; w < CPT / 2; ++w) {
+#if MMF_XPRE_FAST
+      const unsigned es = __vmins2(__viaddmax_s16x2((unsigned)b.w[w], P.Ep2[w], 0u), 0x00fe00feu);  // (XPre::set)
+#else
       const unsigned es = __vmins2(__vmaxs2(__vaddss2((unsigned)b.w[w], P.Ep2[w]), 0u), 0x00fe00feu);
+#endif
       mul2(bl[2 * w], bl[2 * w + 1], b.m[2 * w], b.m[2 * w + 1], __uint_as_float(es << 23),
            __uint_as_float((es >> 16) << 23));
     }

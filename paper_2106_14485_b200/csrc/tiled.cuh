@@ -144,6 +144,32 @@ template <class T_, int CPT, bool FAC = true>
 __device__ __forceinline__ void norm_lane(const DevPtrs& p, const typename T_::M* s, const int* E,
                                           Lane<typename T_::M, typename T_::E, CPT>& out, int l0, int node) {
   typedef typename T_::M M;
+  if constexpr (sizeof(M) == 4 && !FAC) {
+    // (the pipelined epilogues) one range flag per lane and a single rare branch instead of a compare-and-branch
+    // per element; same results: a nonzero element with |e| > ELIM sets ERR_RANGE and is clamped
+    bool bad = false;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const unsigned u = __float_as_uint(s[c]);
+      const int e = E[c] + (int)(u >> 23) - 127;
+      bad |= u != 0u && (unsigned)(e + ELIM) > 2u * ELIM;
+      out.m[c] = u == 0u ? 0.f : __uint_as_float((u & 0x007fffffu) | 0x3f800000u);
+      out.e[c] = (typename T_::E)(u == 0u ? EZERO : e);
+      MMF_DASSERT(node >= 0 && node < p.N && l0 + c < p.Lp);
+    }
+    if (bad) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const unsigned u = __float_as_uint(s[c]);
+        const int e = E[c] + (int)(u >> 23) - 127;
+        if (u != 0u && (e > ELIM || e < -ELIM)) {
+          set_error(p, ERR_RANGE, l0 + c, node);
+          out.e[c] = (typename T_::E)(e > 0 ? ELIM : -ELIM);
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
     M m;

@@ -136,7 +136,7 @@ __device__ __forceinline__ void gather_sum(const typename T_::M* gm, const typen
       for (int j = 0; j < NP; ++j) E2[j] = __viaddmax_s16x2(ew[j], k2, E2[j]);
     }
     XPre<CPT> P;
-    P.set(E2);
+    P.template set<false>(E2);  // (see XPre::set)
 #pragma unroll
     for (int c = 0; c < CPT; ++c) E[c] = P.E[c];
     float acc[CPT];

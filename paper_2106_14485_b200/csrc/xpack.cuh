@@ -59,17 +59,33 @@ template <class T_, int CPT> struct Row {
 #else
 #define MMF_HI23(d2) (((d2)&0xffff0000u) << 7)
 #endif
-template <int CPT> struct XPre {  // per-item constants of a lane: -E and the low clamp E - 32512, packed
+#ifndef MMF_XPRE_FAST
+#define MMF_XPRE_FAST 1
+#endif
+template <int CPT> struct XPre {  // per-item constants of a lane: -E and the low clamp E - 126 (E - 32512 saturated in the emulated form), packed
   unsigned nE2[CPT / 2 > 0 ? CPT / 2 : 1], Lo2[CPT / 2 > 0 ? CPT / 2 : 1], Ep2[CPT / 2 > 0 ? CPT / 2 : 1];
   int nE[CPT];
   int E[CPT];
-  __device__ __forceinline__ void set(const unsigned* E2) {
+  // FAST = false: the emulated saturating form (kept for the register-capped wide-lane kernels, whose allocation
+  // spills more with the native form: 284 vs 188 bytes in the 64-register fp32 forward)
+  template <bool FAST = (MMF_XPRE_FAST != 0)> __device__ __forceinline__ void set(const unsigned* E2) {
     if constexpr (CPT % 2 == 0) {
 #pragma unroll
       for (int w = 0; w < CPT / 2; ++w) {
         nE2[w] = __vneg2(E2[w]);
+        if constexpr (FAST) {
+        // (native VIMNMX / VIADD.16x2 instead of the emulated saturating __vsubss2 / __vaddss2, 6-7 instructions
+        // each; same results) Lo2 = E - 126: the terms' low clamp u = max(e + ke, E - 126) keeps u - E in
+        // [-126, 0] (E >= -32384 whenever a row exists: e >= EZERO, ke >= -ELIM; the floor only guards the
+        // row-less maximum 0x8000, whose terms are never formed).  Ep2 = clamp(E, +-16131) + 127: for a nonzero
+        // beta (|e_b| <= ELIM) e_b + E + 127 clamped to [0, 254] is unchanged by the clamp of E, and
+        // e_b + Ep2 stays inside int16 (beta_lin adds it without saturation)
+        Lo2[w] = __vadd2(__vmaxs2(E2[w], 0x81808180u), 0xff82ff82u);
+        Ep2[w] = __vadd2(__vmins2(__vmaxs2(E2[w], 0xc0fdc0fdu), 0x3f033f03u), 0x007f007fu);
+        } else {
         Lo2[w] = __vsubss2(E2[w], 0x7f007f00u);
         Ep2[w] = __vaddss2(E2[w], 0x007f007fu);  // E + 127 (float exponent bias), saturated
+        }
         E[2 * w] = (int)(short)(E2[w] & 0xffffu);
         E[2 * w + 1] = (int)E2[w] >> 16;
       }
