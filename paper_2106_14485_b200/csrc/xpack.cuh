@@ -49,12 +49,16 @@ template <class T_, int CPT> struct Row {
 // Exponents are handled two per 32-bit word (CPT even): the max of (row exponent + arc exponent) by one
 // VIADDMNMX.S16x2 per pair (exact: |e| <= 16384, |ke| <= 16000); the scale 2^d, d = max(max(e + ke,
 // E - 32512) - E, -126) (no 16-bit wrap) by two more; then K W 2^d by an integer add into the float's
-// exponent field — mod 2^32 the low / high half of d << 23 equals d2 << 23 / (d2 >> 16) << 23 (SHF + LEA).
+// exponent field — mod 2^32 the low / high half of d << 23 equals d2 << 23 / (d2 >> 16) << 23 (PRMT + LEA).
 
 #ifndef MMF_HI_SHF
-#define MMF_HI_SHF 1
+#define MMF_HI_SHF 2
 #endif
-#if MMF_HI_SHF
+#if MMF_HI_SHF == 2
+// (PRMT + LEA: written as a shift, ptxas folds it into SHL + LOP3 + IADD; the byte permute [b2 b3 b2 b3] is
+// opaque to it and its low half is d2's high half, the copy above shifts out)
+#define MMF_HI23(d2) (__byte_perm((d2), 0u, 0x3232) << 23)
+#elif MMF_HI_SHF
 #define MMF_HI23(d2) (((d2) >> 16) << 23)
 #else
 #define MMF_HI23(d2) (((d2)&0xffff0000u) << 7)
