@@ -34,6 +34,9 @@ struct WideCfg {
   int prefetch;  // 1: pass 1 also prefetches the significand rows into L1
 };
 
+#ifndef MMF_WIDE_XFAST
+#define MMF_WIDE_XFAST false  // native 16x2 form of the per-item exponent constants (XPre::set)
+#endif
 #ifndef MMF_WIDE_THREADS
 #define MMF_WIDE_THREADS 256
 #endif
@@ -136,7 +139,7 @@ __device__ __forceinline__ void gather_sum(const typename T_::M* gm, const typen
       for (int j = 0; j < NP; ++j) E2[j] = __viaddmax_s16x2(ew[j], k2, E2[j]);
     }
     XPre<CPT> P;
-    P.template set<false>(E2);  // (see XPre::set)
+    P.template set<MMF_WIDE_XFAST>(E2);  // (see XPre::set)
 #pragma unroll
     for (int c = 0; c < CPT; ++c) E[c] = P.E[c];
     float acc[CPT];

@@ -71,7 +71,8 @@ template <int CPT> struct XPre {  // per-item constants of a lane: -E and the lo
   int nE[CPT];
   int E[CPT];
   // FAST = false: the emulated saturating form (kept for the register-capped wide-lane kernels, whose allocation
-  // spills more with the native form: 284 vs 188 bytes in the 64-register fp32 forward)
+  // spills more with the native form: 284 vs 188 bytes in the 64-register fp32 forward, [5] forward 62.1 vs 58.0 ms
+  // per sweep measured; option MMF_WIDE_XFAST)
   template <bool FAST = (MMF_XPRE_FAST != 0)> __device__ __forceinline__ void set(const unsigned* E2) {
     if constexpr (CPT % 2 == 0) {
 #pragma unroll
